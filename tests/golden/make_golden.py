@@ -1,0 +1,226 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Each fixture stores float32 scene inputs (the reference is fed exactly these
+values, widened to float64), the camera, the mode/config, and the reference's
+outputs: projection stats and SplatBatch, the sorted tile lists
+(``bin_and_sort``), the frame (colour / transmittance / depth) and per-pixel
+blend records.  The files are committed; nothing on the GPU box reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = os.environ.get("SPLATSORT_REF", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import splatsort as S  # noqa: E402
+from splatsort.fixtures import random_cloud  # noqa: E402
+
+from paper_2402_00525_b200 import scenes  # noqa: E402
+
+
+def to_gaussians(arrs):
+    n = len(arrs["opacity"])
+    sh = np.zeros((n, 16, 3))
+    k = arrs["sh"].shape[1]
+    sh[:, :k] = arrs["sh"]
+    return [S.Gaussian3D(mean=arrs["means"][i].astype(np.float64),
+                         rotation=arrs["quats"][i].astype(np.float64),
+                         scale=arrs["scales"][i].astype(np.float64),
+                         opacity=float(arrs["opacity"][i]), sh=sh[i]) for i in range(n)]
+
+
+def from_gaussians(gs):
+    if not gs:
+        return {"means": np.zeros((0, 3), np.float32), "quats": np.zeros((0, 4), np.float32),
+                "scales": np.zeros((0, 3), np.float32), "opacity": np.zeros(0, np.float32),
+                "sh": np.zeros((0, 16, 3), np.float32)}
+    return scenes.to_f32_scene({
+        "means": np.stack([g.mean for g in gs]), "quats": np.stack([g.rotation for g in gs]),
+        "scales": np.stack([g.scale for g in gs]), "opacity": np.array([g.opacity for g in gs]),
+        "sh": np.stack([g.sh for g in gs])})
+
+
+def ball(mean, scale, opacity, rgb, rot=(1, 0, 0, 0)):
+    sh = np.zeros((16, 3))
+    sh[0] = (np.asarray(rgb, dtype=np.float64) - 0.5) / 0.28209479177387814
+    return S.Gaussian3D(mean=mean, rotation=rot, scale=[scale] * 3 if np.isscalar(scale) else scale,
+                        opacity=opacity, sh=sh)
+
+
+def axis_cam(w, h, f=110.0, R=None, pos=None, cx=None, cy=None):
+    return S.Camera(rotation=np.eye(3) if R is None else R,
+                    position=np.zeros(3) if pos is None else pos,
+                    fx=f, fy=f, width=w, height=h, cx=cx, cy=cy)
+
+
+def save(name, arrs, cam, mode, cfg, sh_coeffs=16, rec_pixels=None, store_batch=True):
+    arrs = dict(arrs)
+    arrs["sh"] = np.ascontiguousarray(arrs["sh"][:, :sh_coeffs])
+    gs = to_gaussians(arrs)
+    cfg_d = dict(tile_size=cfg.tile_size, opacity_eps=cfg.opacity_eps,
+                 termination=cfg.termination, alpha_cap=cfg.alpha_cap,
+                 background=[float(v) for v in cfg.background], near=cfg.near,
+                 guard_band=cfg.guard_band, dilation=cfg.dilation,
+                 inv_scale_clamp=cfg.inv_scale_clamp, with_depth=cfg.with_depth,
+                 exact_tile_culling=cfg.exact_tile_culling)
+    mode_d = dict(queue_tail=mode.queue_tail, queue_mid=mode.queue_mid,
+                  queue_head=mode.queue_head, batch_load=mode.batch_load,
+                  batch_mid=mode.batch_mid, batch_head=mode.batch_head,
+                  mid_depth_at_center=mode.mid_depth_at_center)
+    cfg_rec = S.RenderConfig(**{**cfg_d, "capture_records": True})
+    t0 = time.time()
+    frame = S.render(gs, cam, mode, cfg_rec)
+    dt = time.time() - t0
+    batch, pstats = S.project_scene(gs, cam, near=cfg.near, guard=cfg.guard_band,
+                                    dilation=cfg.dilation, inv_scale_clamp=cfg.inv_scale_clamp,
+                                    eps=cfg.opacity_eps)
+    bins = S.bin_and_sort(batch, cam, mode, cfg)
+    gw = -(-cam.width // cfg.tile_size)
+    tile_id = np.concatenate([np.full(len(b), b.tile_y * gw + b.tile_x, np.int32) for b in bins]) \
+        if bins else np.zeros(0, np.int32)
+    splat = np.concatenate([b.splat for b in bins]).astype(np.int32) if bins else np.zeros(0, np.int32)
+    key = np.concatenate([b.key for b in bins]) if bins else np.zeros(0)
+    H, W = cam.height, cam.width
+    if rec_pixels is None:
+        ys, xs = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+        rec_pixels = np.stack([ys.ravel(), xs.ravel()], 1)
+    rec_pixels = np.asarray(rec_pixels, dtype=np.int32)
+    counts = np.array([len(frame.records[y][x]) for y, x in rec_pixels], dtype=np.int32)
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    rs = np.zeros(int(offs[-1]), np.int32)
+    rt = np.zeros(int(offs[-1]), np.float32)
+    ra = np.zeros(int(offs[-1]), np.float32)
+    for i, (y, x) in enumerate(rec_pixels):
+        r = frame.records[y][x]
+        rs[offs[i]:offs[i + 1]] = r.splat
+        rt[offs[i]:offs[i + 1]] = r.depth
+        ra[offs[i]:offs[i + 1]] = r.alpha
+    out = dict(
+        means=arrs["means"], quats=arrs["quats"], scales=arrs["scales"],
+        opacity=arrs["opacity"], sh=arrs["sh"],
+        cam_R=cam.rotation, cam_pos=cam.position,
+        cam_intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy]),
+        cam_size=np.array([cam.width, cam.height], np.int32),
+        cfg_json=np.array(json.dumps(cfg_d)), mode_json=np.array(json.dumps(mode_d)),
+        proj_stats=np.array([pstats[k] for k in ("input", "behind", "guard", "degenerate", "kept")]),
+        source_index=batch.source_index.astype(np.int32),
+        bin_tile=tile_id, bin_splat=splat,
+        color=frame.color.astype(np.float32), transmittance=frame.transmittance.astype(np.float32),
+        color64_absmax=np.array(np.abs(frame.color).max() if frame.color.size else 0.0),
+        rec_pixels=rec_pixels, rec_offsets=offs, rec_splat=rs, rec_t=rt, rec_alpha=ra,
+        ref_seconds=np.array(dt),
+    )
+    if cfg.with_depth:
+        out["depth"] = frame.depth.astype(np.float32)
+    if store_batch:
+        out.update(b_mean2d=batch.mean2d, b_conic=batch.conic, b_color=batch.color,
+                   b_radius=batch.radius, b_inv_cov3=batch.inv_cov3,
+                   b_inv_cov_center=batch.inv_cov_center, bin_key=key)
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: kept={pstats['kept']} entries={len(splat)} tiles={len(bins)} "
+          f"ref={dt:.2f}s -> {os.path.getsize(path) / 1e6:.2f} MB", flush=True)
+
+
+def main(only=None):
+    H = S.Hierarchical()
+    jobs = {}
+
+    # 1. dense random cloud (reference fixture), background + depth
+    def cloud300():
+        gs, cams, _ = random_cloud(300, seed=5)
+        save("cloud300", from_gaussians(gs), cams[0], H,
+             S.RenderConfig(with_depth=True, background=np.array([0.1, 0.2, 0.3])))
+    jobs["cloud300"] = cloud300
+
+    # 2. rotated camera of the same fixture (3 deg yaw), SH degree 3
+    def cloud300_rot():
+        gs, cams, _ = random_cloud(300, seed=6)
+        save("cloud300_rot", from_gaussians(gs), cams[1], H, S.RenderConfig(with_depth=True))
+    jobs["cloud300_rot"] = cloud300_rot
+
+    # 3. shallow scene: <= 4 contributions per ray (test_rasterizer.py:398-412)
+    def shallow():
+        gs = [ball([0.0, 0.0, 2.0], 0.25, 0.6, [0.8, 0.2, 0.2]),
+              ball([0.05, 0.02, 2.5], 0.25, 0.6, [0.2, 0.8, 0.2]),
+              ball([-0.04, 0.03, 3.1], 0.25, 0.6, [0.2, 0.2, 0.8]),
+              ball([0.02, -0.05, 3.7], 0.25, 0.6, [0.7, 0.7, 0.1])]
+        save("shallow", from_gaussians(gs), axis_cam(48, 48), H, S.RenderConfig(with_depth=True))
+    jobs["shallow"] = shallow
+
+    # 4. edge cases: coincident pair (rank tie-break), near/guard/low-opacity culls
+    def edges():
+        gs = [ball([0.0, 0.0, 2.0], 0.1, 0.5, [1.0, 0.0, 0.0]),
+              ball([0.0, 0.0, 2.0], 0.1, 0.5, [0.0, 0.0, 1.0]),
+              ball([0.3, 0.1, 0.1], 0.1, 0.5, [0.0, 1.0, 0.0]),      # behind near plane
+              ball([5.0, 0.0, 2.0], 0.1, 0.5, [0.0, 1.0, 0.0]),      # outside guard band
+              ball([-0.2, 0.2, 2.0], 0.2, 1e-4, [1.0, 1.0, 0.0]),    # below eps
+              ball([0.2, -0.2, 2.5], 0.3, 1.0, [1.0, 1.0, 1.0]),     # alpha cap
+              ball([-0.3, -0.3, 3.0], [0.6, 0.01, 0.01], 0.9, [0.3, 0.6, 0.9],
+                   rot=[0.9238795, 0.0, 0.0, 0.3826834])]           # elongated, rotated
+        save("edges", from_gaussians(gs), axis_cam(37, 29, f=40.0), H,
+             S.RenderConfig(with_depth=True, background=np.array([0.5, 0.5, 0.5])))
+    jobs["edges"] = edges
+
+    # 5. SH degree 3 frustum cloud, rotated + translated camera, off-centre
+    #    principal point, ragged image size (partial tiles and sub-tiles)
+    def sh3_border():
+        arrs = scenes.frustum_cloud(1500, 21, 203, 117, 150.0, z_lo=1.0, z_hi=5.0)
+        arrs["scales"] = arrs["scales"] * 4.0
+        pos = np.array([0.1, -0.05, -0.2])
+        R = scenes.look_at(pos, np.array([0.15, 0.0, 3.0]))
+        cam = axis_cam(203, 117, f=150.0, R=R, pos=pos, cx=97.3, cy=61.9)
+        save("sh3_border", scenes.to_f32_scene(arrs), cam, H, S.RenderConfig(with_depth=True))
+    jobs["sh3_border"] = sh3_border
+
+    # 6. mode variants: mid_depth_at_center, non-default queues, coarse binning
+    def variants():
+        gs, cams, _ = random_cloud(200, seed=11)
+        a = from_gaussians(gs)
+        save("var_center", a, cams[0], S.Hierarchical(mid_depth_at_center=True),
+             S.RenderConfig(with_depth=True))
+        save("var_queues", a, cams[0], S.Hierarchical(queue_tail=96, queue_mid=12, queue_head=8),
+             S.RenderConfig(with_depth=True))
+        save("var_coarse", a, cams[0], H,
+             S.RenderConfig(with_depth=True, exact_tile_culling=False))
+        save("var_q4", a, cams[0], S.Hierarchical(queue_mid=4, queue_head=1),
+             S.RenderConfig(with_depth=True))
+    jobs["variants"] = variants
+
+    # 7. empty scene -> background
+    def empty():
+        save("empty", from_gaussians([]), axis_cam(32, 32), H,
+             S.RenderConfig(background=np.array([0.2, 0.4, 0.6])))
+    jobs["empty"] = empty
+
+    # 8. config #1 (BASELINE.json configs[0]): 10k random Gaussians, SH0, 256^2
+    def c1():
+        sc, cams = scenes.config_scene("C1")
+        rng = np.random.default_rng(123)
+        pix = np.stack([rng.integers(0, 256, 400), rng.integers(0, 256, 400)], 1)
+        save("c1", sc, cams[0], H, S.RenderConfig(with_depth=True), sh_coeffs=1,
+             rec_pixels=pix, store_batch=False)
+    jobs["c1"] = c1
+
+    for name, fn in jobs.items():
+        if only and name not in only:
+            continue
+        fn()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or None)
