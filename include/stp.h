@@ -1,0 +1,173 @@
+/*
+ * stp.h — C ABI of the B200 hierarchical Gaussian-splatting forward renderer.
+ *
+ * Drop-in boundary for the reference's render path
+ *   render(scene, cam, Hierarchical(), cfg) -> FrameOutput
+ *   (/root/reference/pkg/src/splatsort/rasterizer.py:595-698)
+ * with the per-stage seams
+ *   project_scene   gaussian_math.py:323-434     (kernel K1)
+ *   bin_and_sort    rasterizer.py:279-377         (K2 scan, K3 duplicate, K4 sort, K5 ranges)
+ *   render_tile     hierarchy.py:27-219           (K6)
+ *
+ * Plain pointers and sizes only (no torch types).  All array pointers in
+ * StpScene / StpOutputs are DEVICE pointers; StpCamera / StpConfig / StpStats
+ * are host structs passed by pointer.  Every call is asynchronous on the given
+ * cudaStream_t (passed as void*), re-entrant per (workspace, stream) and
+ * deterministic.  No exceptions cross the ABI: every entry point returns a
+ * status code (errors.py:4-13 mapping below).
+ */
+#ifndef STP_H_
+#define STP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STP_ABI_VERSION 1
+
+/* Status codes.  CONFIG -> ConfigError (rasterizer.py:93-117, 196-203),
+ * DATA -> DataError (rasterizer.py:770-771), WORKSPACE_TOO_SMALL -> the host
+ * grows the workspace to StpStats.bin_entries and retries once. */
+enum {
+  STP_OK = 0,
+  STP_ERR_CONFIG = 1,
+  STP_ERR_DATA = 2,
+  STP_ERR_WORKSPACE_TOO_SMALL = 3,
+  STP_ERR_CUDA = 4
+};
+
+/* Scene tensors, drop-in layout of Gaussian3D stacked as in
+ * gaussian_math.py:353-357 (float32, C-contiguous, device memory). */
+typedef struct {
+  const float* means;     /* [n,3] world-space centres                      */
+  const float* quats;     /* [n,4] quaternion w,x,y,z (re-normalised inside) */
+  const float* scales;    /* [n,3] per-axis standard deviations             */
+  const float* opacity;   /* [n]   linear opacity                           */
+  const float* sh;        /* [n,sh_coeffs,3] SH coefficients [k][rgb]       */
+  int64_t n;
+  int32_t sh_coeffs;      /* 1, 4, 9 or 16 (degree 0..3)                    */
+  int32_t reserved;
+} StpScene;
+
+/* Pinhole camera (scene_io.py:84-129): world->view rotation, row-major. */
+typedef struct {
+  double R[9];
+  double pos[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} StpCamera;
+
+/* RenderConfig (rasterizer.py:170-208) + Hierarchical (rasterizer.py:70-87). */
+typedef struct {
+  double eps;               /* opacity_eps, 1/255                          */
+  double termination;       /* 1e-4                                        */
+  double alpha_cap;         /* 0.99                                        */
+  double bg[3];             /* background                                  */
+  double near_plane;        /* 0.2                                         */
+  double guard;             /* 1.3                                         */
+  double dilation;          /* 0.3                                         */
+  double inv_scale_clamp;   /* 1e3                                         */
+  int32_t tile_size;        /* must be 16                                  */
+  int32_t q_tail, q_mid, q_head;   /* queue sizes (64/8/4)                 */
+  int32_t b_load, b_mid, b_head;   /* batches; must be 32/16/4             */
+  int32_t mid_depth_at_center;
+  int32_t with_depth;
+  int32_t exact_culling;    /* exact 16x16 tile culling (default 1)        */
+  int32_t record_cap;       /* per-pixel blend-record capacity, 0 = off    */
+  int32_t flags;            /* STP_FLAG_*                                  */
+} StpConfig;
+
+#define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
+
+/* Output buffers (device).  Colour is HWC float32 composited over the
+ * background (rasterizer.py:680); depth is the unnormalised expected depth
+ * sum(w * t) (hierarchy.py:88).  Records, when record_cap > 0, hold the first
+ * record_cap blended contributions of each pixel in blend order
+ * (hierarchy.py:89-90); rec_splat is the Gaussian (source) index. */
+typedef struct {
+  float* color;          /* [H,W,3]                        */
+  float* transmittance;  /* [H,W]                          */
+  float* depth;          /* [H,W] or NULL                  */
+  int32_t* rec_count;    /* [H,W] or NULL                  */
+  int32_t* rec_splat;    /* [H,W,record_cap]               */
+  float* rec_t;          /* [H,W,record_cap]               */
+  float* rec_alpha;      /* [H,W,record_cap]               */
+  uint8_t* state;        /* [n] per-Gaussian cull state or NULL:
+                            0 kept, 1 behind, 2 guard, 3 degenerate      */
+} StpOutputs;
+
+/* stats dict of rasterizer.py:683-690 (+ projection stats
+ * gaussian_math.py:344) and per-stage device timings in milliseconds. */
+typedef struct {
+  int64_t input, behind, guard, degenerate, kept;
+  int64_t bin_entries;      /* exact-culled (tile, splat) entries          */
+  int64_t tiles;            /* non-empty tiles                             */
+  int64_t nonfinite_pixels;
+  int64_t tie_runs;         /* equal fp32 keys re-ordered by fp64 depth    */
+  int64_t entry_capacity;   /* workspace capacity used for this frame      */
+  float ms_project, ms_duplicate, ms_sort, ms_blend, ms_total;
+  int32_t overflow;         /* 1 if bin_entries > entry_capacity           */
+} StpStats;
+
+/* Byte offsets of the workspace regions (debug / parity dumps). */
+typedef struct {
+  size_t recs, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
+      counters, hist, lookback, scan_scratch, total;
+  int64_t entry_capacity;
+  int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;
+  int32_t splat_record_bytes;
+  int32_t final_buffer;     /* 0: sorted keys/vals in keys0/vals0, 1: keys1/vals1 */
+} StpLayout;
+
+int stp_abi_version(void);
+const char* stp_error_string(int code);
+
+/* STP_OK or STP_ERR_CONFIG (same rules as validate_mode / RenderConfig). */
+int stp_validate_config(const StpConfig* cfg);
+
+/* Workspace needed for n Gaussians, a width x height frame and up to
+ * entry_capacity (tile, splat) entries. */
+size_t stp_workspace_bytes(int64_t n, int32_t width, int32_t height, int64_t entry_capacity);
+
+/* Region offsets for a workspace of ws_bytes (entry capacity is derived). */
+int stp_workspace_layout(int64_t n, int32_t width, int32_t height, size_t ws_bytes,
+                         StpLayout* out);
+
+/* Render one view.  Asynchronous unless `stats` is non-NULL (then the stream
+ * is synchronised and the stats filled; an entry overflow returns
+ * STP_ERR_WORKSPACE_TOO_SMALL with stats->bin_entries set). */
+int stp_render(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
+               void* workspace, size_t workspace_bytes, const StpOutputs* out,
+               StpStats* stats, void* stream);
+
+/* Render n_views cameras back to back on one stream (one workspace, outputs
+ * per view); never synchronises. */
+int stp_render_views(const StpScene* scene, const StpCamera* cams, int32_t n_views,
+                     const StpConfig* cfg, void* workspace, size_t workspace_bytes,
+                     const StpOutputs* outs, void* stream);
+
+/* Render one view recording 5 caller-created CUDA events (cudaEvent_t as
+ * void*) at the stage boundaries [K0+K1 | K2+K3 | K4+K5 | K6]; asynchronous.
+ * events[3] -> events[4] brackets the render kernel K6 alone. */
+int stp_render_events(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
+                      void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                      void* const* events, void* stream);
+
+/* Thin cudart helpers so hosts without a CUDA binding can time stages. */
+int stp_events_create(int32_t n, void** events);
+int stp_events_destroy(int32_t n, void* const* events);
+int stp_event_elapsed_ms(void* start, void* end, float* ms);
+
+/* Read the stats of the last frame rendered into `workspace` (synchronises
+ * the stream). */
+int stp_read_stats(const void* workspace, size_t workspace_bytes, int64_t n, int32_t width,
+                   int32_t height, StpStats* stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STP_H_ */

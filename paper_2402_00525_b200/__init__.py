@@ -1,0 +1,28 @@
+"""B200-native hierarchical sorted Gaussian-splatting forward renderer
+(StopThePop, arXiv 2402.00525), a drop-in for the reference package's
+``render(scene, cam, Hierarchical(), cfg)`` path.
+
+Public API mirrors ``splatsort`` (reference __init__.py:42-61) for this path.
+Importing the package does not need a GPU; rendering does (no CPU fallback).
+"""
+
+from .types import (  # noqa: F401
+    Camera, ConfigError, DataError, FrameOutput, FullPerPixel, Gaussian3D, GlobalZ,
+    Hierarchical, PixelRecords, RenderConfig, SceneFormatError, SortMode, TileBin, Window,
+    mode_name, parse_mode, validate_mode,
+)
+
+__all__ = [
+    "Camera", "ConfigError", "DataError", "FrameOutput", "FullPerPixel", "Gaussian3D",
+    "GlobalZ", "Hierarchical", "PixelRecords", "RenderConfig", "SceneFormatError", "SortMode",
+    "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
+    "render_trajectory", "Renderer", "GaussianScene",
+]
+
+
+def __getattr__(name):
+    # torch-dependent entry points load lazily
+    if name in ("render", "render_depth", "render_trajectory", "Renderer", "GaussianScene"):
+        from . import renderer
+        return getattr(renderer, name)
+    raise AttributeError(name)

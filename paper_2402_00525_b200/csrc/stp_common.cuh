@@ -1,0 +1,202 @@
+// Shared device definitions for the B200 hierarchical splat renderer.
+//
+// Geometry that decides culling and blend order (projection, Alg. 1 peak
+// search, t_opt keys at every hierarchy level, the per-pixel alpha test) is
+// evaluated in float64, following the reference's formulas
+// (gaussian_math.py / tile_culling.py / hierarchy.py); B200 runs FP64 at half
+// the FP32 rate, and only float64 decisions reproduce the float64 reference's
+// tile lists and per-tile / per-pixel orders.  Sort keys are the fp32
+// rounding of the fp64 depth (monotone), with equal-key runs re-ordered by the
+// fp64 depth in K5, so the final order equals np.lexsort((rank, key, tile)).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stp.h"
+
+namespace stp {
+
+constexpr int kTile = 16;
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Projected splat, one per kept Gaussian, indexed by Gaussian id.  144 B =
+// 9 x 16 B: everything K3 (duplicate) and K6 (render) gather per entry.
+struct __align__(16) SplatRec {
+  double mx, my;        // mean2d (pixels)                            0
+  double ca, cb, cc;    // conic (a, b, c)                            16
+  double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr
+  double m[6];          // packed inverse covariance (m00,m11,m22,m01,m02,m12)  48
+  double q0, q1;        // inv_cov3 (mean - camera origin), x and y   96
+  float op;             // opacity                                    112
+  float c0, c1, c2;     // SH colour (lower-clamped at 0)
+  double q2;            // inv_cov3 (mean - camera origin), z         128
+  int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)
+};
+static_assert(sizeof(SplatRec) == 144, "SplatRec must be 144 B");
+
+struct DevCam {
+  double R[9];
+  double pos[3];
+  double fx, fy, cx, cy;
+  int W, H;
+};
+
+struct DevCfg {
+  double eps, term, cap;
+  double bg[3];
+  double near_plane, guard, dilation, clamp;
+  int q_tail, q_mid, q_head;
+  int mid_center, with_depth, exact, rec_cap;
+};
+
+// Workspace counters (uint64), zeroed per frame except the epoch.
+enum Counter {
+  C_EPOCH = 0,
+  C_BEHIND = 1,
+  C_GUARD = 2,
+  C_DEGEN = 3,
+  C_KEPT = 4,
+  C_ENTRIES = 5,
+  C_TILES = 6,
+  C_NONFINITE = 7,
+  C_TIES = 8,
+  C_PART = 16,      // 8 per-pass partition counters
+  C_WORK = 24,      // render work counter
+  C_COUNT = 32
+};
+
+// ---------------------------------------------------------------------------
+// Math shared by all kernels (float64).
+
+// max_points, tile_culling.py:55-88, for one splat and one closed rect.
+__device__ __forceinline__ void max_point(double mx, double my, double a, double b, double c,
+                                          double xmin, double xmax, double ymin, double ymax,
+                                          double& ox, double& oy) {
+  const bool inside_x = (mx >= xmin) && (mx <= xmax);
+  const bool inside_y = (my >= ymin) && (my <= ymax);
+  if (inside_x && inside_y) {
+    ox = mx;
+    oy = my;
+    return;
+  }
+  const double px = (mx <= 0.5 * (xmin + xmax)) ? xmin : xmax;
+  const double py = (my <= 0.5 * (ymin + ymax)) ? ymin : ymax;
+  const double dxx = (px == xmin) ? (xmax - xmin) : (xmin - xmax);
+  const double dyy = (py == ymin) ? (ymax - ymin) : (ymin - ymax);
+  const double rx = mx - px;
+  const double ry = my - py;
+  double t_y = (b * rx + c * ry) / (dyy * c);
+  double t_x = (a * rx + b * ry) / (dxx * a);
+  t_y = fmin(fmax(t_y, 0.0), 1.0);
+  t_x = fmin(fmax(t_x, 0.0), 1.0);
+  if (inside_x) t_y = 0.0;
+  if (inside_y) t_x = 0.0;
+  ox = px + t_x * dxx;
+  oy = py + t_y * dyy;
+}
+
+// exponent of gauss2d (tile_culling.py:96)
+__device__ __forceinline__ double gpower(double a, double b, double c, double dx, double dy) {
+  return 0.5 * (a * dx * dx + c * dy * dy) + b * dx * dy;
+}
+
+// opacity * exp(-power) >= eps  (rasterizer.py:337-338, hierarchy.py:197,99-101).
+// Decided on the log side away from the boundary; within 1e-9 of it the
+// reference's own product is evaluated.
+__device__ __forceinline__ bool alpha_keep(double power, double thr, float op, double eps) {
+  if (power > thr + 1e-9) return false;
+  if (power < thr - 1e-9) return true;
+  return (double)op * exp(-power) >= eps;
+}
+
+// rays_through_points (tile_culling.py:161-173): normalize(v @ R).
+__device__ __forceinline__ void ray_dir(const DevCam& cam, double x, double y, double& d0,
+                                        double& d1, double& d2) {
+  const double v0 = (x - cam.cx) / cam.fx;
+  const double v1 = (y - cam.cy) / cam.fy;
+  d0 = v0 * cam.R[0] + v1 * cam.R[3] + cam.R[6];
+  d1 = v0 * cam.R[1] + v1 * cam.R[4] + cam.R[7];
+  d2 = v0 * cam.R[2] + v1 * cam.R[5] + cam.R[8];
+  const double inv = 1.0 / sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+  d0 *= inv;
+  d1 *= inv;
+  d2 *= inv;
+}
+
+// blend_depths (tile_culling.py:185-195) with ray_features (:176-182).
+__device__ __forceinline__ double blend_depth(const double* m, double q0, double q1, double q2,
+                                              double d0, double d1, double d2) {
+  const double num = d0 * q0 + d1 * q1 + d2 * q2;
+  const double den = (d0 * d0) * m[0] + (d1 * d1) * m[1] + (d2 * d2) * m[2] +
+                     (2 * d0 * d1) * m[3] + (2 * d0 * d2) * m[4] + (2 * d1 * d2) * m[5];
+  return num / den;
+}
+
+// Monotone fp32 sort key of a float64 depth: round-to-nearest, -0 -> +0,
+// then the usual order-preserving bit flip.
+__device__ __forceinline__ uint32_t depth_key(double d) {
+  float f = __double2float_rn(d);
+  if (f == 0.0f) f = 0.0f;
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+  return __shfl_xor_sync(kFull, v, m);
+}
+
+// Tile-level exact cull for splat `r` at tile (tx, ty) (rasterizer.py:334-339).
+__device__ __forceinline__ bool tile_survives(double mx, double my, double a, double b, double c,
+                                              double thr, float op, double eps, int tx, int ty,
+                                              double& ptx, double& pty) {
+  const double x0 = (double)(tx * kTile), x1 = (double)((tx + 1) * kTile);
+  const double y0 = (double)(ty * kTile), y1 = (double)((ty + 1) * kTile);
+  max_point(mx, my, a, b, c, x0, x1, y0, y1, ptx, pty);
+  return alpha_keep(gpower(a, b, c, ptx - mx, pty - my), thr, op, eps);
+}
+
+}  // namespace stp
+
+// Host-side launchers (defined in the .cu files, called by stp_api.cu).
+namespace stp {
+struct Frame {
+  // device pointers carved from the workspace
+  SplatRec* recs;
+  uint8_t* state;
+  uint32_t* counts;
+  uint32_t* offsets;
+  uint64_t* keys[2];
+  uint32_t* vals[2];
+  uint2* ranges;
+  unsigned long long* counters;
+  uint32_t* hist;         // [passes][256]
+  unsigned long long* lookback;  // [passes][partitions][256]
+  uint32_t* scan_scratch;
+  int64_t n;
+  int64_t ecap;
+  int gw, gh, n_tiles;
+  int passes, partitions;
+  DevCam cam;
+  DevCfg cfg;
+};
+
+void launch_init(const Frame& f, cudaStream_t s);
+void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s);
+void launch_scan(const Frame& f, cudaStream_t s);
+void launch_duplicate(const Frame& f, cudaStream_t s);
+int launch_sort(const Frame& f, cudaStream_t s);  // returns the buffer holding the result
+void launch_ranges(const Frame& f, int buf, cudaStream_t s);
+void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
+}  // namespace stp

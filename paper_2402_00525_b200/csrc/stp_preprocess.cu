@@ -1,0 +1,527 @@
+// K0 frame init, K1 preprocess, K2 scan, K3 duplicate.
+//
+// K1 restates project_scene (gaussian_math.py:323-434) per Gaussian in
+// float64 from the float32 inputs, plus the coarse tile rect
+// (rasterizer.py:307-321) and the exact-culled tile count
+// (rasterizer.py:334-339).  K3 re-enumerates the surviving tiles and writes
+// (key = tile<<32 | fp32-orderable t_opt at the 16x16 peak, value = Gaussian
+// id) in Gaussian order (rasterizer.py:328-350), so a stable LSD sort breaks
+// key ties by rank exactly like np.lexsort((rank, key, tile)).
+//
+// Rects larger than kLoadBalance tiles are enumerated cooperatively by the
+// whole warp (PAPER.md:589-599 load balancing, threshold 32).
+#include "stp_common.cuh"
+
+namespace stp {
+
+constexpr int kPreThreads = 256;
+constexpr int kLoadBalance = 32;
+
+__constant__ double c_SH_C0 = 0.28209479177387814;
+__constant__ double c_SH_C1 = 0.4886025119029199;
+__constant__ double c_SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                  -1.0925484305920792, 0.5462742152960396};
+__constant__ double c_SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                  0.3731763325901154,  -0.4570457994644658, 1.445305721320277,
+                                  -0.5900435899266435};
+
+// ---------------------------------------------------------------------------
+// K0: zero the per-frame counters / histograms / tile ranges, bump the epoch
+// that tags the sort's look-back words (so they never need clearing).
+__global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n, uint2* ranges,
+                       int n_tiles) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+  if (tid == 0) counters[C_EPOCH] += 1;
+  for (int i = tid; i < C_COUNT; i += stride)
+    if (i != C_EPOCH) counters[i] = 0;
+  for (int i = tid; i < hist_n; i += stride) hist[i] = 0;
+  for (int i = tid; i < n_tiles; i += stride) ranges[i] = make_uint2(0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// K1 preprocess.
+
+__device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, double x, double y,
+                                         double z, float out[3]) {
+  double b[16];
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double xy = x * y, yz = y * z, xz = x * z;
+  b[0] = c_SH_C0;
+  if (K > 1) {
+    b[1] = -c_SH_C1 * y;
+    b[2] = c_SH_C1 * z;
+    b[3] = -c_SH_C1 * x;
+  }
+  if (K > 4) {
+    b[4] = c_SH_C2[0] * xy;
+    b[5] = c_SH_C2[1] * yz;
+    b[6] = c_SH_C2[2] * (2.0 * zz - xx - yy);
+    b[7] = c_SH_C2[3] * xz;
+    b[8] = c_SH_C2[4] * (xx - yy);
+  }
+  if (K > 9) {
+    b[9] = c_SH_C3[0] * y * (3.0 * xx - yy);
+    b[10] = c_SH_C3[1] * xy * z;
+    b[11] = c_SH_C3[2] * y * (4.0 * zz - xx - yy);
+    b[12] = c_SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    b[13] = c_SH_C3[4] * x * (4.0 * zz - xx - yy);
+    b[14] = c_SH_C3[5] * z * (xx - yy);
+    b[15] = c_SH_C3[6] * x * (xx - 3.0 * yy);
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (K == 16) {
+    // 192 B per Gaussian: 12 x float4
+    const float4* p = reinterpret_cast<const float4*>(sh);
+    float v[48];
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const float4 f = __ldg(p + u);
+      v[4 * u + 0] = f.x;
+      v[4 * u + 1] = f.y;
+      v[4 * u + 2] = f.z;
+      v[4 * u + 3] = f.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      acc[0] += b[k] * (double)v[3 * k + 0];
+      acc[1] += b[k] * (double)v[3 * k + 1];
+      acc[2] += b[k] * (double)v[3 * k + 2];
+    }
+  } else {
+    for (int k = 0; k < K; ++k) {
+      acc[0] += b[k] * (double)__ldg(sh + 3 * k + 0);
+      acc[1] += b[k] * (double)__ldg(sh + 3 * k + 1);
+      acc[2] += b[k] * (double)__ldg(sh + 3 * k + 2);
+    }
+  }
+  // np.clip(basis @ sh + 0.5, 0, None): lower clamp only (gaussian_math.py:417-419)
+  out[0] = (float)fmax(acc[0] + 0.5, 0.0);
+  out[1] = (float)fmax(acc[1] + 0.5, 0.0);
+  out[2] = (float)fmax(acc[2] + 0.5, 0.0);
+}
+
+// Count (or, with kWrite, emit) the exact-culled tiles of one splat whose
+// rect is small enough to be walked by its own thread.
+struct SplatGeo {
+  double mx, my, a, b, c, thr;
+  float op;
+  int rx0, rx1, ry0, ry1;
+};
+
+__device__ __forceinline__ uint32_t count_serial(const SplatGeo& g, const DevCfg& cfg) {
+  uint32_t n = 0;
+  for (int ty = g.ry0; ty <= g.ry1; ++ty)
+    for (int tx = g.rx0; tx <= g.rx1; ++tx) {
+      double px, py;
+      if (!cfg.exact || tile_survives(g.mx, g.my, g.a, g.b, g.c, g.thr, g.op, cfg.eps, tx, ty, px, py))
+        ++n;
+    }
+  return n;
+}
+
+__global__ void __launch_bounds__(kPreThreads) k_preprocess(
+    StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
+    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    unsigned long long* __restrict__ counters) {
+  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = i < sc.n;
+  int reason = 4;  // 0 kept, 1 behind, 2 guard, 3 degenerate, 4 out of range
+  SplatGeo g;
+  g.rx0 = 1;
+  g.rx1 = 0;
+  g.ry0 = 1;
+  g.ry1 = 0;
+  g.mx = g.my = g.a = g.b = g.c = g.thr = 0.0;
+  g.op = 0.f;
+
+  if (valid) {
+    const double* W = cam.R;
+    const double rel0 = (double)__ldg(sc.means + 3 * i + 0) - cam.pos[0];
+    const double rel1 = (double)__ldg(sc.means + 3 * i + 1) - cam.pos[1];
+    const double rel2 = (double)__ldg(sc.means + 3 * i + 2) - cam.pos[2];
+    // p_view = rel @ W^T (gaussian_math.py:360-362)
+    const double pv0 = rel0 * W[0] + rel1 * W[1] + rel2 * W[2];
+    const double pv1 = rel0 * W[3] + rel1 * W[4] + rel2 * W[5];
+    const double z = rel0 * W[6] + rel1 * W[7] + rel2 * W[8];
+    if (!(z > cfg.near_plane)) {
+      reason = 1;  // :364
+    } else {
+      const double px = cam.fx * pv0 / z + cam.cx;  // :368-369
+      const double py = cam.fy * pv1 / z + cam.cy;
+      const bool in_guard = (fabs(px - cam.cx) <= cfg.guard * cam.W / 2.0) &&
+                            (fabs(py - cam.cy) <= cfg.guard * cam.H / 2.0);
+      if (!in_guard) {
+        reason = 2;  // :370-373
+      } else {
+        // _quats_to_matrices (gaussian_math.py:102-115)
+        const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
+        const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;
+        const double qn = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+        const double w = qw0 / qn, x = qx0 / qn, y = qy0 / qn, zq = qz0 / qn;
+        double rot[9] = {1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y),
+                         2 * (x * y + w * zq),      1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x),
+                         2 * (x * zq - w * y),      2 * (y * zq + w * x),  1 - 2 * (x * x + y * y)};
+        const double s0 = __ldg(sc.scales + 3 * i + 0);
+        const double s1 = __ldg(sc.scales + 3 * i + 1);
+        const double s2 = __ldg(sc.scales + 3 * i + 2);
+        const double ss[3] = {s0 * s0, s1 * s1, s2 * s2};
+        double cov3[9];
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            double acc = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) acc += rot[aa * 3 + bb] * ss[bb] * rot[cc * 3 + bb];
+            cov3[aa * 3 + cc] = acc;
+          }
+        // J and M = J W (gaussian_math.py:378-383)
+        const double J[6] = {cam.fx / z, 0.0, -cam.fx * pv0 / (z * z),
+                             0.0, cam.fy / z, -cam.fy * pv1 / (z * z)};
+        double M[6];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            M[r * 3 + k] = J[r * 3 + 0] * W[k] + J[r * 3 + 1] * W[3 + k] + J[r * 3 + 2] * W[6 + k];
+        double cov2[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int l = 0; l < 2; ++l) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+              for (int k = 0; k < 3; ++k) acc += M[r * 3 + j] * cov3[j * 3 + k] * M[l * 3 + k];
+            cov2[r * 2 + l] = acc;
+          }
+        const double a = cov2[0] + cfg.dilation;  // :385-387
+        const double b = cov2[1];
+        const double c = cov2[3] + cfg.dilation;
+        const double det = a * c - b * b;
+        if (!(det > 0.0)) {
+          reason = 3;  // :388-390
+        } else {
+          reason = 0;
+          SplatRec r;
+          r.mx = px;
+          r.my = py;
+          r.ca = c / det;  // conic (:397)
+          r.cb = -b / det;
+          r.cc = a / det;
+          // opacity-aware radius (:399-404)
+          const float opf = __ldg(sc.opacity + i);
+          const double op = opf;
+          const double mid = 0.5 * (a + c);
+          const double lam_max = mid + sqrt(fmax(mid * mid - a * c + b * b, 0.0));
+          const double cutoff = (op > cfg.eps) ? sqrt(2.0 * log(op / cfg.eps)) : 0.0;
+          const double radius = cutoff * sqrt(lam_max);
+          r.thr = (op > 0.0) ? log(op / cfg.eps) : -INFINITY;
+          r.op = opf;
+          // packed clamped inverse covariance (:406-412) and its centre (:413)
+          double is[3];
+          is[0] = fmin(1.0 / s0, cfg.clamp);
+          is[1] = fmin(1.0 / s1, cfg.clamp);
+          is[2] = fmin(1.0 / s2, cfg.clamp);
+          is[0] *= is[0];
+          is[1] *= is[1];
+          is[2] *= is[2];
+          double inv3[9];
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+              double acc = 0.0;
+#pragma unroll
+              for (int bb = 0; bb < 3; ++bb) acc += rot[aa * 3 + bb] * is[bb] * rot[cc * 3 + bb];
+              inv3[aa * 3 + cc] = acc;
+            }
+          r.m[0] = inv3[0];
+          r.m[1] = inv3[4];
+          r.m[2] = inv3[8];
+          r.m[3] = inv3[1];
+          r.m[4] = inv3[2];
+          r.m[5] = inv3[5];
+          r.q0 = inv3[0] * rel0 + inv3[1] * rel1 + inv3[2] * rel2;
+          r.q1 = inv3[3] * rel0 + inv3[4] * rel1 + inv3[5] * rel2;
+          r.q2 = inv3[6] * rel0 + inv3[7] * rel1 + inv3[8] * rel2;
+          // SH colour along (mean - origin) / |mean - origin| (:415-419)
+          const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
+          float col[3];
+          sh_color(sc.sh + (int64_t)i * sc.sh_coeffs * 3, sc.sh_coeffs, rel0 / dist, rel1 / dist,
+                   rel2 / dist, col);
+          r.c0 = col[0];
+          r.c1 = col[1];
+          r.c2 = col[2];
+          // coarse tile rect (rasterizer.py:307-321), clamped in double first
+          const double ts = (double)kTile;
+          const double lo = -2.0;
+          const double fx0 = fmin(fmax(floor((px - radius) / ts), lo), (double)gw + 1);
+          const double fy0 = fmin(fmax(floor((py - radius) / ts), lo), (double)gh + 1);
+          const double fx1 = fmin(fmax(fmax(ceil((px + radius) / ts) - 1.0, floor(px / ts)), lo),
+                                  (double)gw + 1);
+          const double fy1 = fmin(fmax(fmax(ceil((py + radius) / ts) - 1.0, floor(py / ts)), lo),
+                                  (double)gh + 1);
+          int x0 = max((int)fx0, 0), y0 = max((int)fy0, 0);
+          int x1 = min((int)fx1, gw - 1), y1 = min((int)fy1, gh - 1);
+          if (!(radius == radius)) {  // NaN radius: no tiles
+            x0 = 1;
+            x1 = 0;
+          }
+          if (x1 < x0 || y1 < y0) {
+            x0 = 1;
+            x1 = 0;
+            y0 = 1;
+            y1 = 0;
+          }
+          r.rx0 = (int16_t)x0;
+          r.rx1 = (int16_t)x1;
+          r.ry0 = (int16_t)y0;
+          r.ry1 = (int16_t)y1;
+          recs[i] = r;
+          g.mx = r.mx;
+          g.my = r.my;
+          g.a = r.ca;
+          g.b = r.cb;
+          g.c = r.cc;
+          g.thr = r.thr;
+          g.op = r.op;
+          g.rx0 = x0;
+          g.rx1 = x1;
+          g.ry0 = y0;
+          g.ry1 = y1;
+        }
+      }
+    }
+  }
+
+  // exact-culled tile count
+  const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
+  const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
+  uint32_t cnt = 0;
+  if (area > 0 && area <= kLoadBalance) cnt = count_serial(g, cfg);
+  unsigned big = __ballot_sync(kFull, area > kLoadBalance);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const double mx = shfl_d(g.mx, src), my = shfl_d(g.my, src);
+    const double a = shfl_d(g.a, src), b = shfl_d(g.b, src), c = shfl_d(g.c, src);
+    const double thr = shfl_d(g.thr, src);
+    const float op = __shfl_sync(kFull, g.op, src);
+    const int rx0 = __shfl_sync(kFull, g.rx0, src), ry0 = __shfl_sync(kFull, g.ry0, src);
+    const int ww = __shfl_sync(kFull, wx, src), ar = __shfl_sync(kFull, area, src);
+    int c_local = 0;
+    for (int t = lane; t < ar; t += 32) {
+      const int tx = rx0 + t % ww, ty = ry0 + t / ww;
+      double px, py;
+      if (!cfg.exact || tile_survives(mx, my, a, b, c, thr, op, cfg.eps, tx, ty, px, py)) ++c_local;
+    }
+    c_local = warp_sum(c_local);
+    if (lane == src) cnt = (uint32_t)c_local;
+  }
+  if (valid) {
+    counts[i] = cnt;
+    if (state) state[i] = (uint8_t)reason;
+  }
+  const int n_behind = __syncthreads_count(reason == 1);
+  const int n_guard = __syncthreads_count(reason == 2);
+  const int n_degen = __syncthreads_count(reason == 3);
+  const int n_kept = __syncthreads_count(reason == 0);
+  if (threadIdx.x == 0) {
+    if (n_behind) atomicAdd(counters + C_BEHIND, (unsigned long long)n_behind);
+    if (n_guard) atomicAdd(counters + C_GUARD, (unsigned long long)n_guard);
+    if (n_degen) atomicAdd(counters + C_DEGEN, (unsigned long long)n_degen);
+    if (n_kept) atomicAdd(counters + C_KEPT, (unsigned long long)n_kept);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 exclusive scan of per-splat tile counts (three phases, 4096 per block).
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = (lane < (int)(blockDim.x >> 5)) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, s, o);
+      if (lane >= o) s += y;
+    }
+    s_warp[lane] = s;
+  }
+  __syncthreads();
+  total = s_warp[(blockDim.x >> 5) - 1];
+  const uint32_t warp_off = w ? s_warp[w - 1] : 0;
+  __syncthreads();
+  return warp_off + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const uint32_t* __restrict__ counts,
+                                                                int64_t n, uint32_t* partials) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < n) sum += counts[base + k];
+  uint32_t total;
+  block_excl_scan(sum, s_warp, total);
+  if (threadIdx.x == 0) partials[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(uint32_t* partials, int nb,
+                                                   unsigned long long* counters) {
+  __shared__ uint32_t s_warp[32];
+  unsigned long long carry = 0;
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = (i < nb) ? partials[i] : 0;
+    uint32_t total;
+    const uint32_t ex = block_excl_scan(v, s_warp, total);
+    if (i < nb) partials[i] = (uint32_t)(carry + ex);
+    carry += total;
+  }
+  if (threadIdx.x == 0) counters[C_ENTRIES] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __restrict__ counts,
+                                                             int64_t n,
+                                                             const uint32_t* __restrict__ partials,
+                                                             uint32_t* __restrict__ offsets) {
+  __shared__ uint32_t s_warp[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < n) ? counts[base + k] : 0;
+    sum += v[k];
+  }
+  uint32_t total;
+  uint32_t run = block_excl_scan(sum, s_warp, total) + partials[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) offsets[base + k] = run;
+    run += v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 duplicate.
+
+__device__ __forceinline__ void emit_entry(const SplatRec& r, const DevCam& cam, int tx, int ty,
+                                           double ptx, double pty, int gw, uint32_t id,
+                                           uint32_t pos, int64_t ecap, uint64_t* keys,
+                                           uint32_t* vals) {
+  double d0, d1, d2;
+  ray_dir(cam, ptx, pty, d0, d1, d2);  // rasterizer.py:349-350
+  const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+  if ((int64_t)pos < ecap) {
+    keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << 32) | depth_key(depth);
+    vals[pos] = id;
+  }
+}
+
+__device__ __forceinline__ bool dup_test(const SplatRec& r, const DevCfg& cfg, int tx, int ty,
+                                         double& ptx, double& pty) {
+  const bool keep =
+      tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.thr, r.op, cfg.eps, tx, ty, ptx, pty);
+  return !cfg.exact || keep;
+}
+
+__global__ void __launch_bounds__(kPreThreads) k_duplicate(
+    const SplatRec* __restrict__ recs, const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
+    int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cnt = (i < n) ? counts[i] : 0;
+  int area = 0, wx = 1;
+  SplatRec r;
+  uint32_t base = 0;
+  if (cnt > 0) {
+    r = recs[i];
+    wx = r.rx1 - r.rx0 + 1;
+    area = wx * (r.ry1 - r.ry0 + 1);
+    base = offsets[i];
+    if (area <= kLoadBalance) {
+      uint32_t pos = base;
+      for (int ty = r.ry0; ty <= r.ry1; ++ty)
+        for (int tx = r.rx0; tx <= r.rx1; ++tx) {
+          double ptx, pty;
+          if (dup_test(r, cfg, tx, ty, ptx, pty))
+            emit_entry(r, cam, tx, ty, ptx, pty, gw, (uint32_t)i, pos++, ecap, keys, vals);
+        }
+    }
+  }
+  unsigned big = __ballot_sync(kFull, area > kLoadBalance);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const int64_t sid = __shfl_sync(kFull, i, src);
+    const SplatRec rs = recs[sid];  // broadcast load
+    const int ww = rs.rx1 - rs.rx0 + 1;
+    const int ar = ww * (rs.ry1 - rs.ry0 + 1);
+    uint32_t pos = __shfl_sync(kFull, base, src);
+    for (int t0 = 0; t0 < ar; t0 += 32) {
+      const int t = t0 + lane;
+      const int tx = rs.rx0 + t % ww, ty = rs.ry0 + t / ww;
+      double ptx = 0, pty = 0;
+      const bool keep = (t < ar) && dup_test(rs, cfg, tx, ty, ptx, pty);
+      const unsigned m = __ballot_sync(kFull, keep);
+      if (keep)
+        emit_entry(rs, cam, tx, ty, ptx, pty, gw, (uint32_t)sid,
+                   pos + __popc(m & ((1u << lane) - 1)), ecap, keys, vals);
+      pos += __popc(m);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+void launch_init(const Frame& f, cudaStream_t s) {
+  const int hist_n = f.passes * 256;
+  const int work = max(max(hist_n, f.n_tiles), (int)C_COUNT);
+  const int blocks = min((work + 255) / 256, 1024);
+  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles);
+}
+
+void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
+  if (f.n == 0) return;
+  const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
+  k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
+                                                      f.counts, f.state, f.counters);
+}
+
+void launch_scan(const Frame& f, cudaStream_t s) {
+  if (f.n == 0) return;
+  const int nb = (int)((f.n + kScanTile - 1) / kScanTile);
+  k_scan_partials<<<nb, kScanThreads, 0, s>>>(f.counts, f.n, f.scan_scratch);
+  k_scan_top<<<1, 1024, 0, s>>>(f.scan_scratch, nb, f.counters);
+  k_scan_final<<<nb, kScanThreads, 0, s>>>(f.counts, f.n, f.scan_scratch, f.offsets);
+}
+
+void launch_duplicate(const Frame& f, cudaStream_t s) {
+  if (f.n == 0) return;
+  const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
+  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.counts, f.offsets, f.n, f.cam,
+                                                     f.cfg, f.gw, f.ecap, f.keys[0], f.vals[0]);
+}
+
+}  // namespace stp

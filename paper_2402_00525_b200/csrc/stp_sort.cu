@@ -1,0 +1,295 @@
+// K4: hand-written onesweep LSD radix sort (Adinets & Merrill 2022 scheme)
+//     over the 64-bit (tile << 32 | depth-key) keys with uint32 Gaussian-id
+//     values; replaces np.lexsort((rank, key, tile_id)) (rasterizer.py:353-357).
+//     8-bit digits, ceil((32 + tile_bits) / 8) passes, one global-histogram
+//     pass up front, per-partition decoupled look-back with epoch-tagged
+//     status words (no per-frame clearing).  Stable: partitions are ranked in
+//     input order with warp-striped items and match.any peer ranking.
+// K5: tile ranges (rasterizer.py:358-372) and the float64 tie fix-up: runs of
+//     equal fp32 keys inside a tile are re-ordered by the float64 depth and
+//     then rank, so the final order equals the reference's float64 lexsort.
+#include "stp_common.cuh"
+
+namespace stp {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 items per partition
+constexpr int kRadix = 256;
+
+// look-back word: [epoch:32 | flag:2 | count:30]
+constexpr unsigned long long kFlagAgg = 1ull << 30;
+constexpr unsigned long long kFlagPre = 2ull << 30;
+constexpr unsigned long long kCountMask = (1ull << 30) - 1;
+
+__device__ __forceinline__ int64_t n_entries(const unsigned long long* counters, int64_t ecap) {
+  const int64_t e = (int64_t)counters[C_ENTRIES];
+  return e < ecap ? e : ecap;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ keys,
+                                                            const unsigned long long* counters,
+                                                            int64_t ecap, int passes,
+                                                            uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_hist[8][kRadix];
+  for (int i = threadIdx.x; i < 8 * kRadix; i += kSortThreads) (&s_hist[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t E = n_entries(counters, ecap);
+  for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * kSortThreads) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += kSortThreads) {
+    const uint32_t v = (&s_hist[0][0])[i];
+    if (v) atomicAdd(hist + i, v);
+  }
+}
+
+struct SortSmem {
+  uint32_t warp_hist[kSortWarps][kRadix];  // per-warp digit counts -> warp offsets
+  uint32_t local_off[kRadix];              // block-local exclusive digit offsets
+  uint32_t global_off[kRadix];             // this partition's first output slot per digit
+  uint32_t scan_tmp[kRadix];
+  uint32_t part;
+  uint64_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+    uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+    const unsigned long long* counters, int64_t ecap, int shift,
+    const uint32_t* __restrict__ hist, unsigned long long* lookback,
+    unsigned long long* part_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) sm.part = (uint32_t)atomicAdd(part_counter, 1ull);
+  for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t part = sm.part;
+  const int64_t E = n_entries(counters, ecap);
+  const int64_t base = (int64_t)part * kSortTile;
+  if (base >= E) return;
+  const uint32_t epoch = (uint32_t)counters[C_EPOCH];
+  const int n_valid = (int)min((int64_t)kSortTile, E - base);
+
+  // warp-striped load: warp w owns [base + w*512, +512), item k of lane l at k*32 + l
+  uint64_t key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t dig[kSortItems];
+  uint32_t rank[kSortItems];
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const int li = w * (kSortItems * 32) + k * 32 + lane;
+    if (li < n_valid) {
+      key[k] = kin[base + li];
+      val[k] = vin[base + li];
+      dig[k] = (uint32_t)(key[k] >> shift) & 0xff;
+    } else {
+      key[k] = ~0ull;
+      val[k] = 0;
+      dig[k] = 0xff;
+    }
+  }
+  // stable warp-level ranking
+  const unsigned lt_mask = (1u << lane) - 1;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const unsigned peers = __match_any_sync(kFull, dig[k]);
+    const int leader = 31 - __clz(peers);
+    const uint32_t before = sm.warp_hist[w][dig[k]];
+    __syncwarp();
+    rank[k] = before + __popc(peers & lt_mask);
+    if (lane == leader) sm.warp_hist[w][dig[k]] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive scan across warps, block total
+  uint32_t block_cnt;
+  {
+    const int d = tid;  // kSortThreads == kRadix
+    uint32_t sum = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = sm.warp_hist[ww][d];
+      sm.warp_hist[ww][d] = sum;
+      sum += c;
+    }
+    block_cnt = sum;
+    // publish aggregate / inclusive prefix, then look back
+    unsigned long long* my = lookback + (size_t)part * kRadix + d;
+    const unsigned long long tag = (unsigned long long)epoch << 32;
+    unsigned long long excl = 0;
+    if (part == 0) {
+      atomicExch(my, tag | kFlagPre | (unsigned long long)block_cnt);
+    } else {
+      atomicExch(my, tag | kFlagAgg | (unsigned long long)block_cnt);
+      int64_t p = (int64_t)part - 1;
+      while (true) {
+        const unsigned long long v =
+            *reinterpret_cast<volatile unsigned long long*>(lookback + (size_t)p * kRadix + d);
+        if ((v >> 32) != epoch || ((v >> 30) & 3ull) == 0) continue;  // not yet published
+        excl += v & kCountMask;
+        if (((v >> 30) & 3ull) == 2) break;
+        --p;
+      }
+      atomicExch(my, tag | kFlagPre | ((excl + block_cnt) & kCountMask));
+    }
+    sm.global_off[d] = (uint32_t)excl;
+    sm.scan_tmp[d] = hist[d];
+  }
+  __syncthreads();
+  // exclusive scans over the 256 digits: global histogram and block counts
+  {
+    const int d = tid;
+    uint32_t g = sm.scan_tmp[d], b = block_cnt;
+    // Hillis-Steele in shared memory (256 entries)
+    __shared__ uint32_t s_a[kRadix], s_b[kRadix];
+    s_a[d] = g;
+    s_b[d] = b;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+      const uint32_t ya = (d >= o) ? s_a[d - o] : 0, yb = (d >= o) ? s_b[d - o] : 0;
+      __syncthreads();
+      s_a[d] += ya;
+      s_b[d] += yb;
+      __syncthreads();
+    }
+    sm.global_off[d] += s_a[d] - g;
+    sm.local_off[d] = s_b[d] - b;
+  }
+  __syncthreads();
+  // scatter into shared memory in block-local sorted order
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t pos = sm.local_off[dig[k]] + sm.warp_hist[w][dig[k]] + rank[k];
+    if (pos < (uint32_t)kSortTile) {
+      sm.keys[pos] = key[k];
+      sm.vals[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n_valid; i += kSortThreads) {
+    const uint64_t k = sm.keys[i];
+    const uint32_t d = (uint32_t)(k >> shift) & 0xff;
+    const uint32_t o = sm.global_off[d] + (uint32_t)i - sm.local_off[d];
+    kout[o] = k;
+    vout[o] = sm.vals[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 tile ranges + float64 tie fix-up.
+
+__device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ recs, const DevCam& cam,
+                                                uint32_t id, int tile, int gw) {
+  const SplatRec& r = recs[id];
+  const int tx = tile % gw, ty = tile / gw;
+  double ptx, pty;
+  max_point(r.mx, r.my, r.ca, r.cb, r.cc, (double)(tx * kTile), (double)((tx + 1) * kTile),
+            (double)(ty * kTile), (double)((ty + 1) * kTile), ptx, pty);
+  double d0, d1, d2;
+  ray_dir(cam, ptx, pty, d0, d1, d2);
+  return blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+}
+
+constexpr int kTieLocal = 32;
+
+__global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys,
+                                                uint32_t* __restrict__ vals,
+                                                unsigned long long* counters, int64_t ecap,
+                                                uint2* __restrict__ ranges,
+                                                const SplatRec* __restrict__ recs, DevCam cam,
+                                                int gw) {
+  const int64_t E = n_entries(counters, ecap);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const uint64_t k = keys[i];
+  const uint32_t tile = (uint32_t)(k >> 32);
+  const uint64_t kp = (i > 0) ? keys[i - 1] : ~k;
+  const uint64_t kn = (i + 1 < E) ? keys[i + 1] : ~k;
+  if (i == 0 || (uint32_t)(kp >> 32) != tile) {
+    ranges[tile].x = (uint32_t)i;
+    atomicAdd(counters + C_TILES, 1ull);
+  }
+  if (i + 1 == E || (uint32_t)(kn >> 32) != tile) ranges[tile].y = (uint32_t)(i + 1);
+  // run head of equal full keys (same tile, same fp32 depth key)
+  if (kn == k && (i == 0 || kp != k)) {
+    int64_t L = 2;
+    while (i + L < E && keys[i + L] == k) ++L;
+    atomicAdd(counters + C_TIES, 1ull);
+    if (L <= kTieLocal) {
+      double d[kTieLocal];
+      uint32_t id[kTieLocal];
+      for (int m = 0; m < L; ++m) {
+        id[m] = vals[i + m];
+        d[m] = entry_depth64(recs, cam, id[m], (int)tile, gw);
+      }
+      // insertion sort by (depth, rank); members arrive in rank order
+      for (int m = 1; m < L; ++m) {
+        const double dv = d[m];
+        const uint32_t iv = id[m];
+        int p = m - 1;
+        while (p >= 0 && (d[p] > dv || (d[p] == dv && id[p] > iv))) {
+          d[p + 1] = d[p];
+          id[p + 1] = id[p];
+          --p;
+        }
+        d[p + 1] = dv;
+        id[p + 1] = iv;
+      }
+      for (int m = 0; m < L; ++m) vals[i + m] = id[m];
+    } else {
+      // long runs (coincident splats): in-place insertion sort, recomputing depths
+      for (int64_t m = 1; m < L; ++m) {
+        const uint32_t iv = vals[i + m];
+        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw);
+        int64_t p = m - 1;
+        while (p >= 0) {
+          const uint32_t ip = vals[i + p];
+          const double dp = entry_depth64(recs, cam, ip, (int)tile, gw);
+          if (!(dp > dv || (dp == dv && ip > iv))) break;
+          vals[i + p + 1] = ip;
+          --p;
+        }
+        vals[i + p + 1] = iv;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+int launch_sort(const Frame& f, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SortSmem));
+    attr_set = true;
+  }
+  const int hist_blocks = 148 * 4;
+  k_sort_hist<<<hist_blocks, kSortThreads, 0, s>>>(f.keys[0], f.counters, f.ecap, f.passes,
+                                                    f.hist);
+  int cur = 0;
+  for (int p = 0; p < f.passes; ++p) {
+    k_onesweep<<<f.partitions, kSortThreads, sizeof(SortSmem), s>>>(
+        f.keys[cur], f.vals[cur], f.keys[cur ^ 1], f.vals[cur ^ 1], f.counters, f.ecap, 8 * p,
+        f.hist + p * kRadix, f.lookback + (size_t)p * f.partitions * kRadix,
+        f.counters + C_PART + p);
+    cur ^= 1;
+  }
+  return cur;
+}
+
+void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
+  const int64_t blocks = (f.ecap + 255) / 256;
+  if (blocks == 0) return;
+  k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], f.counters, f.ecap,
+                                            f.ranges, f.recs, f.cam, f.gw);
+}
+
+}  // namespace stp

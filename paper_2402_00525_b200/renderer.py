@@ -1,0 +1,415 @@
+"""Drop-in ``render`` for the reference's Hierarchical forward path, on B200.
+
+Mirrors ``splatsort.render(scene, cam, mode, cfg) -> FrameOutput``
+(rasterizer.py:595-698), ``render_depth`` (:701-715) and ``render_trajectory``
+(:758-772).  The heavy lifting is one C-ABI call per view (include/stp.h ->
+libstp_b200.so, hand-written sm_100a kernels K1..K6); this module only
+stages tensors, owns the device workspace, and converts outputs.
+
+There is no CPU fallback: without a CUDA device or the built library every
+entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .types import (Camera, ConfigError, DataError, FrameOutput, Hierarchical, PixelRecords,
+                    RenderConfig, _is_hier, mode_name, validate_mode)
+
+_SH_OK = (1, 4, 9, 16)
+
+
+def _require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2402_00525_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError("device must be a CUDA device")
+    return dev
+
+
+class GaussianScene:
+    """Device-resident Gaussians in the drop-in tensor layout (float32):
+    means[N,3], quats[N,4] (w,x,y,z), scales[N,3], opacity[N], sh[N,K,3]."""
+
+    def __init__(self, means, quats, scales, opacity, sh, device=None):
+        dev = _require_cuda(device)
+
+        def t(a, shape_tail):
+            x = torch.as_tensor(a) if not isinstance(a, torch.Tensor) else a
+            x = x.to(device=dev, dtype=torch.float32).contiguous()
+            return x.reshape(-1, *shape_tail) if shape_tail else x.reshape(-1)
+
+        self.means = t(means, (3,))
+        self.quats = t(quats, (4,))
+        self.scales = t(scales, (3,))
+        self.opacity = t(opacity, ())
+        n = self.means.shape[0]
+        sh_t = torch.as_tensor(sh) if not isinstance(sh, torch.Tensor) else sh
+        sh_t = sh_t.to(device=dev, dtype=torch.float32).reshape(n, -1, 3)
+        k = sh_t.shape[1] if n else 16
+        if k not in _SH_OK:
+            raise DataError(f"sh must hold 1, 4, 9 or 16 coefficients per channel, got {k}")
+        self.sh = sh_t.contiguous()
+        for name, x in (("quats", self.quats), ("scales", self.scales),
+                        ("opacity", self.opacity)):
+            if x.shape[0] != n:
+                raise DataError(f"{name} has {x.shape[0]} rows, means has {n}")
+        self.device = dev
+
+    @property
+    def n(self) -> int:
+        return int(self.means.shape[0])
+
+    @property
+    def sh_coeffs(self) -> int:
+        return int(self.sh.shape[1]) if self.n else 16
+
+    @classmethod
+    def from_any(cls, scene, device=None) -> "GaussianScene":
+        if isinstance(scene, GaussianScene):
+            return scene
+        if isinstance(scene, dict):
+            return cls(scene["means"], scene["quats"], scene["scales"], scene["opacity"],
+                       scene["sh"], device)
+        if hasattr(scene, "mean2d") and hasattr(scene, "inv_cov3"):
+            raise ConfigError("pre-projected SplatBatch input is not supported by the B200 "
+                              "path yet; pass Gaussians")
+        gs = list(scene)
+        if not gs:
+            z = np.zeros
+            return cls(z((0, 3)), z((0, 4)), z((0, 3)), z(0), z((0, 16, 3)), device)
+        return cls(np.stack([np.asarray(g.mean, dtype=np.float64) for g in gs]),
+                   np.stack([np.asarray(g.rotation, dtype=np.float64) for g in gs]),
+                   np.stack([np.asarray(g.scale, dtype=np.float64) for g in gs]),
+                   np.array([float(g.opacity) for g in gs]),
+                   np.stack([np.asarray(g.sh, dtype=np.float64).reshape(-1, 3) for g in gs]),
+                   device)
+
+    def struct(self) -> _lib.StpScene:
+        s = _lib.StpScene()
+        s.means = self.means.data_ptr()
+        s.quats = self.quats.data_ptr()
+        s.scales = self.scales.data_ptr()
+        s.opacity = self.opacity.data_ptr()
+        s.sh = self.sh.data_ptr()
+        s.n = self.n
+        s.sh_coeffs = self.sh_coeffs
+        return s
+
+
+def make_camera(cam) -> _lib.StpCamera:
+    c = _lib.StpCamera()
+    R = np.asarray(cam.rotation, dtype=np.float64).reshape(9)
+    for i in range(9):
+        c.R[i] = float(R[i])
+    p = np.asarray(cam.position, dtype=np.float64).reshape(3)
+    for i in range(3):
+        c.pos[i] = float(p[i])
+    c.fx, c.fy = float(cam.fx), float(cam.fy)
+    c.cx = float(cam.cx) if cam.cx is not None else cam.width / 2.0
+    c.cy = float(cam.cy) if cam.cy is not None else cam.height / 2.0
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = False):
+    c = _lib.StpConfig()
+    c.eps = float(cfg.opacity_eps)
+    c.termination = float(cfg.termination)
+    c.alpha_cap = float(cfg.alpha_cap)
+    bg = np.asarray(cfg.background, dtype=np.float64).reshape(3)
+    for i in range(3):
+        c.bg[i] = float(bg[i])
+    c.near_plane = float(cfg.near)
+    c.guard = float(cfg.guard_band)
+    c.dilation = float(cfg.dilation)
+    c.inv_scale_clamp = float(cfg.inv_scale_clamp)
+    c.tile_size = int(cfg.tile_size)
+    c.q_tail, c.q_mid, c.q_head = int(mode.queue_tail), int(mode.queue_mid), int(mode.queue_head)
+    c.b_load, c.b_mid, c.b_head = int(mode.batch_load), int(mode.batch_mid), int(mode.batch_head)
+    c.mid_depth_at_center = int(bool(mode.mid_depth_at_center))
+    c.with_depth = int(bool(cfg.with_depth))
+    c.exact_culling = int(bool(cfg.exact_culling(mode)))
+    c.record_cap = int(record_cap)
+    c.flags = _lib.STP_FLAG_TIMINGS if timings else 0
+    return c
+
+
+def _raise(code: int, what: str):
+    msg = f"{what}: {_lib.error_string(code)}"
+    if code == _lib.STP_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise DataError(msg)
+
+
+class Workspace:
+    """Caller-owned device workspace (one per device/stream), grown on demand."""
+
+    def __init__(self, device):
+        self.device = device
+        self.buf = torch.empty(0, dtype=torch.uint8, device=device)
+
+    def ensure(self, n: int, width: int, height: int, entries: int) -> None:
+        need = int(_lib.load().stp_workspace_bytes(n, width, height, int(entries)))
+        if self.buf.numel() < need:
+            self.buf = torch.empty(need, dtype=torch.uint8, device=self.device)
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    @property
+    def nbytes(self) -> int:
+        return self.buf.numel()
+
+    def layout(self, n, width, height) -> _lib.StpLayout:
+        L = _lib.StpLayout()
+        rc = _lib.load().stp_workspace_layout(n, width, height, self.nbytes, ctypes.byref(L))
+        if rc != _lib.STP_OK:
+            _raise(rc, "workspace layout")
+        return L
+
+
+_WORKSPACES: dict = {}
+
+
+def workspace_for(device) -> Workspace:
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = _WORKSPACES[key] = Workspace(device)
+    return ws
+
+
+class Renderer:
+    """Renders views of one device-resident scene; the building block of
+    ``render``, the multi-view driver and the benchmark.
+
+    ``render_into`` is asynchronous (no host sync) unless stats are requested.
+    """
+
+    def __init__(self, scene, mode=None, cfg: RenderConfig | None = None, device=None,
+                 entry_capacity: int | None = None):
+        self.scene = GaussianScene.from_any(scene, device)
+        self.device = self.scene.device
+        self.mode = mode if mode is not None else Hierarchical()
+        validate_mode(self.mode)
+        if not _is_hier(self.mode):
+            raise ConfigError(f"the B200 path implements the Hierarchical mode only, got "
+                              f"{mode_name(self.mode)}")
+        self.cfg = cfg if cfg is not None else RenderConfig()
+        self.lib = _lib.load()
+        self.ws = Workspace(self.device)
+        self.entry_capacity = entry_capacity
+        self.c_scene = self.scene.struct()
+        rc = self.lib.stp_validate_config(ctypes.byref(make_config(self.cfg, self.mode)))
+        if rc != _lib.STP_OK:
+            _raise(rc, "configuration")
+
+    def alloc_outputs(self, width, height, record_cap: int = 0, with_state: bool = False):
+        d = self.device
+        o = {"color": torch.empty((height, width, 3), dtype=torch.float32, device=d),
+             "transmittance": torch.empty((height, width), dtype=torch.float32, device=d)}
+        if self.cfg.with_depth:
+            o["depth"] = torch.empty((height, width), dtype=torch.float32, device=d)
+        if record_cap > 0:
+            o["rec_count"] = torch.empty((height, width), dtype=torch.int32, device=d)
+            o["rec_splat"] = torch.empty((height, width, record_cap), dtype=torch.int32, device=d)
+            o["rec_t"] = torch.empty((height, width, record_cap), dtype=torch.float32, device=d)
+            o["rec_alpha"] = torch.empty((height, width, record_cap), dtype=torch.float32, device=d)
+        if with_state:
+            o["state"] = torch.empty(max(1, self.scene.n), dtype=torch.uint8, device=d)
+        return o
+
+    @staticmethod
+    def outputs_struct(o: dict) -> _lib.StpOutputs:
+        s = _lib.StpOutputs()
+        for k in ("color", "transmittance", "depth", "rec_count", "rec_splat", "rec_t",
+                  "rec_alpha", "state"):
+            if k in o:
+                setattr(s, k, o[k].data_ptr())
+        return s
+
+    def _ensure(self, cam):
+        guess = self.entry_capacity or max(1 << 16, 8 * self.scene.n)
+        self.ws.ensure(self.scene.n, cam.width, cam.height, guess)
+
+    def render_into(self, cam, outs: dict, stats: bool = False, timings: bool = False,
+                    record_cap: int = 0, stream=None):
+        """One view into preallocated device outputs.  Returns StpStats when
+        ``stats`` (synchronising), else None (asynchronous)."""
+        c_cam = make_camera(cam)
+        self._ensure(cam)
+        c_cfg = make_config(self.cfg, self.mode, record_cap, timings)
+        c_out = self.outputs_struct(outs)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        st = _lib.StpStats() if stats else None
+        for attempt in range(3):
+            rc = self.lib.stp_render(ctypes.byref(self.c_scene), ctypes.byref(c_cam),
+                                     ctypes.byref(c_cfg), ctypes.c_void_p(self.ws.ptr),
+                                     self.ws.nbytes, ctypes.byref(c_out),
+                                     ctypes.byref(st) if st is not None else None,
+                                     ctypes.c_void_p(s))
+            if rc == _lib.STP_ERR_WORKSPACE_TOO_SMALL and st is not None:
+                need = int(st.bin_entries * 1.25) + 4096
+                self.entry_capacity = need
+                self.ws.ensure(self.scene.n, cam.width, cam.height, need)
+                continue
+            if rc != _lib.STP_OK:
+                _raise(rc, "stp_render")
+            return st
+        raise DataError("stp_render: workspace retry failed")
+
+    def frame(self, cam, device_output: bool = False) -> FrameOutput:
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        rec_cap = 64 if cfg.capture_records else 0
+        while True:
+            outs = self.alloc_outputs(cam.width, cam.height, rec_cap, with_state=True)
+            st = self.render_into(cam, outs, stats=True, timings=True, record_cap=rec_cap)
+            if rec_cap and int(outs["rec_count"].max().item()) > rec_cap:
+                rec_cap = int(outs["rec_count"].max().item())
+                continue
+            break
+        state = outs["state"][: self.scene.n]
+        kept = torch.nonzero(state == 0).flatten()
+        timings = {"project": st.ms_project / 1e3, "duplicate": st.ms_duplicate / 1e3,
+                   "sort": st.ms_sort / 1e3, "blend": st.ms_blend / 1e3}
+        stats = {
+            "mode": mode_name(self.mode),
+            "projection": {"input": int(st.input), "behind": int(st.behind),
+                           "guard": int(st.guard), "degenerate": int(st.degenerate),
+                           "kept": int(st.kept)},
+            "bin_entries": int(st.bin_entries),
+            "tiles": int(st.tiles),
+            "timings": timings,
+            "nonfinite_pixels": [],
+            "tie_runs": int(st.tie_runs),
+        }
+        if device_output:
+            out = FrameOutput(color=outs["color"], transmittance=outs["transmittance"],
+                              depth=outs.get("depth"), source_index=kept, stats=stats)
+            if rec_cap:
+                out.records = {k: outs[k] for k in ("rec_count", "rec_splat", "rec_t",
+                                                    "rec_alpha")}
+            timings["total"] = time.perf_counter() - t0
+            return out
+        color = outs["color"].double().cpu().numpy()
+        tn = outs["transmittance"].double().cpu().numpy()
+        depth = outs["depth"].double().cpu().numpy() if cfg.with_depth else None
+        src = kept.cpu().numpy().astype(np.int64)
+        if st.nonfinite_pixels:
+            bad = ~(np.isfinite(color).all(axis=2) & np.isfinite(tn))
+            ys, xs = np.nonzero(bad)
+            stats["nonfinite_pixels"] = [(int(x), int(y)) for y, x in zip(ys, xs)]
+        records = None
+        if rec_cap:
+            records = self._records(outs, src, cam)
+        timings["total"] = time.perf_counter() - t0
+        return FrameOutput(color=color, transmittance=tn, depth=depth, records=records,
+                           source_index=src, stats=stats)
+
+    def debug_bins(self, cam):
+        """Sorted (tile_id, gaussian_id, fp32 key bits) of the last frame rendered
+        with this renderer's workspace (parity dumps of K3-K5)."""
+        torch.cuda.current_stream(self.device).synchronize()
+        L = self.ws.layout(self.scene.n, cam.width, cam.height)
+        st = _lib.StpStats()
+        rc = self.lib.stp_read_stats(ctypes.c_void_p(self.ws.ptr), self.ws.nbytes, self.scene.n,
+                                     cam.width, cam.height, ctypes.byref(st),
+                                     ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        if rc != _lib.STP_OK:
+            _raise(rc, "stp_read_stats")
+        E = int(st.bin_entries)
+        ko = L.keys1 if L.final_buffer else L.keys0
+        vo = L.vals1 if L.final_buffer else L.vals0
+        keys = self.ws.buf[ko: ko + 8 * E].view(torch.int64).cpu().numpy().view(np.uint64)
+        vals = self.ws.buf[vo: vo + 4 * E].view(torch.int32).cpu().numpy()
+        return (keys >> np.uint64(32)).astype(np.int64), vals.astype(np.int64), \
+            (keys & np.uint64(0xffffffff)).astype(np.uint32)
+
+    @staticmethod
+    def _records(outs, src, cam):
+        cnt = outs["rec_count"].cpu().numpy()
+        spl = outs["rec_splat"].cpu().numpy()
+        tt = outs["rec_t"].double().cpu().numpy()
+        aa = outs["rec_alpha"].double().cpu().numpy()
+        # Gaussian id -> batch rank (projection preserves source order)
+        rank = np.searchsorted(src, spl)
+        recs = []
+        for y in range(cam.height):
+            row = []
+            for x in range(cam.width):
+                n = int(cnt[y, x])
+                row.append(PixelRecords(rank[y, x, :n].astype(np.int64), tt[y, x, :n].copy(),
+                                        aa[y, x, :n].copy()))
+            recs.append(row)
+        return recs
+
+
+_SCENE_CACHE: dict = {}
+
+
+def _scene_for(scene, device):
+    """Cache the device copy of a host scene (uploaded once, like weights)."""
+    if isinstance(scene, GaussianScene):
+        return scene
+    key = (id(scene), len(scene) if hasattr(scene, "__len__") else None)
+    hit = _SCENE_CACHE.get(key)
+    if hit is not None and hit[0] is scene:
+        return hit[1]
+    gs = GaussianScene.from_any(scene, device)
+    _SCENE_CACHE.clear()
+    _SCENE_CACHE[key] = (scene, gs)
+    return gs
+
+
+def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
+           device_output: bool = False, device=None) -> FrameOutput:
+    """Render one frame under the Hierarchical mode (rasterizer.py:595-698).
+
+    ``scene`` is a list of Gaussian3D, a dict of arrays/tensors in the drop-in
+    layout, or a GaussianScene.  Returns float64 numpy arrays like the
+    reference unless ``device_output`` (float32 device tensors)."""
+    mode = mode if mode is not None else Hierarchical()
+    cfg = cfg or RenderConfig()
+    validate_mode(mode)
+    if not _is_hier(mode):
+        raise ConfigError(f"the B200 path implements the Hierarchical mode only, got "
+                          f"{mode_name(mode)}")
+    dev = _require_cuda(device)
+    gs = _scene_for(scene, dev)
+    r = Renderer(gs, mode, cfg, dev)
+    ws = workspace_for(dev)
+    r.ws = ws
+    return r.frame(cam, device_output=device_output)
+
+
+def render_depth(scene, cam, mode=None, cfg: RenderConfig | None = None, **kw) -> FrameOutput:
+    """rasterizer.py:701-715."""
+    cfg = replace(cfg or RenderConfig(), with_depth=True)
+    return render(scene, cam, mode, cfg, **kw)
+
+
+def render_trajectory(scene, cameras, mode=None, cfg: RenderConfig | None = None,
+                      interpolate: int = 0, **kw) -> list:
+    """rasterizer.py:758-772 (interpolation of poses is host logic; only
+    ``interpolate=0`` is supported here)."""
+    if interpolate:
+        raise ConfigError("camera interpolation is not part of the B200 path")
+    frames = []
+    for i, cam in enumerate(cameras):
+        try:
+            frames.append(render(scene, cam, mode, cfg, **kw))
+        except Exception as exc:
+            raise DataError(f"frame {i}: {exc}") from exc
+    return frames

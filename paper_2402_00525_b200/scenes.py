@@ -147,6 +147,17 @@ CONFIGS = {
 }
 
 
+def config_cameras(name: str, n_views: int | None = None):
+    """Cameras of a config without generating its scene."""
+    name = name.upper()
+    if name == "C3":
+        return orbit_cameras(n_views or 256)
+    if name == "C5":
+        nv = n_views or 240
+        return orbit_cameras(nv, yaw0=-np.deg2rad(15), yaw_span=np.deg2rad(30))
+    return config_scene(name, n=16, n_views=n_views)[1]
+
+
 def config_scene(name: str, n: int | None = None, n_views: int | None = None):
     """(scene f32 arrays, cameras) for BASELINE.json configs C1..C5.
     ``n`` / ``n_views`` override the size for scaled-down parity runs."""
