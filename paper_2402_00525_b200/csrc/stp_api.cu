@@ -124,6 +124,8 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
   f.cam.fy = cam->fy;
   f.cam.cx = cam->cx;
   f.cam.cy = cam->cy;
+  f.cam.inv_fx = 1.0 / cam->fx;
+  f.cam.inv_fy = 1.0 / cam->fy;
   f.cam.W = cam->width;
   f.cam.H = cam->height;
   f.cfg.eps = cfg->eps;

@@ -21,25 +21,27 @@ constexpr int kTile = 16;
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 
-// Projected splat, one per kept Gaussian, indexed by Gaussian id.  144 B =
-// 9 x 16 B: everything K3 (duplicate) and K6 (render) gather per entry.
+// Projected splat, one per kept Gaussian, indexed by Gaussian id.  160 B =
+// 10 x 16 B: everything K3 (duplicate) and K6 (render) gather per entry.
 struct __align__(16) SplatRec {
-  double mx, my;        // mean2d (pixels)                            0
-  double ca, cb, cc;    // conic (a, b, c)                            16
-  double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr
-  double m[6];          // packed inverse covariance (m00,m11,m22,m01,m02,m12)  48
-  double q0, q1;        // inv_cov3 (mean - camera origin), x and y   96
-  float op;             // opacity                                    112
+  double mx, my;        // mean2d (pixels)                                   0
+  double ca, cb, cc;    // conic (a, b, c)                                   16
+  double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr  40
+  double m[6];          // packed inverse covariance (m00,m11,m22,m01,m02,m12) 48
+  double q0, q1;        // inv_cov3 (mean - camera origin), x and y          96
+  float op;             // opacity                                           112
   float c0, c1, c2;     // SH colour (lower-clamped at 0)
-  double q2;            // inv_cov3 (mean - camera origin), z         128
+  double q2;            // inv_cov3 (mean - camera origin), z                128
   int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)
+  double inv_a, inv_c;  // 1/a, 1/c for the Alg. 1 edge searches            144
 };
-static_assert(sizeof(SplatRec) == 144, "SplatRec must be 144 B");
+static_assert(sizeof(SplatRec) == 160, "SplatRec must be 160 B");
 
 struct DevCam {
   double R[9];
   double pos[3];
   double fx, fy, cx, cy;
+  double inv_fx, inv_fy;
   int W, H;
 };
 
@@ -70,10 +72,39 @@ enum Counter {
 // ---------------------------------------------------------------------------
 // Math shared by all kernels (float64).
 
+// Branch-free float64 division / rsqrt for the normal, finite operands of the
+// geometry: MUFU approximation + two Newton steps + one residual correction
+// (within an ulp of the correctly rounded result).
+__device__ __forceinline__ double rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+__device__ __forceinline__ double fdiv(double n, double d) {
+  double r = rcp_approx(d);
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  const double q = n * r;
+  return fma(r, fma(-d, q, n), q);
+}
+
+__device__ __forceinline__ double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+
 // max_points, tile_culling.py:55-88, for one splat and one closed rect.
+// The two edge searches divide by (dyy * c) and (dxx * a); with the rect
+// extents powers of two (16, 4, 2) this is a multiply by 1/c (1/a) and an
+// exact power-of-two scale.
 __device__ __forceinline__ void max_point(double mx, double my, double a, double b, double c,
-                                          double xmin, double xmax, double ymin, double ymax,
-                                          double& ox, double& oy) {
+                                          double inv_a, double inv_c, double xmin, double xmax,
+                                          double ymin, double ymax, double& ox, double& oy) {
   const bool inside_x = (mx >= xmin) && (mx <= xmax);
   const bool inside_y = (my >= ymin) && (my <= ymax);
   if (inside_x && inside_y) {
@@ -87,8 +118,8 @@ __device__ __forceinline__ void max_point(double mx, double my, double a, double
   const double dyy = (py == ymin) ? (ymax - ymin) : (ymin - ymax);
   const double rx = mx - px;
   const double ry = my - py;
-  double t_y = (b * rx + c * ry) / (dyy * c);
-  double t_x = (a * rx + b * ry) / (dxx * a);
+  double t_y = (b * rx + c * ry) * inv_c / dyy;
+  double t_x = (a * rx + b * ry) * inv_a / dxx;
   t_y = fmin(fmax(t_y, 0.0), 1.0);
   t_x = fmin(fmax(t_x, 0.0), 1.0);
   if (inside_x) t_y = 0.0;
@@ -114,12 +145,12 @@ __device__ __forceinline__ bool alpha_keep(double power, double thr, float op, d
 // rays_through_points (tile_culling.py:161-173): normalize(v @ R).
 __device__ __forceinline__ void ray_dir(const DevCam& cam, double x, double y, double& d0,
                                         double& d1, double& d2) {
-  const double v0 = (x - cam.cx) / cam.fx;
-  const double v1 = (y - cam.cy) / cam.fy;
+  const double v0 = (x - cam.cx) * cam.inv_fx;
+  const double v1 = (y - cam.cy) * cam.inv_fy;
   d0 = v0 * cam.R[0] + v1 * cam.R[3] + cam.R[6];
   d1 = v0 * cam.R[1] + v1 * cam.R[4] + cam.R[7];
   d2 = v0 * cam.R[2] + v1 * cam.R[5] + cam.R[8];
-  const double inv = 1.0 / sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+  const double inv = frsqrt(d0 * d0 + d1 * d1 + d2 * d2);
   d0 *= inv;
   d1 *= inv;
   d2 *= inv;
@@ -131,7 +162,7 @@ __device__ __forceinline__ double blend_depth(const double* m, double q0, double
   const double num = d0 * q0 + d1 * q1 + d2 * q2;
   const double den = (d0 * d0) * m[0] + (d1 * d1) * m[1] + (d2 * d2) * m[2] +
                      (2 * d0 * d1) * m[3] + (2 * d0 * d2) * m[4] + (2 * d1 * d2) * m[5];
-  return num / den;
+  return fdiv(num, den);
 }
 
 // Monotone fp32 sort key of a float64 depth: round-to-nearest, -0 -> +0,
@@ -159,11 +190,12 @@ __device__ __forceinline__ double shfl_xor_d(double v, int m) {
 
 // Tile-level exact cull for splat `r` at tile (tx, ty) (rasterizer.py:334-339).
 __device__ __forceinline__ bool tile_survives(double mx, double my, double a, double b, double c,
-                                              double thr, float op, double eps, int tx, int ty,
-                                              double& ptx, double& pty) {
+                                              double inv_a, double inv_c, double thr, float op,
+                                              double eps, int tx, int ty, double& ptx,
+                                              double& pty) {
   const double x0 = (double)(tx * kTile), x1 = (double)((tx + 1) * kTile);
   const double y0 = (double)(ty * kTile), y1 = (double)((ty + 1) * kTile);
-  max_point(mx, my, a, b, c, x0, x1, y0, y1, ptx, pty);
+  max_point(mx, my, a, b, c, inv_a, inv_c, x0, x1, y0, y1, ptx, pty);
   return alpha_keep(gpower(a, b, c, ptx - mx, pty - my), thr, op, eps);
 }
 

@@ -104,7 +104,7 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, do
 // Count (or, with kWrite, emit) the exact-culled tiles of one splat whose
 // rect is small enough to be walked by its own thread.
 struct SplatGeo {
-  double mx, my, a, b, c, thr;
+  double mx, my, a, b, c, ia, ic, thr;
   float op;
   int rx0, rx1, ry0, ry1;
 };
@@ -114,7 +114,7 @@ __device__ __forceinline__ uint32_t count_serial(const SplatGeo& g, const DevCfg
   for (int ty = g.ry0; ty <= g.ry1; ++ty)
     for (int tx = g.rx0; tx <= g.rx1; ++tx) {
       double px, py;
-      if (!cfg.exact || tile_survives(g.mx, g.my, g.a, g.b, g.c, g.thr, g.op, cfg.eps, tx, ty, px, py))
+      if (!cfg.exact || tile_survives(g.mx, g.my, g.a, g.b, g.c, g.ia, g.ic, g.thr, g.op, cfg.eps, tx, ty, px, py))
         ++n;
     }
   return n;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
   g.rx1 = 0;
   g.ry0 = 1;
   g.ry1 = 0;
-  g.mx = g.my = g.a = g.b = g.c = g.thr = 0.0;
+  g.mx = g.my = g.a = g.b = g.c = g.ia = g.ic = g.thr = 0.0;
   g.op = 0.f;
 
   if (valid) {
@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.ca = c / det;  // conic (:397)
           r.cb = -b / det;
           r.cc = a / det;
+          r.inv_a = 1.0 / r.ca;
+          r.inv_c = 1.0 / r.cc;
           // opacity-aware radius (:399-404)
           const float opf = __ldg(sc.opacity + i);
           const double op = opf;
@@ -287,6 +289,8 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           g.a = r.ca;
           g.b = r.cb;
           g.c = r.cc;
+          g.ia = r.inv_a;
+          g.ic = r.inv_c;
           g.thr = r.thr;
           g.op = r.op;
           g.rx0 = x0;
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     big &= big - 1;
     const double mx = shfl_d(g.mx, src), my = shfl_d(g.my, src);
     const double a = shfl_d(g.a, src), b = shfl_d(g.b, src), c = shfl_d(g.c, src);
+    const double ia = shfl_d(g.ia, src), ic = shfl_d(g.ic, src);
     const double thr = shfl_d(g.thr, src);
     const float op = __shfl_sync(kFull, g.op, src);
     const int rx0 = __shfl_sync(kFull, g.rx0, src), ry0 = __shfl_sync(kFull, g.ry0, src);
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     for (int t = lane; t < ar; t += 32) {
       const int tx = rx0 + t % ww, ty = ry0 + t / ww;
       double px, py;
-      if (!cfg.exact || tile_survives(mx, my, a, b, c, thr, op, cfg.eps, tx, ty, px, py)) ++c_local;
+      if (!cfg.exact || tile_survives(mx, my, a, b, c, ia, ic, thr, op, cfg.eps, tx, ty, px, py)) ++c_local;
     }
     c_local = warp_sum(c_local);
     if (lane == src) cnt = (uint32_t)c_local;
@@ -440,7 +445,8 @@ __device__ __forceinline__ void emit_entry(const SplatRec& r, const DevCam& cam,
 __device__ __forceinline__ bool dup_test(const SplatRec& r, const DevCfg& cfg, int tx, int ty,
                                          double& ptx, double& pty) {
   const bool keep =
-      tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.thr, r.op, cfg.eps, tx, ty, ptx, pty);
+      tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op, cfg.eps, tx, ty,
+                    ptx, pty);
   return !cfg.exact || keep;
 }
 

@@ -1,73 +1,122 @@
-// K6: hierarchical resort + front-to-back blend, one CTA per 16x16 tile.
+// K6: hierarchical resort + front-to-back blend.
 //
 // Exact restatement of hierarchy.render_tile (hierarchy.py:27-219; contract in
-// SURVEY.md Appendix A).  One warp owns two horizontally adjacent 4x4
-// sub-tiles; half-warp s = lane>>4 is sub-tile s, lane&15 its pixel.
+// SURVEY.md Appendix A).  Work unit = one 4x4 sub-tile = one warp; persistent
+// warps pull (tile, sub-tile) items in tile-major order from a global counter,
+// so long bins and early-terminated sub-tiles balance across the GPU.
 //
-//   load   : lane l evaluates bin entry pos+l against both 4x4 rects
-//            (max_points + alpha test + t_opt on the peak ray, float64),
+//   load   : lane l evaluates bin entry pos+l against the 4x4 rect
+//            (Alg. 1 peak, alpha test, t_opt on the peak ray; float64),
 //            hierarchy.py:190-199
-//   sort   : warp bitonic network on (d4, rank) for both sub-tiles at once,
-//            merged into the tail queue kept in shared memory (:200-207)
+//   sort   : warp bitonic network on (d4, rank), merged into the tail queue
+//            (shared memory) by rank counting (:200-207)
 //   drain  : while len(tail) > q_tail - 32 pop 16 -> push_mid (:178-182)
-//   mid    : lane (s, quad, group) re-keys 4 entries at its 2x2 rect, sorts
-//            them, and the four groups of a quad merge into its mid queue in
-//            order, popping 4 at a time while len(mid) >= q_mid (:147-176)
-//   pixel  : every lane consumes its quad's emitted stream: alpha, eps test,
-//            cap, pixel-ray t_opt, register insertion queue of q_head,
-//            blending the minimum on overflow (:93-113, 81-91)
+//   mid    : 32 lanes re-key 16 entries at the four 2x2 rects (2 per lane),
+//            lane pairs form sorted groups of 4, and each quad's groups merge
+//            into its mid queue in order, popping 4 while len >= q_mid
+//            (:147-176)
+//   pixel  : two lanes per pixel evaluate consecutive emitted entries
+//            (alpha, eps test, cap, pixel-ray t_opt; the expensive part) and
+//            the even lane inserts both, in order, into the pixel's register
+//            queue of q_head, blending the minimum on overflow (:93-113, 81-91)
 //   drain  : tail -> mids -> heads at the end of the bin (:210-217)
 //
-// Termination (:187-189) is checked per batch for the warp's 32 pixels; a
-// terminated pixel's blends are no-ops, so stopping at warp granularity is
-// output-identical.  Sub-tiles / quads outside the image run the same queues
-// (their rects stay full size, hierarchy.py:124-142) and write nothing.
+// Termination (:187-189) is checked per batch for the sub-tile's 16 pixels,
+// exactly as the reference; a terminated pixel also skips its emits (its
+// blends are no-ops).  Rects stay full size at image borders
+// (hierarchy.py:124-142); pixels outside the image run as terminated.
 #include "stp_common.cuh"
 
 namespace stp {
 
-constexpr int kRenderThreads = 256;  // 8 warps = 16 sub-tiles = one tile
+constexpr int kWarpsPerBlock = 4;
+constexpr int kRenderThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kNoId = 0xffffffffu;
 
 __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t ib) {
   return da < db || (da == db && ia < ib);
 }
 
-// Per-warp shared-memory queues for the two sub-tiles, addressed
-// arithmetically (no runtime-indexed pointer arrays): per sub-tile s a double
-// block [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4)] and an
-// id block [tail0 | tail1 | batch | mid | scratch | emitted 4*emcap], then
-// the small counters nm[2][4], ne[2][4].
+// ---------------------------------------------------------------------------
+// float64 exp(-p), p >= 0: exp(-p) = 2^-(k/64) * exp(-r), |r| <= ln2/128,
+// degree-6 Taylor (error < 3e-20) and a 64-entry table of 2^(-j/64).
+__device__ const double kExp2Tab[64] = {
+    0x1.0000000000000p+0, 0x1.fa7c1819e90d8p-1, 0x1.f50765b6e4540p-1, 0x1.efa1bee615a27p-1,
+    0x1.ea4afa2a490dap-1, 0x1.e502ee78b3ff6p-1, 0x1.dfc97337b9b5fp-1, 0x1.da9e603db3285p-1,
+    0x1.d5818dcfba487p-1, 0x1.d072d4a07897cp-1, 0x1.cb720dcef9069p-1, 0x1.c67f12e57d14bp-1,
+    0x1.c199bdd85529cp-1, 0x1.bcc1e904bc1d2p-1, 0x1.b7f76f2fb5e47p-1, 0x1.b33a2b84f15fbp-1,
+    0x1.ae89f995ad3adp-1, 0x1.a9e6b5579fdbfp-1, 0x1.a5503b23e255dp-1, 0x1.a0c667b5de565p-1,
+    0x1.9c49182a3f090p-1, 0x1.97d829fde4e50p-1, 0x1.93737b0cdc5e5p-1, 0x1.8f1ae99157736p-1,
+    0x1.8ace5422aa0dbp-1, 0x1.868d99b4492edp-1, 0x1.82589994cce13p-1, 0x1.7e2f336cf4e62p-1,
+    0x1.7a11473eb0187p-1, 0x1.75feb564267c9p-1, 0x1.71f75e8ec5f74p-1, 0x1.6dfb23c651a2fp-1,
+    0x1.6a09e667f3bcdp-1, 0x1.6623882552225p-1, 0x1.6247eb03a5585p-1, 0x1.5e76f15ad2148p-1,
+    0x1.5ab07dd485429p-1, 0x1.56f4736b527dap-1, 0x1.5342b569d4f82p-1, 0x1.4f9b2769d2ca7p-1,
+    0x1.4bfdad5362a27p-1, 0x1.486a2b5c13cd0p-1, 0x1.44e086061892dp-1, 0x1.4160a21f72e2ap-1,
+    0x1.3dea64c123422p-1, 0x1.3a7db34e59ff7p-1, 0x1.371a7373aa9cbp-1, 0x1.33c08b26416ffp-1,
+    0x1.306fe0a31b715p-1, 0x1.2d285a6e4030bp-1, 0x1.29e9df51fdee1p-1, 0x1.26b4565e27cddp-1,
+    0x1.2387a6e756238p-1, 0x1.2063b88628cd6p-1, 0x1.1d4873168b9aap-1, 0x1.1a35beb6fcb75p-1,
+    0x1.172b83c7d517bp-1, 0x1.1429aaea92de0p-1, 0x1.11301d0125b51p-1, 0x1.0e3ec32d3d1a2p-1,
+    0x1.0b5586cf9890fp-1, 0x1.0874518759bc8p-1, 0x1.059b0d3158574p-1, 0x1.02c9a3e778061p-1};
+
+__device__ __forceinline__ double exp_neg(double p, const double* tab) {
+  if (p > 700.0) return 0.0;
+  const double kd = rint(p * 0x1.71547652b82fep+6);  // p * 64 / ln2
+  const int k = (int)kd;
+  double r = fma(-kd, 0x1.62e42fefa39efp-7, p);  // p - k ln2/64 (hi)
+  r = fma(-kd, 0x1.abc9e3b39803fp-62, r);       // (lo)
+  // exp(-r), |r| <= ln2/128
+  double e = 1.0 / 720.0;
+  e = fma(e, -r, 1.0 / 120.0);
+  e = fma(e, -r, 1.0 / 24.0);
+  e = fma(e, -r, 1.0 / 6.0);
+  e = fma(e, -r, 0.5);
+  e = fma(e, -r, 1.0);
+  e = fma(e, -r, 1.0);
+  const int j = k & 63, ex = k >> 6;
+  // 2^-ex by exponent construction (ex <= 1010 here)
+  const double scale = __hiloint2double((1023 - ex) << 20, 0);
+  return tab[j] * e * scale;
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp shared-memory queues of one sub-tile, addressed arithmetically:
+// doubles [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4) |
+// groups 64], ids [same | emitted 4*emcap].
 struct WarpQ {
   double* dbase;
   uint32_t* ibase;
-  int* cnt;
-  int qt, qm, emcap, ds, is;
-  __device__ __forceinline__ double* td(int s, int c) const { return dbase + s * ds + c * qt; }
-  __device__ __forceinline__ uint32_t* ti(int s, int c) const { return ibase + s * is + c * qt; }
-  __device__ __forceinline__ double* bd(int s) const { return dbase + s * ds + 2 * qt; }
-  __device__ __forceinline__ uint32_t* bi(int s) const { return ibase + s * is + 2 * qt; }
-  __device__ __forceinline__ double* md(int s, int q) const { return dbase + s * ds + 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ uint32_t* mi(int s, int q) const { return ibase + s * is + 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ double* sd(int s, int q) const {
-    return dbase + s * ds + 2 * qt + 32 + 4 * qm + q * (qm + 4);
+  int qt, qm, emcap;
+  __device__ __forceinline__ double* td(int c) const { return dbase + c * qt; }
+  __device__ __forceinline__ uint32_t* ti(int c) const { return ibase + c * qt; }
+  __device__ __forceinline__ double* bd() const { return dbase + 2 * qt; }
+  __device__ __forceinline__ uint32_t* bi() const { return ibase + 2 * qt; }
+  __device__ __forceinline__ double* md(int q) const { return dbase + 2 * qt + 32 + q * qm; }
+  __device__ __forceinline__ uint32_t* mi(int q) const { return ibase + 2 * qt + 32 + q * qm; }
+  __device__ __forceinline__ double* sd(int q) const {
+    return dbase + 2 * qt + 32 + 4 * qm + q * (qm + 4);
   }
-  __device__ __forceinline__ uint32_t* si(int s, int q) const {
-    return ibase + s * is + 2 * qt + 32 + 4 * qm + q * (qm + 4);
+  __device__ __forceinline__ uint32_t* si(int q) const {
+    return ibase + 2 * qt + 32 + 4 * qm + q * (qm + 4);
   }
-  __device__ __forceinline__ uint32_t* em(int s, int q) const {
-    return ibase + s * is + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + q * emcap;
+  __device__ __forceinline__ double* gd(int q) const {
+    return dbase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
   }
-  __device__ __forceinline__ int& nm(int s, int q) const { return cnt[s * 4 + q]; }
-  __device__ __forceinline__ int& ne(int s, int q) const { return cnt[8 + s * 4 + q]; }
+  __device__ __forceinline__ uint32_t* gi(int q) const {
+    return ibase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
+  }
+  __device__ __forceinline__ uint32_t* em(int q) const {
+    return ibase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64 + q * emcap;
+  }
 };
 
-__host__ __device__ inline int emit_cap(int qm) { return qm + 20; }
-__host__ __device__ inline int q_ds(int qt, int qm) { return 2 * qt + 32 + 4 * qm + 4 * (qm + 4); }
+__host__ __device__ inline int emit_cap(int qm) { return qm + 16; }
+__host__ __device__ inline int q_ds(int qt, int qm) {
+  return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64;
+}
 __host__ __device__ inline int q_is(int qt, int qm) { return q_ds(qt, qm) + 4 * emit_cap(qm); }
 
 __host__ __device__ inline size_t warp_smem_bytes(int qt, int qm) {
-  size_t b = 2 * (size_t)q_ds(qt, qm) * 8 + 2 * (size_t)q_is(qt, qm) * 4 + 16 * 4;
+  const size_t b = (size_t)q_ds(qt, qm) * 8 + (size_t)q_is(qt, qm) * 4;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -76,11 +125,8 @@ __device__ inline WarpQ carve(unsigned char* base, int qt, int qm) {
   q.qt = qt;
   q.qm = qm;
   q.emcap = emit_cap(qm);
-  q.ds = q_ds(qt, qm);
-  q.is = q_is(qt, qm);
   q.dbase = reinterpret_cast<double*>(base);
-  q.ibase = reinterpret_cast<uint32_t*>(q.dbase + 2 * q.ds);
-  q.cnt = reinterpret_cast<int*>(q.ibase + 2 * q.is);
+  q.ibase = reinterpret_cast<uint32_t*>(q.dbase + q_ds(qt, qm));
   return q;
 }
 
@@ -89,19 +135,17 @@ struct Head {
   double t[QH];
   double a[QH];
   uint32_t id[QH];
-  float c0[QH], c1[QH], c2[QH];
   int n;
 };
 
 struct Pixel {
   double px, py;
-  double d0, d1, d2;            // unit pixel ray (rasterizer.py:405)
-  double f[6];                  // ray features (rasterizer.py:406)
-  double T;                     // transmittance (float64: the termination test)
+  double d0, d1, d2;  // unit pixel ray (rasterizer.py:405)
+  double f[6];        // ray features (rasterizer.py:406)
+  double T;           // transmittance (float64: the termination test)
   float C0, C1, C2, D;
-  int rc;                       // records written
-  bool in_img;
-  int64_t pix;                  // y * W + x
+  int rc;             // blend records written
+  int64_t pix;        // y * W + x, -1 outside the image
 };
 
 struct RenderArgs {
@@ -110,23 +154,24 @@ struct RenderArgs {
   const uint2* __restrict__ ranges;
   DevCam cam;
   DevCfg cfg;
-  int gw;
+  int gw, n_items;
   StpOutputs out;
   unsigned long long* counters;
 };
 
+// blend (hierarchy.py:81-91)
 __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, double al,
-                                      uint32_t id, float c0, float c1, float c2) {
-  // hierarchy.py:81-91
+                                      uint32_t id) {
   if (P.T < A.cfg.term) return;
+  const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
   const double w = al * P.T;
   const float wf = (float)w;
-  P.C0 += c0 * wf;
-  P.C1 += c1 * wf;
-  P.C2 += c2 * wf;
+  P.C0 += oc.y * wf;
+  P.C1 += oc.z * wf;
+  P.C2 += oc.w * wf;
   P.D += (float)(t * w);
-  if (A.cfg.rec_cap > 0 && P.in_img) {
-    if (P.rc < A.cfg.rec_cap) {
+  if (A.cfg.rec_cap > 0) {
+    if (P.rc < A.cfg.rec_cap && P.pix >= 0) {
       const int64_t o = P.pix * A.cfg.rec_cap + P.rc;
       A.out.rec_splat[o] = (int32_t)id;
       A.out.rec_t[o] = (float)t;
@@ -137,20 +182,20 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.T = P.T * (1.0 - al);
 }
 
-// emit_to_pixel (hierarchy.py:93-113) for one entry.
-template <int QH>
-__device__ __forceinline__ void emit(Pixel& P, Head<QH>& H, const RenderArgs& A, int qh,
-                                     uint32_t id) {
+// alpha / eps test / cap / pixel-ray t_opt of one emitted entry
+// (hierarchy.py:94-105).  Returns false when the entry is dropped.
+__device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, uint32_t id,
+                                          const double* tab, double& t, double& al) {
   const SplatRec* r = A.recs + id;
   const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
   const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
   const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
   const double dx = P.px - mxy.x, dy = P.py - mxy.y;
   const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
-  if (pw > ct.y + 1e-9) return;  // alpha < eps far from the boundary
-  const float4 oc = __ldg(reinterpret_cast<const float4*>(&r->op));
-  double al = (double)oc.x * exp(-pw);
-  if (al < A.cfg.eps) return;
+  if (pw > ct.y + 1e-9) return false;  // alpha < eps, away from the boundary
+  const float op = __ldg(&r->op);
+  al = (double)op * exp_neg(pw, tab);
+  if (al < A.cfg.eps) return false;
   if (al > A.cfg.cap) al = A.cfg.cap;
   const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
   const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
@@ -160,90 +205,70 @@ __device__ __forceinline__ void emit(Pixel& P, Head<QH>& H, const RenderArgs& A,
   const double num = P.d0 * q01.x + P.d1 * q01.y + P.d2 * q2;
   const double den = P.f[0] * m01.x + P.f[1] * m01.y + P.f[2] * m23.x + P.f[3] * m23.y +
                      P.f[4] * m45.x + P.f[5] * m45.y;
-  const double t = num / den;
-  // insort + pop-min-on-overflow
-  if (H.n < qh) {
-    bool placed = false;
-#pragma unroll
-    for (int i = QH - 1; i >= 0; --i) {
-      if (i > H.n) continue;
-      if (i > 0 && lt(t, id, H.t[i - 1], H.id[i - 1])) {
-        H.t[i] = H.t[i - 1];
-        H.a[i] = H.a[i - 1];
-        H.id[i] = H.id[i - 1];
-        H.c0[i] = H.c0[i - 1];
-        H.c1[i] = H.c1[i - 1];
-        H.c2[i] = H.c2[i - 1];
-      } else if (!placed) {
-        H.t[i] = t;
-        H.a[i] = al;
-        H.id[i] = id;
-        H.c0[i] = oc.y;
-        H.c1[i] = oc.z;
-        H.c2[i] = oc.w;
-        placed = true;
-      }
-    }
-    H.n++;
-  } else if (lt(t, id, H.t[0], H.id[0])) {
-    blend(P, A, t, al, id, oc.y, oc.z, oc.w);
-  } else {
-    blend(P, A, H.t[0], H.a[0], H.id[0], H.c0[0], H.c1[0], H.c2[0]);
-    bool placed = false;
+  t = fdiv(num, den);
+  return true;
+}
+
+// insort into the pixel queue; on overflow blend the minimum
+// (hierarchy.py:110-113).  Branch-free: empty slots hold (+inf, ~0), the
+// overflow case blends min(e, H[0]) and, if H[0] left, shifts the queue and
+// re-inserts e; insertion is a compare-and-select bubble over the slots.
+// EXACT: the queue size equals QH; else runtime qh <= QH.
+template <int QH, bool EXACT>
+__device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArgs& A, int qh_rt,
+                                          double t, double al, uint32_t id) {
+  const int qh = EXACT ? QH : qh_rt;
+  const bool full = H.n >= qh;
+  if (full) {
+    const bool e_min = lt(t, id, H.t[0], H.id[0]);
+    blend(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
+    if (e_min) return;
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
-      if (i >= qh || placed) continue;
-      const bool last = (i + 1 >= qh) || (i + 1 >= QH);
-      if (last || lt(t, id, H.t[(i + 1 < QH) ? i + 1 : i], H.id[(i + 1 < QH) ? i + 1 : i])) {
-        H.t[i] = t;
-        H.a[i] = al;
-        H.id[i] = id;
-        H.c0[i] = oc.y;
-        H.c1[i] = oc.z;
-        H.c2[i] = oc.w;
-        placed = true;
-      } else {
-        const int j = (i + 1 < QH) ? i + 1 : i;
-        H.t[i] = H.t[j];
-        H.a[i] = H.a[j];
-        H.id[i] = H.id[j];
-        H.c0[i] = H.c0[j];
-        H.c1[i] = H.c1[j];
-        H.c2[i] = H.c2[j];
-      }
+      const bool in = (i + 1 < QH) && (EXACT || i + 1 < qh);
+      H.t[i] = in ? H.t[(i + 1 < QH) ? i + 1 : i] : INFINITY;
+      H.a[i] = in ? H.a[(i + 1 < QH) ? i + 1 : i] : 0.0;
+      H.id[i] = in ? H.id[(i + 1 < QH) ? i + 1 : i] : kNoId;
     }
+  } else {
+    H.n++;
+  }
+  double xt = t, xa = al;
+  uint32_t xi = id;
+#pragma unroll
+  for (int i = 0; i < QH; ++i) {
+    const bool sw = lt(xt, xi, H.t[i], H.id[i]);
+    const double ht = H.t[i], ha = H.a[i];
+    const uint32_t hi = H.id[i];
+    H.t[i] = sw ? xt : ht;
+    H.a[i] = sw ? xa : ha;
+    H.id[i] = sw ? xi : hi;
+    xt = sw ? ht : xt;
+    xa = sw ? ha : xa;
+    xi = sw ? hi : xi;
   }
 }
 
-// Bitonic sort of one (d, id) pair per lane, ascending across the warp.
-__device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1, uint32_t& i1,
-                                           int lane) {
+// Bitonic sort of one (d, id) per lane, ascending across the warp.
+__device__ __forceinline__ void warp_sort(double& d, uint32_t& id, int lane) {
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      const double od0 = shfl_xor_d(d0, j);
-      const uint32_t oi0 = __shfl_xor_sync(kFull, i0, j);
-      const double od1 = shfl_xor_d(d1, j);
-      const uint32_t oi1 = __shfl_xor_sync(kFull, i1, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      const bool want_min = (lower == up);
-      const bool o_less0 = lt(od0, oi0, d0, i0);
-      const bool o_less1 = lt(od1, oi1, d1, i1);
-      if (want_min ? o_less0 : (!o_less0 && !(od0 == d0 && oi0 == i0))) {
-        d0 = od0;
-        i0 = oi0;
-      }
-      if (want_min ? o_less1 : (!o_less1 && !(od1 == d1 && oi1 == i1))) {
-        d1 = od1;
-        i1 = oi1;
+      const double od = shfl_xor_d(d, j);
+      const uint32_t oi = __shfl_xor_sync(kFull, id, j);
+      const bool want_min = (((lane & j) == 0) == ((lane & k) == 0));
+      const bool o_less = lt(od, oi, d, id);
+      const bool o_greater = lt(d, id, od, oi);
+      if (want_min ? o_less : o_greater) {
+        d = od;
+        id = oi;
       }
     }
   }
 }
 
-// number of (d,id) in sorted array a[0..n) strictly below (x, xi)
+// number of (d,id) in sorted a[0..n) strictly below (x, xi)
 __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai, int n, double x,
                                            uint32_t xi) {
   int lo = 0, hi = n;
@@ -255,302 +280,312 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
   return lo;
 }
 
-template <int QH>
-__global__ void __launch_bounds__(kRenderThreads) k_render(RenderArgs A) {
+template <int QH, bool EXACT>
+__global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh = A.cfg.q_head;
+  __shared__ double s_tab[64];
+  const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh_rt = A.cfg.q_head;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 64; i += kRenderThreads) s_tab[i] = kExp2Tab[i];
+  __syncthreads();
   const WarpQ Q = carve(smem_raw + warp * warp_smem_bytes(qt, qm), qt, qm);
-
-  const int tile = blockIdx.x;
-  const int tx = tile % A.gw, ty = tile / A.gw;
-  const int x0 = tx * kTile, y0 = ty * kTile;
-  const int sr = warp >> 1, sc = (warp & 1) * 2;  // sub-tile row, first sub-tile column
   const double term = A.cfg.term;
+  const int drain_lim = qt - 32;  // drain_tail(q_tail - batch_load)
 
-  // this lane's pixel
-  Pixel P;
-  const int ps = lane >> 4, pp = lane & 15, ppx = pp & 3, ppy = pp >> 2;
+  // pixel role: lane&15 = pixel (4x4 row-major), lane>>4 = emit parity
+  const int pp = lane & 15, ph = lane >> 4;
+  const int ppx = pp & 3, ppy = pp >> 2;
   const int pq = (ppy >> 1) * 2 + (ppx >> 1);
-  {
-    const int gx = x0 + (sc + ps) * 4 + ppx, gy = y0 + sr * 4 + ppy;
-    P.in_img = gx < A.cam.W && gy < A.cam.H;
-    P.pix = (int64_t)gy * A.cam.W + gx;
-    P.px = (double)gx + 0.5;
-    P.py = (double)gy + 0.5;
-    ray_dir(A.cam, P.px, P.py, P.d0, P.d1, P.d2);
-    P.f[0] = P.d0 * P.d0;
-    P.f[1] = P.d1 * P.d1;
-    P.f[2] = P.d2 * P.d2;
-    P.f[3] = 2 * P.d0 * P.d1;
-    P.f[4] = 2 * P.d0 * P.d2;
-    P.f[5] = 2 * P.d1 * P.d2;
-    P.T = P.in_img ? 1.0 : 0.0;
-    P.C0 = P.C1 = P.C2 = P.D = 0.f;
-    P.rc = 0;
-  }
-  Head<QH> H;
-  H.n = 0;
+  // push_mid role: quad, group, half of group
+  const int mq = lane >> 3, mg = (lane >> 1) & 3, mh = lane & 1;
 
-  const uint2 rg = A.ranges[tile];
-  const int start = (int)rg.x, k_total = (int)(rg.y - rg.x);
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = (int)atomicAdd(A.counters + C_WORK, 1ull);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= A.n_items) break;
+    const int tile = item >> 4, sub = item & 15;
+    const int tx = tile % A.gw, ty = tile / A.gw;
+    const int sx0 = tx * kTile + (sub & 3) * 4, sy0 = ty * kTile + (sub >> 2) * 4;
 
-  if (k_total > 0) {
-    // 4x4 rects of the two sub-tiles (hierarchy.py:124-127), always full size
-    double r4x[2], r4y[2];
-    r4x[0] = (double)(x0 + sc * 4);
-    r4x[1] = (double)(x0 + (sc + 1) * 4);
-    const double r4y0 = (double)(y0 + sr * 4);
-    r4y[0] = r4y[1] = r4y0;
-    // push_mid lane role: (sub s, quad q, group g)
-    const int ms = lane >> 4, mq = (lane >> 2) & 3, mg = lane & 3;
-    const double r2x0 = r4x[ms] + (mq & 1) * 2, r2y0 = r4y0 + (mq >> 1) * 2;
-
-    // tail state per sub-tile (warp-uniform): ping-pong buffer, head, length
-    int cur0 = 0, cur1 = 0, th0 = 0, th1 = 0, nt0 = 0, nt1 = 0;
-    if (lane < 16) Q.cnt[lane] = 0;
-    __syncwarp();
-
-    // push_mid for chunk sizes c[0], c[1] taken from the tail fronts
-    auto push_mid = [&](int c0, int c1) {
-      const int ce = ms ? c1 : c0;
-      double gd[4];
-      uint32_t gi[4];
-      const uint32_t* tip = Q.ti(ms, ms ? cur1 : cur0) + (ms ? th1 : th0);
+    Pixel P;
+    {
+      const int gx = sx0 + ppx, gy = sy0 + ppy;
+      const bool in_img = gx < A.cam.W && gy < A.cam.H;
+      P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
+      P.px = (double)gx + 0.5;
+      P.py = (double)gy + 0.5;
+      ray_dir(A.cam, P.px, P.py, P.d0, P.d1, P.d2);
+      P.f[0] = P.d0 * P.d0;
+      P.f[1] = P.d1 * P.d1;
+      P.f[2] = P.d2 * P.d2;
+      P.f[3] = 2 * P.d0 * P.d1;
+      P.f[4] = 2 * P.d0 * P.d2;
+      P.f[5] = 2 * P.d1 * P.d2;
+      P.T = in_img ? 1.0 : 0.0;
+      P.C0 = P.C1 = P.C2 = P.D = 0.f;
+      P.rc = 0;
+    }
+    Head<QH> H;
+    H.n = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = 4 * mg + u;
-        gd[u] = INFINITY;
-        gi[u] = kNoId;
-        if (e < ce) {
-          const uint32_t id = tip[e];
-          const SplatRec* r = A.recs + id;
+    for (int i = 0; i < QH; ++i) {
+      H.t[i] = INFINITY;
+      H.a[i] = 0.0;
+      H.id[i] = kNoId;
+    }
+
+    const uint2 rg = A.ranges[tile];
+    const int start = (int)rg.x, k_total = (int)(rg.y - rg.x);
+    const double r4x = (double)sx0, r4y = (double)sy0;
+    const double r2x = r4x + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
+
+    int cur = 0, th = 0, nt = 0, pos = 0;
+    // every quad receives the same chunks in the same groups, so all four mid
+    // queues always have the same length: nm / ne are warp-uniform
+    int nm = 0, ne = 0;
+
+    // One call site per phase (small code): each iteration either loads a
+    // batch, pops a tail chunk, or flushes the mids at the end of the bin.
+    while (k_total > 0) {
+      const int lim = (pos < k_total) ? drain_lim : 0;
+      int action;  // 0 load, 1 pop, 2 flush
+      if (nt > lim) action = 1;
+      else if (pos < k_total) action = 0;
+      else action = 2;
+
+      if (action == 0) {
+        // ---- termination check (hierarchy.py:187-189)
+        if (__all_sync(kFull, ph == 1 || P.T < term)) break;
+        // ---- load + 4x4 cull + d4 (hierarchy.py:190-199)
+        const int j = pos + lane;
+        double d = INFINITY;
+        uint32_t id = kNoId;
+        if (j < k_total) {
+          const uint32_t sid = A.vals[start + j];
+          const SplatRec* r = A.recs + sid;
+          const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
+          const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
+          const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+          const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
+          const float op = __ldg(&r->op);
           double ptx, pty;
-          if (A.cfg.mid_center) {
-            ptx = r2x0 + 1.0;
-            pty = r2y0 + 1.0;
-          } else {
-            max_point(r->mx, r->my, r->ca, r->cb, r->cc, r2x0, r2x0 + 2.0, r2y0, r2y0 + 2.0, ptx,
-                      pty);
-          }
-          double d0, d1, d2;
-          ray_dir(A.cam, ptx, pty, d0, d1, d2);
-          gd[u] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-          gi[u] = id;
-        }
-      }
-      // sort the group of 4 (sorting network)
-#define CSWAP(a, b)                                  \
-  if (lt(gd[b], gi[b], gd[a], gi[a])) {              \
-    const double td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_; \
-    const uint32_t ti_ = gi[a]; gi[a] = gi[b]; gi[b] = ti_; \
-  }
-      CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
-#undef CSWAP
-      // groups merge into the quad's mid queue in order
-      for (int gg = 0; gg < 4; ++gg) {
-        if (mg == gg && 4 * gg < ce) {
-          const int ng = min(4, ce - 4 * gg);
-          double* md = Q.md(ms, mq);
-          uint32_t* mi = Q.mi(ms, mq);
-          double* sd = Q.sd(ms, mq);
-          uint32_t* si = Q.si(ms, mq);
-          uint32_t* em = Q.em(ms, mq);
-          const int n = Q.nm(ms, mq);
-          int ne = Q.ne(ms, mq);
-          // two-pointer merge mid[0..n) with group[0..ng)
-          int a = 0, o = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            if (b >= ng) break;
-            while (a < n && lt(md[a], mi[a], gd[b], gi[b])) {
-              sd[o] = md[a];
-              si[o] = mi[a];
-              ++o;
-              ++a;
-            }
-            sd[o] = gd[b];
-            si[o] = gi[b];
-            ++o;
-          }
-          while (a < n) {
-            sd[o] = md[a];
-            si[o] = mi[a];
-            ++o;
-            ++a;
-          }
-          // while len(mid) >= q_mid: flush_mid pops 4 (hierarchy.py:168-176)
-          int h0 = 0;
-          while (o - h0 >= qm) {
-            for (int u = 0; u < 4; ++u) em[ne++] = si[h0 + u];
-            h0 += 4;
-          }
-          for (int u = h0; u < o; ++u) {
-            md[u - h0] = sd[u];
-            mi[u - h0] = si[u];
-          }
-          Q.nm(ms, mq) = o - h0;
-          Q.ne(ms, mq) = ne;
-        }
-        __syncwarp();
-      }
-    };
-
-    // consume the emitted streams
-    auto pixel_phase = [&]() {
-      __syncwarp();
-      const int n = Q.ne(ps, pq);
-      int nmax = n;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
-      const uint32_t* em = Q.em(ps, pq);
-      for (int e = 0; e < nmax; ++e)
-        if (e < n) emit<QH>(P, H, A, qh, em[e]);
-      __syncwarp();
-      if (lane < 8) Q.cnt[8 + lane] = 0;
-      __syncwarp();
-    };
-
-    const int drain_lim = qt - 32;  // drain_tail(q_tail - batch_load)
-    bool stopped = false;
-    for (int pos = 0; pos < k_total; pos += 32) {
-      if (__all_sync(kFull, P.T < term)) {
-        stopped = true;
-        break;
-      }
-      // ---- load + 4x4 cull + d4 (hierarchy.py:190-199)
-      const int j = pos + lane;
-      double d[2] = {INFINITY, INFINITY};
-      uint32_t ids[2] = {kNoId, kNoId};
-      if (j < k_total) {
-        const uint32_t id = A.vals[start + j];
-        const SplatRec* r = A.recs + id;
-        const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
-        const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-        const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
-        const float op = __ldg(&r->op);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          double ptx, pty;
-          max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, r4x[s], r4x[s] + 4.0, r4y[s], r4y[s] + 4.0,
+          max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4x + 4.0, r4y, r4y + 4.0,
                     ptx, pty);
           if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
                          A.cfg.eps)) {
             double d0, d1, d2;
             ray_dir(A.cam, ptx, pty, d0, d1, d2);
-            d[s] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-            ids[s] = id;
+            d = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+            id = sid;
+          }
+        }
+        pos += 32;
+        const int nk = __popc(__ballot_sync(kFull, id != kNoId));
+        if (nk == 0) continue;
+        warp_sort(d, id, lane);
+        // ---- merge the sorted batch into the tail (heap_merge, :201)
+        Q.bd()[lane] = d;
+        Q.bi()[lane] = id;
+        __syncwarp();
+        const double* td = Q.td(cur) + th;
+        const uint32_t* ti = Q.ti(cur) + th;
+        double* od = Q.td(cur ^ 1);
+        uint32_t* oi = Q.ti(cur ^ 1);
+        if (lane < nk) {
+          const int rk = count_below(td, ti, nt, d, id);
+          od[lane + rk] = d;
+          oi[lane + rk] = id;
+        }
+        for (int t = lane; t < nt; t += 32) {
+          const int rk = count_below(Q.bd(), Q.bi(), nk, td[t], ti[t]);
+          od[t + rk] = td[t];
+          oi[t + rk] = ti[t];
+        }
+        cur ^= 1;
+        th = 0;
+        nt += nk;
+        __syncwarp();
+        continue;
+      }
+
+      if (action == 1) {
+        // ---- push_mid(chunk of c = min(16, len(tail))) (hierarchy.py:147-169)
+        const int c = min(16, nt);
+        const uint32_t* tip = Q.ti(cur) + th;
+        double gd[4];
+        uint32_t gi[4];
+        // this lane re-keys entries 4*mg + 2*mh + {0,1} at quad mq's 2x2 rect
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = 4 * mg + 2 * mh + u;
+          gd[u] = INFINITY;
+          gi[u] = kNoId;
+          if (e < c) {
+            const uint32_t sid = tip[e];
+            const SplatRec* r = A.recs + sid;
+            double ptx, pty;
+            if (A.cfg.mid_center) {
+              ptx = r2x + 1.0;
+              pty = r2y + 1.0;
+            } else {
+              max_point(r->mx, r->my, r->ca, r->cb, r->cc, r->inv_a, r->inv_c, r2x, r2x + 2.0,
+                        r2y, r2y + 2.0, ptx, pty);
+            }
+            double d0, d1, d2;
+            ray_dir(A.cam, ptx, pty, d0, d1, d2);
+            gd[u] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+            gi[u] = sid;
+          }
+        }
+        // the partner lane holds the other half of the group
+        gd[2] = shfl_xor_d(gd[0], 1);
+        gi[2] = __shfl_xor_sync(kFull, gi[0], 1);
+        gd[3] = shfl_xor_d(gd[1], 1);
+        gi[3] = __shfl_xor_sync(kFull, gi[1], 1);
+#define CSWAP(a, b)                                       \
+  if (lt(gd[b], gi[b], gd[a], gi[a])) {                   \
+    const double td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_;  \
+    const uint32_t ti_ = gi[a]; gi[a] = gi[b]; gi[b] = ti_; \
+  }
+        CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
+#undef CSWAP
+        th += c;
+        nt -= c;
+        // stage the sorted groups: lane pair (mg, mh) holds group mg of quad mq
+        Q.gd(mq)[4 * mg + 2 * mh] = gd[2 * mh];
+        Q.gi(mq)[4 * mg + 2 * mh] = gi[2 * mh];
+        Q.gd(mq)[4 * mg + 2 * mh + 1] = gd[2 * mh + 1];
+        Q.gi(mq)[4 * mg + 2 * mh + 1] = gi[2 * mh + 1];
+        __syncwarp();
+        // groups merge into the quad's mid queue in order (:161-169): each
+        // step is a rank-parallel merge, 8 lanes per quad
+        {
+          const double* md = Q.md(mq);
+          const uint32_t* mi = Q.mi(mq);
+          double* sd = Q.sd(mq);
+          uint32_t* si = Q.si(mq);
+          uint32_t* em = Q.em(mq);
+          const int slot0 = lane & 7;
+          for (int gg = 0; 4 * gg < c; ++gg) {
+            const int ng = min(4, c - 4 * gg);
+            const int L = nm + ng;
+            const double* g_d = Q.gd(mq) + 4 * gg;
+            const uint32_t* g_i = Q.gi(mq) + 4 * gg;
+            for (int sl = slot0; sl < L; sl += 8) {
+              double x;
+              uint32_t xi;
+              int rk;
+              if (sl < nm) {
+                x = md[sl];
+                xi = mi[sl];
+                rk = sl;
+                for (int u = 0; u < ng; ++u) rk += lt(g_d[u], g_i[u], x, xi);
+              } else {
+                x = g_d[sl - nm];
+                xi = g_i[sl - nm];
+                rk = sl - nm;
+                for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
+              }
+              sd[rk] = x;
+              si[rk] = xi;
+            }
+            __syncwarp();
+            const int h0 = (L >= qm) ? 4 : 0;  // flush_mid pops 4 (:168-176)
+            for (int sl = slot0; sl < L; sl += 8) {
+              if (sl < h0) em[ne + sl] = si[sl];
+              else {
+                Q.md(mq)[sl - h0] = sd[sl];
+                Q.mi(mq)[sl - h0] = si[sl];
+              }
+            }
+            ne += h0;
+            nm = L - h0;
+            __syncwarp();
+          }
+        }
+      } else {
+        // ---- end of stream: every mid queue flushes completely, in order
+        for (int sl = lane & 7; sl < nm; sl += 8) Q.em(mq)[ne + sl] = Q.mi(mq)[sl];
+        ne += nm;
+        nm = 0;
+        __syncwarp();
+      }
+
+      // ---- pixel phase: consume the emitted streams (equal length per quad)
+      {
+        const uint32_t* em = Q.em(pq);
+        const double Tp = __shfl_sync(kFull, P.T, pp);  // the pixel's T, both lanes
+        for (int i = 0; i < ne; i += 2) {
+          const int e = i + ph;
+          double t = 0.0, al = 0.0;
+          uint32_t id = kNoId;
+          bool ok = false;
+          if (e < ne && Tp >= term) {
+            id = em[e];
+            ok = emit_eval(P, A, id, s_tab, t, al);
+          }
+          const double t1 = __shfl_down_sync(kFull, t, 16);
+          const double al1 = __shfl_down_sync(kFull, al, 16);
+          const uint32_t id1 = __shfl_down_sync(kFull, id, 16);
+          const bool ok1 = __shfl_down_sync(kFull, (int)ok, 16) != 0;
+          if (ph == 0) {
+            if (ok) head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
+            if (ok1) head_push<QH, EXACT>(P, H, A, qh_rt, t1, al1, id1);
           }
         }
       }
-      warp_sort2(d[0], ids[0], d[1], ids[1], lane);
-      int nk[2];
-      nk[0] = __popc(__ballot_sync(kFull, ids[0] != kNoId));
-      nk[1] = __popc(__ballot_sync(kFull, ids[1] != kNoId));
-      Q.bd(0)[lane] = d[0];
-      Q.bi(0)[lane] = ids[0];
-      Q.bd(1)[lane] = d[1];
-      Q.bi(1)[lane] = ids[1];
+      ne = 0;
       __syncwarp();
-      // ---- merge the sorted batch into the tail (heap_merge, :201)
+      if (action == 2) {
+        // heads drain in ascending (t, rank) (hierarchy.py:215-217)
+        if (ph == 0) {
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int nks = nk[s];
-        if (nks == 0) continue;
-        const int cs = s ? cur1 : cur0, ths = s ? th1 : th0, nts = s ? nt1 : nt0;
-        const double* td = Q.td(s, cs) + ths;
-        const uint32_t* ti = Q.ti(s, cs) + ths;
-        double* od = Q.td(s, cs ^ 1);
-        uint32_t* oi = Q.ti(s, cs ^ 1);
-        if (lane < nks) {
-          const int r = count_below(td, ti, nts, d[s], ids[s]);
-          od[lane + r] = d[s];
-          oi[lane + r] = ids[s];
+          for (int i = 0; i < QH; ++i)
+            if (i < H.n) blend(P, A, H.t[i], H.a[i], H.id[i]);
         }
-        for (int t = lane; t < nts; t += 32) {
-          const int r = count_below(Q.bd(s), Q.bi(s), nks, td[t], ti[t]);
-          od[t + r] = td[t];
-          oi[t + r] = ti[t];
-        }
-        if (s) {
-          cur1 ^= 1;
-          th1 = 0;
-          nt1 += nks;
-        } else {
-          cur0 ^= 1;
-          th0 = 0;
-          nt0 += nks;
-        }
-      }
-      __syncwarp();
-      // ---- drain_tail(q_tail - 32): pop 16 while len > limit
-      while (nt0 > drain_lim || nt1 > drain_lim) {
-        const int c0 = nt0 > drain_lim ? 16 : 0;
-        const int c1 = nt1 > drain_lim ? 16 : 0;
-        push_mid(c0, c1);
-        th0 += c0;
-        nt0 -= c0;
-        th1 += c1;
-        nt1 -= c1;
-        pixel_phase();
+        break;
       }
     }
-    if (!stopped) {
-      // ---- end of stream (hierarchy.py:210-217)
-      while (nt0 > 0 || nt1 > 0) {
-        const int c0 = min(16, nt0), c1 = min(16, nt1);
-        push_mid(c0, c1);
-        th0 += c0;
-        nt0 -= c0;
-        th1 += c1;
-        nt1 -= c1;
-        pixel_phase();
-      }
-      // flush every mid queue completely, in order
-      if (mg == 0) {
-        const int n = Q.nm(ms, mq);
-        uint32_t* em = Q.em(ms, mq);
-        const uint32_t* mi = Q.mi(ms, mq);
-        int ne = Q.ne(ms, mq);
-        for (int u = 0; u < n; ++u) em[ne++] = mi[u];
-        Q.ne(ms, mq) = ne;
-        Q.nm(ms, mq) = 0;
-      }
-      pixel_phase();
-      // heads drain in ascending (t, rank)
-#pragma unroll
-      for (int i = 0; i < QH; ++i)
-        if (i < H.n) blend(P, A, H.t[i], H.a[i], H.id[i], H.c0[i], H.c1[i], H.c2[i]);
-    }
-  }
 
-  if (P.in_img) {
-    const float T = (float)P.T;
-    const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
-    const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
-    const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
-    A.out.color[P.pix * 3 + 0] = c0;
-    A.out.color[P.pix * 3 + 1] = c1;
-    A.out.color[P.pix * 3 + 2] = c2;
-    A.out.transmittance[P.pix] = T;
-    if (A.out.depth) A.out.depth[P.pix] = P.D;
-    if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
-    if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
-      atomicAdd(A.counters + C_NONFINITE, 1ull);
+    if (ph == 0 && P.pix >= 0) {
+      const float T = (float)P.T;
+      const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
+      const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
+      const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
+      A.out.color[P.pix * 3 + 0] = c0;
+      A.out.color[P.pix * 3 + 1] = c1;
+      A.out.color[P.pix * 3 + 2] = c2;
+      A.out.transmittance[P.pix] = T;
+      if (A.out.depth) A.out.depth[P.pix] = P.D;
+      if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
+      if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
+        atomicAdd(A.counters + C_NONFINITE, 1ull);
+    }
   }
 }
 
-template <int QH>
-static void launch_render_t(const RenderArgs& A, int n_tiles, size_t smem, cudaStream_t s) {
+size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
+
+template <int QH, bool EXACT>
+static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_render<QH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int blocks_per_sm = 0, n_sm = 0;
+  if (smem != attr || blocks_per_sm == 0) {
+    cudaFuncSetAttribute(k_render<QH, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = smem;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT>,
+                                                  kRenderThreads, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  k_render<QH><<<n_tiles, kRenderThreads, smem, s>>>(A);
+  const int want = (A.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = min(want, n_sm * blocks_per_sm);
+  if (grid > 0) k_render<QH, EXACT><<<grid, kRenderThreads, smem, s>>>(A);
 }
-
-size_t render_smem_bytes(int qt, int qm) { return 8 * warp_smem_bytes(qt, qm); }
 
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
   RenderArgs A;
@@ -560,12 +595,18 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.cam = f.cam;
   A.cfg = f.cfg;
   A.gw = f.gw;
+  A.n_items = f.n_tiles * 16;
   A.out = out;
   A.counters = f.counters;
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
-  if (f.cfg.q_head <= 4) launch_render_t<4>(A, f.n_tiles, smem, s);
-  else if (f.cfg.q_head <= 8) launch_render_t<8>(A, f.n_tiles, smem, s);
-  else launch_render_t<16>(A, f.n_tiles, smem, s);
+  switch (f.cfg.q_head) {
+    case 1: launch_render_t<1, true>(A, smem, s); break;
+    case 2: launch_render_t<2, true>(A, smem, s); break;
+    case 4: launch_render_t<4, true>(A, smem, s); break;
+    case 8: launch_render_t<8, true>(A, smem, s); break;
+    case 16: launch_render_t<16, true>(A, smem, s); break;
+    default: launch_render_t<16, false>(A, smem, s); break;
+  }
 }
 
 }  // namespace stp

@@ -190,7 +190,8 @@ __device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ rec
   const SplatRec& r = recs[id];
   const int tx = tile % gw, ty = tile / gw;
   double ptx, pty;
-  max_point(r.mx, r.my, r.ca, r.cb, r.cc, (double)(tx * kTile), (double)((tx + 1) * kTile),
+  max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
+            (double)((tx + 1) * kTile),
             (double)(ty * kTile), (double)((ty + 1) * kTile), ptx, pty);
   double d0, d1, d2;
   ray_dir(cam, ptx, pty, d0, d1, d2);

@@ -54,7 +54,8 @@ class GaussianScene:
         self.opacity = t(opacity, ())
         n = self.means.shape[0]
         sh_t = torch.as_tensor(sh) if not isinstance(sh, torch.Tensor) else sh
-        sh_t = sh_t.to(device=dev, dtype=torch.float32).reshape(n, -1, 3)
+        sh_t = sh_t.to(device=dev, dtype=torch.float32)
+        sh_t = sh_t.reshape(n, -1, 3) if n else sh_t.reshape(0, 16, 3)[:, :16]
         k = sh_t.shape[1] if n else 16
         if k not in _SH_OK:
             raise DataError(f"sh must hold 1, 4, 9 or 16 coefficients per channel, got {k}")
