@@ -31,15 +31,16 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + \
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))] + \
         [os.path.join(os.path.dirname(HERE), "include", "stp.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra=()) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *ARCH, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    extra = list(extra) + os.environ.get("STP_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *ARCH, *FLAGS, *[e for e in extra if e], *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(CSRC, "ptxas.log")
     with open(log, "w") as f:
@@ -48,6 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libstp_b200.so")
     os.replace(LIB + ".tmp", LIB)
+    os.utime(LIB, None)
     if verbose:
         sys.stdout.write(r.stderr)
     return LIB

@@ -66,7 +66,8 @@ enum Counter {
   C_TIES = 8,
   C_PART = 16,      // 8 per-pass partition counters
   C_WORK = 24,      // render work counter
-  C_COUNT = 32
+  C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
+  C_COUNT = 48
 };
 
 // ---------------------------------------------------------------------------
@@ -83,17 +84,15 @@ __device__ __forceinline__ double rcp_approx(double x) {
 
 __device__ __forceinline__ double fdiv(double n, double d) {
   double r = rcp_approx(d);
-  r = fma(r, fma(-d, r, 1.0), r);
-  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);     // e -> e^2
   const double q = n * r;
-  return fma(r, fma(-d, q, n), q);
+  return fma(r, fma(-d, q, n), q);    // residual correction -> e^4
 }
 
 __device__ __forceinline__ double frsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
   return y * fma(-hx * y, y, 1.5);
 }

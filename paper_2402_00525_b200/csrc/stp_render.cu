@@ -33,6 +33,21 @@ constexpr int kWarpsPerBlock = 4;
 constexpr int kRenderThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kNoId = 0xffffffffu;
 
+// Optional phase profiler (-DSTP_PHASE_PROF): warp-cycles per phase are
+// accumulated into counters C_PROF.. (load, merge, push_mid, pixel, items).
+#ifdef STP_PHASE_PROF
+#define PROF_T0() long long _pt = clock64()
+#define PROF_ADD(slot)                                                              \
+  do {                                                                              \
+    const long long _pn = clock64();                                                \
+    if (lane == 0) atomicAdd(A.counters + C_PROF + (slot), (unsigned long long)(_pn - _pt)); \
+    _pt = _pn;                                                                      \
+  } while (0)
+#else
+#define PROF_T0() (void)0
+#define PROF_ADD(slot) (void)0
+#endif
+
 __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t ib) {
   return da < db || (da == db && ia < ib);
 }
@@ -141,7 +156,6 @@ struct Head {
 struct Pixel {
   double px, py;
   double d0, d1, d2;  // unit pixel ray (rasterizer.py:405)
-  double f[6];        // ray features (rasterizer.py:406)
   double T;           // transmittance (float64: the termination test)
   float C0, C1, C2, D;
   int rc;             // blend records written
@@ -202,9 +216,10 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
   const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
   const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
   const double q2 = __ldg(&r->q2);
+  // t_opt = (d.q) / (f(d).m6), ray_features (rasterizer.py:406) folded in
   const double num = P.d0 * q01.x + P.d1 * q01.y + P.d2 * q2;
-  const double den = P.f[0] * m01.x + P.f[1] * m01.y + P.f[2] * m23.x + P.f[3] * m23.y +
-                     P.f[4] * m45.x + P.f[5] * m45.y;
+  const double den = P.d0 * (P.d0 * m01.x + 2.0 * (P.d1 * m23.y + P.d2 * m45.x)) +
+                     P.d1 * (P.d1 * m01.y + 2.0 * P.d2 * m45.y) + P.d2 * P.d2 * m23.x;
   t = fdiv(num, den);
   return true;
 }
@@ -223,16 +238,23 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     const bool e_min = lt(t, id, H.t[0], H.id[0]);
     blend(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
     if (e_min) return;
+    // drop H[0], insert e at position c among H[1..qh-1]
+    int c = 0;
+#pragma unroll
+    for (int i = 1; i < QH; ++i)
+      if ((EXACT || i < qh) && lt(H.t[i], H.id[i], t, id)) ++c;
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
-      const bool in = (i + 1 < QH) && (EXACT || i + 1 < qh);
-      H.t[i] = in ? H.t[(i + 1 < QH) ? i + 1 : i] : INFINITY;
-      H.a[i] = in ? H.a[(i + 1 < QH) ? i + 1 : i] : 0.0;
-      H.id[i] = in ? H.id[(i + 1 < QH) ? i + 1 : i] : kNoId;
+      const int j = (i + 1 < QH) ? i + 1 : i;
+      const bool take_next = i < c;
+      const bool take_e = i == c;
+      H.t[i] = take_next ? H.t[j] : (take_e ? t : H.t[i]);
+      H.a[i] = take_next ? H.a[j] : (take_e ? al : H.a[i]);
+      H.id[i] = take_next ? H.id[j] : (take_e ? id : H.id[i]);
     }
-  } else {
-    H.n++;
+    return;
   }
+  H.n++;
   double xt = t, xa = al;
   uint32_t xi = id;
 #pragma unroll
@@ -280,8 +302,9 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
   return lo;
 }
 
-template <int QH, bool EXACT>
-__global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
+// QMX = 8: mid queues of at most 8 (loops statically bounded); 0: generic.
+template <int QH, bool EXACT, int QMX>
+__global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
   const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh_rt = A.cfg.q_head;
@@ -316,12 +339,6 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
       P.px = (double)gx + 0.5;
       P.py = (double)gy + 0.5;
       ray_dir(A.cam, P.px, P.py, P.d0, P.d1, P.d2);
-      P.f[0] = P.d0 * P.d0;
-      P.f[1] = P.d1 * P.d1;
-      P.f[2] = P.d2 * P.d2;
-      P.f[3] = 2 * P.d0 * P.d1;
-      P.f[4] = 2 * P.d0 * P.d2;
-      P.f[5] = 2 * P.d1 * P.d2;
       P.T = in_img ? 1.0 : 0.0;
       P.C0 = P.C1 = P.C2 = P.D = 0.f;
       P.rc = 0;
@@ -340,6 +357,8 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
     const double r4x = (double)sx0, r4y = (double)sy0;
     const double r2x = r4x + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
 
+    PROF_T0();
+    PROF_ADD(5);
     int cur = 0, th = 0, nt = 0, pos = 0;
     // every quad receives the same chunks in the same groups, so all four mid
     // queues always have the same length: nm / ne are warp-uniform
@@ -382,6 +401,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
         }
         pos += 32;
         const int nk = __popc(__ballot_sync(kFull, id != kNoId));
+        PROF_ADD(0);
         if (nk == 0) continue;
         warp_sort(d, id, lane);
         // ---- merge the sorted batch into the tail (heap_merge, :201)
@@ -406,6 +426,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
         th = 0;
         nt += nk;
         __syncwarp();
+        PROF_ADD(1);
         continue;
       }
 
@@ -472,31 +493,47 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
             const int L = nm + ng;
             const double* g_d = Q.gd(mq) + 4 * gg;
             const uint32_t* g_i = Q.gi(mq) + 4 * gg;
-            for (int sl = slot0; sl < L; sl += 8) {
-              double x;
-              uint32_t xi;
-              int rk;
-              if (sl < nm) {
-                x = md[sl];
-                xi = mi[sl];
-                rk = sl;
-                for (int u = 0; u < ng; ++u) rk += lt(g_d[u], g_i[u], x, xi);
-              } else {
-                x = g_d[sl - nm];
-                xi = g_i[sl - nm];
-                rk = sl - nm;
-                for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
+#pragma unroll
+            for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
+              for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
+                double x;
+                uint32_t xi;
+                int rk;
+                if (sl < nm) {
+                  x = md[sl];
+                  xi = mi[sl];
+                  rk = sl;
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (u < ng) rk += lt(g_d[u], g_i[u], x, xi);
+                } else {
+                  x = g_d[sl - nm];
+                  xi = g_i[sl - nm];
+                  rk = sl - nm;
+                  if (QMX) {
+#pragma unroll
+                    for (int u = 0; u < (QMX ? QMX : 1); ++u)
+                      if (u < nm) rk += lt(md[u], mi[u], x, xi);
+                  } else {
+                    for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
+                  }
+                }
+                sd[rk] = x;
+                si[rk] = xi;
+                if (QMX) break;
               }
-              sd[rk] = x;
-              si[rk] = xi;
             }
             __syncwarp();
             const int h0 = (L >= qm) ? 4 : 0;  // flush_mid pops 4 (:168-176)
-            for (int sl = slot0; sl < L; sl += 8) {
-              if (sl < h0) em[ne + sl] = si[sl];
-              else {
-                Q.md(mq)[sl - h0] = sd[sl];
-                Q.mi(mq)[sl - h0] = si[sl];
+#pragma unroll
+            for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
+              for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
+                if (sl < h0) em[ne + sl] = si[sl];
+                else {
+                  Q.md(mq)[sl - h0] = sd[sl];
+                  Q.mi(mq)[sl - h0] = si[sl];
+                }
+                if (QMX) break;
               }
             }
             ne += h0;
@@ -512,6 +549,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
         __syncwarp();
       }
 
+      PROF_ADD(2);
       // ---- pixel phase: consume the emitted streams (equal length per quad)
       {
         const uint32_t* em = Q.em(pq);
@@ -537,6 +575,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
       }
       ne = 0;
       __syncwarp();
+      PROF_ADD(3);
       if (action == 2) {
         // heads drain in ascending (t, rank) (hierarchy.py:215-217)
         if (ph == 0) {
@@ -548,6 +587,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
       }
     }
 
+    PROF_ADD(4);
     if (ph == 0 && P.pix >= 0) {
       const float T = (float)P.T;
       const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
@@ -567,15 +607,15 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
 
 size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
 
-template <int QH, bool EXACT>
+template <int QH, bool EXACT, int QMX>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
   static int blocks_per_sm = 0, n_sm = 0;
   if (smem != attr || blocks_per_sm == 0) {
-    cudaFuncSetAttribute(k_render<QH, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_render<QH, EXACT, QMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX>,
                                                   kRenderThreads, smem);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -584,7 +624,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   }
   const int want = (A.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = min(want, n_sm * blocks_per_sm);
-  if (grid > 0) k_render<QH, EXACT><<<grid, kRenderThreads, smem, s>>>(A);
+  if (grid > 0) k_render<QH, EXACT, QMX><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
@@ -599,13 +639,17 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.out = out;
   A.counters = f.counters;
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
+  if (f.cfg.q_mid > 8) {
+    launch_render_t<16, false, 0>(A, smem, s);
+    return;
+  }
   switch (f.cfg.q_head) {
-    case 1: launch_render_t<1, true>(A, smem, s); break;
-    case 2: launch_render_t<2, true>(A, smem, s); break;
-    case 4: launch_render_t<4, true>(A, smem, s); break;
-    case 8: launch_render_t<8, true>(A, smem, s); break;
-    case 16: launch_render_t<16, true>(A, smem, s); break;
-    default: launch_render_t<16, false>(A, smem, s); break;
+    case 1: launch_render_t<1, true, 8>(A, smem, s); break;
+    case 2: launch_render_t<2, true, 8>(A, smem, s); break;
+    case 4: launch_render_t<4, true, 8>(A, smem, s); break;
+    case 8: launch_render_t<8, true, 8>(A, smem, s); break;
+    case 16: launch_render_t<16, true, 8>(A, smem, s); break;
+    default: launch_render_t<16, false, 8>(A, smem, s); break;
   }
 }
 
