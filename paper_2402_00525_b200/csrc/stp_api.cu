@@ -195,7 +195,7 @@ int fill_stats(const void* ws, size_t ws_bytes, int64_t n, int32_t W, int32_t H,
   const int64_t ecap = max_capacity(n, W, H, ws_bytes);
   if (ecap < 0) return STP_ERR_WORKSPACE_TOO_SMALL;
   plan(n, W, H, ecap, L);
-  unsigned long long c[C_COUNT];
+  unsigned long long c[64];
   if (cudaMemcpyAsync(c, static_cast<const unsigned char*>(ws) + L.counters, sizeof(c),
                       cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return STP_ERR_CUDA;

@@ -67,7 +67,10 @@ enum Counter {
   C_PART = 16,      // 8 per-pass partition counters
   C_WORK = 24,      // render work counter
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
-  C_COUNT = 48
+  C_TILE = 40,      // render: global tile counter
+  C_SM = 64,        // render: per-SM sub-tile counters [256]
+  C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
+  C_COUNT = 320 + 256 * 16
 };
 
 // ---------------------------------------------------------------------------

@@ -322,12 +322,37 @@ __global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
   // push_mid role: quad, group, half of group
   const int mq = lane >> 3, mg = (lane >> 1) & 3, mh = lane & 1;
 
+  // Per-SM tile scheduling: tiles are pulled from a global counter, and the
+  // 16 sub-tiles of a tile go to warps of the same SM, so the tile's splat
+  // records are fetched into that SM's L1 once and shared by its 16 warps.
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  smid &= 255;
+  unsigned long long* sm_cnt = A.counters + C_SM + smid;
+  unsigned long long* sm_ring = A.counters + C_SMT + smid * 16;
   for (;;) {
-    int item = 0;
-    if (lane == 0) item = (int)atomicAdd(A.counters + C_WORK, 1ull);
-    item = __shfl_sync(kFull, item, 0);
-    if (item >= A.n_items) break;
-    const int tile = item >> 4, sub = item & 15;
+    int tile = -1, sub = 0;
+    if (lane == 0) {
+      const unsigned long long i = atomicAdd(sm_cnt, 1ull);
+      const unsigned long long tl = i >> 4;  // this SM's tl-th tile
+      sub = (int)(i & 15);
+      unsigned long long* slot = sm_ring + (tl & 15);
+      if (sub == 0) {
+        const int g = (int)atomicAdd(A.counters + C_TILE, 1ull);
+        const int gt = g < A.n_items / 16 ? g : -1;
+        atomicExch(slot, (tl << 32) | (unsigned long long)(gt + 2));
+        tile = gt;
+      } else {
+        unsigned long long v;
+        do {
+          v = *reinterpret_cast<volatile unsigned long long*>(slot);
+        } while ((v >> 32) != tl || (v & 0xffffffffull) == 0);
+        tile = (int)(v & 0xffffffffull) - 2;
+      }
+    }
+    tile = __shfl_sync(kFull, tile, 0);
+    sub = __shfl_sync(kFull, sub, 0);
+    if (tile < 0) break;
     const int tx = tile % A.gw, ty = tile / A.gw;
     const int sx0 = tx * kTile + (sub & 3) * 4, sy0 = ty * kTile + (sub >> 2) * 4;
 

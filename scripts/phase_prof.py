@@ -13,8 +13,7 @@ outs = r.alloc_outputs(cam.width, cam.height)
 for _ in range(2):
     st = r.render_into(cam, outs, stats=True, timings=True)
 L = r.ws.layout(r.scene.n, cam.width, cam.height)
-c = r.ws.buf[L.counters: L.counters + 48 * 8].view(torch.int64).cpu().numpy()
-print("counters", c.tolist(), "kept", st.kept, file=sys.stderr)
+c = r.ws.buf[L.counters: L.counters + 64 * 8].view(torch.int64).cpu().numpy()
 prof = c[32:38].astype(np.float64)
 names = ["load(+cull+d4)", "sort+merge", "push_mid", "pixel", "item_epilogue", "item_prologue"]
 tot = prof.sum()
