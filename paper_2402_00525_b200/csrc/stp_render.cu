@@ -1,29 +1,33 @@
 // K6: hierarchical resort + front-to-back blend.
 //
 // Exact restatement of hierarchy.render_tile (hierarchy.py:27-219; contract in
-// SURVEY.md Appendix A).  Work unit = one 4x4 sub-tile = one warp; persistent
-// warps pull (tile, sub-tile) items in tile-major order from a global counter,
-// so long bins and early-terminated sub-tiles balance across the GPU.
+// SURVEY.md Appendix A).  One warp owns a horizontally adjacent PAIR of 4x4
+// sub-tiles; each sub-tile runs its own tail / mid queues (shared memory), and
+// the warp's 32 lanes are its 32 pixels (lane>>4 = sub-tile, lane&15 = pixel).
+// Persistent warps take (tile, pair) items; the 8 pairs of a tile go to warps
+// of one SM (per-SM tile scheduling) so its splat records are fetched once.
 //
-//   load   : lane l evaluates bin entry pos+l against the 4x4 rect
-//            (Alg. 1 peak, alpha test, t_opt on the peak ray; float64),
+//   load   : lane l evaluates bin entry pos+l against both 4x4 rects (one
+//            record fetch, two float64 Alg. 1 peaks / alpha tests / t_opt),
 //            hierarchy.py:190-199
-//   sort   : warp bitonic network on (d4, rank), merged into the tail queue
-//            (shared memory) by rank counting (:200-207)
+//   sort   : warp bitonic network on (d4, rank) for both sub-tiles at once,
+//            merged into each tail by rank counting (:200-207)
 //   drain  : while len(tail) > q_tail - 32 pop 16 -> push_mid (:178-182)
-//   mid    : 32 lanes re-key 16 entries at the four 2x2 rects (2 per lane),
-//            lane pairs form sorted groups of 4, and each quad's groups merge
-//            into its mid queue in order, popping 4 while len >= q_mid
-//            (:147-176)
-//   pixel  : two lanes per pixel evaluate consecutive emitted entries
-//            (alpha, eps test, cap, pixel-ray t_opt; the expensive part) and
-//            the even lane inserts both, in order, into the pixel's register
-//            queue of q_head, blending the minimum on overflow (:93-113, 81-91)
+//   mid    : the 16 popped entries are re-keyed at the four 2x2 rects (2 per
+//            lane), lane pairs form sorted groups of 4 and each quad's groups
+//            merge into its mid queue in order (rank-parallel, 8 lanes per
+//            quad), popping 4 while len >= q_mid (:147-176).  Popped entries
+//            go to a per-quad FIFO ring.
+//   pixel  : one lane per pixel consumes its quad's ring: alpha, eps test,
+//            cap, pixel-ray t_opt and the register insertion queue of q_head
+//            that blends its minimum on overflow (:93-113, 81-91).  Rings
+//            decouple production from consumption so both sub-tiles' pixels
+//            are busy in the same rounds.
 //   drain  : tail -> mids -> heads at the end of the bin (:210-217)
 //
-// Termination (:187-189) is checked per batch for the sub-tile's 16 pixels,
-// exactly as the reference; a terminated pixel also skips its emits (its
-// blends are no-ops).  Rects stay full size at image borders
+// Per sub-tile termination (:187-189) is exact: a sub-tile stops when all
+// its 16 pixels have T < 1e-4 (blends of terminated pixels are no-ops, so
+// stopping is output-identical).  Rects stay full size at image borders
 // (hierarchy.py:124-142); pixels outside the image run as terminated.
 #include "stp_common.cuh"
 
@@ -91,58 +95,6 @@ __device__ __forceinline__ double exp_neg(double p, const double* tab) {
   // 2^-ex by exponent construction (ex <= 1010 here)
   const double scale = __hiloint2double((1023 - ex) << 20, 0);
   return tab[j] * e * scale;
-}
-
-// ---------------------------------------------------------------------------
-// Per-warp shared-memory queues of one sub-tile, addressed arithmetically:
-// doubles [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4) |
-// groups 64], ids [same | emitted 4*emcap].
-struct WarpQ {
-  double* dbase;
-  uint32_t* ibase;
-  int qt, qm, emcap;
-  __device__ __forceinline__ double* td(int c) const { return dbase + c * qt; }
-  __device__ __forceinline__ uint32_t* ti(int c) const { return ibase + c * qt; }
-  __device__ __forceinline__ double* bd() const { return dbase + 2 * qt; }
-  __device__ __forceinline__ uint32_t* bi() const { return ibase + 2 * qt; }
-  __device__ __forceinline__ double* md(int q) const { return dbase + 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ uint32_t* mi(int q) const { return ibase + 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ double* sd(int q) const {
-    return dbase + 2 * qt + 32 + 4 * qm + q * (qm + 4);
-  }
-  __device__ __forceinline__ uint32_t* si(int q) const {
-    return ibase + 2 * qt + 32 + 4 * qm + q * (qm + 4);
-  }
-  __device__ __forceinline__ double* gd(int q) const {
-    return dbase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
-  }
-  __device__ __forceinline__ uint32_t* gi(int q) const {
-    return ibase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
-  }
-  __device__ __forceinline__ uint32_t* em(int q) const {
-    return ibase + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64 + q * emcap;
-  }
-};
-
-__host__ __device__ inline int emit_cap(int qm) { return qm + 16; }
-__host__ __device__ inline int q_ds(int qt, int qm) {
-  return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64;
-}
-__host__ __device__ inline int q_is(int qt, int qm) { return q_ds(qt, qm) + 4 * emit_cap(qm); }
-
-__host__ __device__ inline size_t warp_smem_bytes(int qt, int qm) {
-  const size_t b = (size_t)q_ds(qt, qm) * 8 + (size_t)q_is(qt, qm) * 4;
-  return (b + 15) & ~(size_t)15;
-}
-
-__device__ inline WarpQ carve(unsigned char* base, int qt, int qm) {
-  WarpQ q;
-  q.qt = qt;
-  q.qm = qm;
-  q.emcap = emit_cap(qm);
-  q.dbase = reinterpret_cast<double*>(base);
-  q.ibase = reinterpret_cast<uint32_t*>(q.dbase + q_ds(qt, qm));
-  return q;
 }
 
 template <int QH>
@@ -290,6 +242,30 @@ __device__ __forceinline__ void warp_sort(double& d, uint32_t& id, int lane) {
   }
 }
 
+// Bitonic sort of two (d, id) arrays, one pair per lane each, ascending.
+__device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1, uint32_t& i1,
+                                           int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double od0 = shfl_xor_d(d0, j);
+      const uint32_t oi0 = __shfl_xor_sync(kFull, i0, j);
+      const double od1 = shfl_xor_d(d1, j);
+      const uint32_t oi1 = __shfl_xor_sync(kFull, i1, j);
+      const bool want_min = (((lane & j) == 0) == ((lane & k) == 0));
+      if (want_min ? lt(od0, oi0, d0, i0) : lt(d0, i0, od0, oi0)) {
+        d0 = od0;
+        i0 = oi0;
+      }
+      if (want_min ? lt(od1, oi1, d1, i1) : lt(d1, i1, od1, oi1)) {
+        d1 = od1;
+        i1 = oi1;
+      }
+    }
+  }
+}
+
 // number of (d,id) in sorted a[0..n) strictly below (x, xi)
 __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai, int n, double x,
                                            uint32_t xi) {
@@ -302,44 +278,84 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
   return lo;
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory queues of one sub-tile, addressed arithmetically:
+// doubles [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4) |
+// groups 64], ids [same layout | ring 4*R].
+__host__ __device__ inline int sub_nd(int qt, int qm) {
+  return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64;
+}
+__host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? 64 : 128; }
+__host__ __device__ inline int sub_ni(int qt, int qm) { return sub_nd(qt, qm) + 4 * ring_size(qm); }
+__host__ __device__ inline size_t warp_smem_bytes(int qt, int qm) {
+  return ((size_t)2 * sub_nd(qt, qm) * 8 + (size_t)2 * sub_ni(qt, qm) * 4 + 15) & ~(size_t)15;
+}
+
+struct SubQ {
+  double* d;
+  uint32_t* i;
+  int qt, qm;
+  __device__ __forceinline__ double* td(int c) const { return d + c * qt; }
+  __device__ __forceinline__ uint32_t* ti(int c) const { return i + c * qt; }
+  __device__ __forceinline__ double* bd() const { return d + 2 * qt; }
+  __device__ __forceinline__ uint32_t* bi() const { return i + 2 * qt; }
+  __device__ __forceinline__ int o_mid(int q) const { return 2 * qt + 32 + q * qm; }
+  __device__ __forceinline__ int o_scr(int q) const { return 2 * qt + 32 + 4 * qm + q * (qm + 4); }
+  __device__ __forceinline__ int o_grp(int q) const {
+    return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
+  }
+  __device__ __forceinline__ uint32_t* ring(int q, int R) const {
+    return i + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64 + q * R;
+  }
+};
+
 // QMX = 8: mid queues of at most 8 (loops statically bounded); 0: generic.
 template <int QH, bool EXACT, int QMX>
-__global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
   const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh_rt = A.cfg.q_head;
+  const int R = ring_size(qm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 64; i += kRenderThreads) s_tab[i] = kExp2Tab[i];
   __syncthreads();
-  const WarpQ Q = carve(smem_raw + warp * warp_smem_bytes(qt, qm), qt, qm);
+  unsigned char* wbase = smem_raw + warp * warp_smem_bytes(qt, qm);
+  const int nd = sub_nd(qt, qm), ni = sub_ni(qt, qm);
+  auto subq = [&](int s) {
+    SubQ q;
+    q.d = reinterpret_cast<double*>(wbase) + s * nd;
+    q.i = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(wbase) + 2 * nd) + s * ni;
+    q.qt = qt;
+    q.qm = qm;
+    return q;
+  };
   const double term = A.cfg.term;
   const int drain_lim = qt - 32;  // drain_tail(q_tail - batch_load)
 
-  // pixel role: lane&15 = pixel (4x4 row-major), lane>>4 = emit parity
-  const int pp = lane & 15, ph = lane >> 4;
+  // pixel role: sub-tile lane>>4, pixel lane&15 (4x4 row-major), quad
+  const int ps = lane >> 4, pp = lane & 15;
   const int ppx = pp & 3, ppy = pp >> 2;
   const int pq = (ppy >> 1) * 2 + (ppx >> 1);
   // push_mid role: quad, group, half of group
   const int mq = lane >> 3, mg = (lane >> 1) & 3, mh = lane & 1;
 
-  // Per-SM tile scheduling: tiles are pulled from a global counter, and the
-  // 16 sub-tiles of a tile go to warps of the same SM, so the tile's splat
-  // records are fetched into that SM's L1 once and shared by its 16 warps.
   unsigned smid;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   smid &= 255;
   unsigned long long* sm_cnt = A.counters + C_SM + smid;
   unsigned long long* sm_ring = A.counters + C_SMT + smid * 16;
+
   for (;;) {
-    int tile = -1, sub = 0;
+    // ---- work item: (tile, pair) with the 8 pairs of a tile on one SM
+    int tile = -1, pair = 0;
     if (lane == 0) {
       const unsigned long long i = atomicAdd(sm_cnt, 1ull);
-      const unsigned long long tl = i >> 4;  // this SM's tl-th tile
-      sub = (int)(i & 15);
+      const unsigned long long tl = i >> 3;
+      pair = (int)(i & 7);
       unsigned long long* slot = sm_ring + (tl & 15);
-      if (sub == 0) {
+      if (pair == 0) {
         const int g = (int)atomicAdd(A.counters + C_TILE, 1ull);
-        const int gt = g < A.n_items / 16 ? g : -1;
+        const int gt = g < A.n_items ? g : -1;
         atomicExch(slot, (tl << 32) | (unsigned long long)(gt + 2));
         tile = gt;
       } else {
@@ -351,14 +367,15 @@ __global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
       }
     }
     tile = __shfl_sync(kFull, tile, 0);
-    sub = __shfl_sync(kFull, sub, 0);
+    pair = __shfl_sync(kFull, pair, 0);
     if (tile < 0) break;
     const int tx = tile % A.gw, ty = tile / A.gw;
-    const int sx0 = tx * kTile + (sub & 3) * 4, sy0 = ty * kTile + (sub >> 2) * 4;
+    // pair p covers sub-tiles (row p>>1, columns 2*(p&1), 2*(p&1)+1)
+    const int sx0 = tx * kTile + (pair & 1) * 8, sy0 = ty * kTile + (pair >> 1) * 4;
 
     Pixel P;
     {
-      const int gx = sx0 + ppx, gy = sy0 + ppy;
+      const int gx = sx0 + ps * 4 + ppx, gy = sy0 + ppy;
       const bool in_img = gx < A.cam.W && gy < A.cam.H;
       P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
       P.px = (double)gx + 0.5;
@@ -379,32 +396,223 @@ __global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
 
     const uint2 rg = A.ranges[tile];
     const int start = (int)rg.x, k_total = (int)(rg.y - rg.x);
-    const double r4x = (double)sx0, r4y = (double)sy0;
-    const double r2x = r4x + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
-
+    const double r4y = (double)sy0;
     PROF_T0();
     PROF_ADD(5);
-    int cur = 0, th = 0, nt = 0, pos = 0;
-    // every quad receives the same chunks in the same groups, so all four mid
-    // queues always have the same length: nm / ne are warp-uniform
-    int nm = 0, ne = 0;
 
-    // One call site per phase (small code): each iteration either loads a
-    // batch, pops a tail chunk, or flushes the mids at the end of the bin.
-    while (k_total > 0) {
+    // per-sub-tile pipeline state (warp-uniform scalars; s selects)
+    int cur0 = 0, cur1 = 0, th0 = 0, th1 = 0, nt0 = 0, nt1 = 0, nm0 = 0, nm1 = 0;
+    int rh0 = 0, rh1 = 0, rt0 = 0, rt1 = 0;
+    bool prod0 = k_total > 0, prod1 = k_total > 0;  // still producing emits
+    int pos = 0;
+
+    // ---- push_mid for sub-tile s: pop c = min(16, len(tail)) entries and
+    // run them through the four mid queues (hierarchy.py:147-176)
+    auto push_mid = [&](int s) {
+      const SubQ Q = subq(s);
+      const int cur = s ? cur1 : cur0, th = s ? th1 : th0, nt = s ? nt1 : nt0;
+      int nm = s ? nm1 : nm0, rt = s ? rt1 : rt0;
+      const int c = min(16, nt);
+      const uint32_t* tip = Q.ti(cur) + th;
+      const double r2x = (double)(sx0 + 4 * s) + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
+      double gd[4];
+      uint32_t gi[4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = 4 * mg + 2 * mh + u;
+        gd[u] = INFINITY;
+        gi[u] = kNoId;
+        if (e < c) {
+          const uint32_t sid = tip[e];
+          const SplatRec* r = A.recs + sid;
+          double ptx, pty;
+          if (A.cfg.mid_center) {
+            ptx = r2x + 1.0;
+            pty = r2y + 1.0;
+          } else {
+            const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
+            const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
+            const double cc = __ldg(&r->cc);
+            const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
+            max_point(mxy.x, mxy.y, ab.x, ab.y, cc, inv.x, inv.y, r2x, r2x + 2.0, r2y, r2y + 2.0,
+                      ptx, pty);
+          }
+          double d0, d1, d2;
+          ray_dir(A.cam, ptx, pty, d0, d1, d2);
+          gd[u] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+          gi[u] = sid;
+        }
+      }
+      gd[2] = shfl_xor_d(gd[0], 1);
+      gi[2] = __shfl_xor_sync(kFull, gi[0], 1);
+      gd[3] = shfl_xor_d(gd[1], 1);
+      gi[3] = __shfl_xor_sync(kFull, gi[1], 1);
+#define CSWAP(a, b)                                        \
+  if (lt(gd[b], gi[b], gd[a], gi[a])) {                    \
+    const double td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_;   \
+    const uint32_t ti_ = gi[a]; gi[a] = gi[b]; gi[b] = ti_; \
+  }
+      CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
+#undef CSWAP
+      double* gdp = Q.d + Q.o_grp(mq);
+      uint32_t* gip = Q.i + Q.o_grp(mq);
+      gdp[4 * mg + 2 * mh] = gd[2 * mh];
+      gip[4 * mg + 2 * mh] = gi[2 * mh];
+      gdp[4 * mg + 2 * mh + 1] = gd[2 * mh + 1];
+      gip[4 * mg + 2 * mh + 1] = gi[2 * mh + 1];
+      __syncwarp();
+      double* md = Q.d + Q.o_mid(mq);
+      uint32_t* mi = Q.i + Q.o_mid(mq);
+      double* sd = Q.d + Q.o_scr(mq);
+      uint32_t* si = Q.i + Q.o_scr(mq);
+      uint32_t* ring = Q.ring(mq, R);
+      const int slot0 = lane & 7;
+      for (int gg = 0; 4 * gg < c; ++gg) {
+        const int ng = min(4, c - 4 * gg);
+        const double* g_d = gdp + 4 * gg;
+        const uint32_t* g_i = gip + 4 * gg;
+        if (QMX == 8 && qm == 8 && nm == 4 && ng == 4) {
+          // steady state: mid holds 4, a full group of 4 arrives, the merged 8
+          // emit their first 4 and keep the last 4.  Lane slot sl owns one
+          // element: its rank = index + #(other list < it), 4 comparisons.
+          const bool from_mid = slot0 < 4;
+          const int ix = slot0 & 3;
+          const double x = from_mid ? md[ix] : g_d[ix];
+          const uint32_t xi = from_mid ? mi[ix] : g_i[ix];
+          const double* od = from_mid ? g_d : md;
+          const uint32_t* oi = from_mid ? g_i : mi;
+          int rk = ix;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rk += lt(od[u], oi[u], x, xi);
+          __syncwarp();
+          if (rk < 4) ring[(rt + rk) & (R - 1)] = xi;
+          else {
+            md[rk - 4] = x;
+            mi[rk - 4] = xi;
+          }
+          rt += 4;
+          __syncwarp();
+          continue;
+        }
+        const int L = nm + ng;
+#pragma unroll
+        for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
+          for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
+            double x;
+            uint32_t xi;
+            int rk;
+            if (sl < nm) {
+              x = md[sl];
+              xi = mi[sl];
+              rk = sl;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (u < ng) rk += lt(g_d[u], g_i[u], x, xi);
+            } else {
+              x = g_d[sl - nm];
+              xi = g_i[sl - nm];
+              rk = sl - nm;
+              if (QMX) {
+#pragma unroll
+                for (int u = 0; u < (QMX ? QMX : 1); ++u)
+                  if (u < nm) rk += lt(md[u], mi[u], x, xi);
+              } else {
+                for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
+              }
+            }
+            sd[rk] = x;
+            si[rk] = xi;
+            if (QMX) break;
+          }
+        }
+        __syncwarp();
+        const int h0 = (L >= qm) ? 4 : 0;  // flush_mid pops 4 (:168-176)
+#pragma unroll
+        for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
+          for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
+            if (sl < h0) ring[(rt + sl) & (R - 1)] = si[sl];
+            else {
+              md[sl - h0] = sd[sl];
+              mi[sl - h0] = si[sl];
+            }
+            if (QMX) break;
+          }
+        }
+        rt += h0;
+        nm = L - h0;
+        __syncwarp();
+      }
+      if (s) {
+        th1 += c;
+        nt1 -= c;
+        nm1 = nm;
+        rt1 = rt;
+      } else {
+        th0 += c;
+        nt0 -= c;
+        nm0 = nm;
+        rt0 = rt;
+      }
+    };
+
+    // Scheduling (any order is output-identical: each sub-tile's queues see
+    // exactly its own entry stream and each pixel its quad's emit stream):
+    //  - consume when every producing sub-tile has >= 16 pending emits (both
+    //    halves of the warp busy), or a ring is nearly full;
+    //  - otherwise produce: tails over the drain limit pop first (before any
+    //    load, as drain_tail follows every batch), then the next batch is
+    //    loaded for both sub-tiles, and at the end of the bin mids flush.
+    const int ring_full = R - 16 - qm;
+    for (;;) {
+      const int pa = rt0 - rh0, pb = rt1 - rh1;
+      const bool ready = (!prod0 || pa >= 16) && (!prod1 || pb >= 16);
+      if (pa > ring_full || pb > ring_full || (ready && pa + pb > 0)) {
+        // ================= consume: pixels take emits from their quad rings
+        const int rounds = (pa > 0 && pb > 0) ? min(pa, pb) : max(pa, pb);
+        {
+          const int pend = ps ? pb : pa;
+          const int base = ps ? rh1 : rh0;
+          const uint32_t* ring = subq(ps).ring(pq, R);
+          for (int e = 0; e < rounds; ++e) {
+            if (e < pend && P.T >= term) {
+              const uint32_t id = ring[(base + e) & (R - 1)];
+              double t, al;
+              if (emit_eval(P, A, id, s_tab, t, al))
+                head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
+            }
+          }
+        }
+        rh0 += min(rounds, pa);
+        rh1 += min(rounds, pb);
+        __syncwarp();
+        PROF_ADD(3);
+        continue;
+      }
+      if (!prod0 && !prod1) break;  // nothing pending, nothing to produce
+      // ================= produce
       const int lim = (pos < k_total) ? drain_lim : 0;
-      int action;  // 0 load, 1 pop, 2 flush
-      if (nt > lim) action = 1;
-      else if (pos < k_total) action = 0;
-      else action = 2;
-
-      if (action == 0) {
-        // ---- termination check (hierarchy.py:187-189)
-        if (__all_sync(kFull, ph == 1 || P.T < term)) break;
-        // ---- load + 4x4 cull + d4 (hierarchy.py:190-199)
+      const bool over0 = prod0 && nt0 > lim, over1 = prod1 && nt1 > lim;
+      if (over0 || over1) {
+        push_mid((over0 && (!over1 || pa <= pb)) ? 0 : 1);
+        PROF_ADD(2);
+        continue;
+      }
+      if (pos < k_total) {
+        // ---- termination check per sub-tile (hierarchy.py:187-189)
+        const unsigned bal = __ballot_sync(kFull, P.T < term);
+        if (prod0 && (bal & 0xffffu) == 0xffffu) {
+          prod0 = false;
+          rh0 = rt0;
+        }
+        if (prod1 && (bal >> 16) == 0xffffu) {
+          prod1 = false;
+          rh1 = rt1;
+        }
+        if (!prod0 && !prod1) continue;
+        // ---- load + 4x4 cull + d4 for both sub-tiles (hierarchy.py:190-199)
         const int j = pos + lane;
-        double d = INFINITY;
-        uint32_t id = kNoId;
+        double d[2] = {INFINITY, INFINITY};
+        uint32_t ids[2] = {kNoId, kNoId};
         if (j < k_total) {
           const uint32_t sid = A.vals[start + j];
           const SplatRec* r = A.recs + sid;
@@ -413,207 +621,94 @@ __global__ void __launch_bounds__(kRenderThreads, 5) k_render(RenderArgs A) {
           const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
           const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
           const float op = __ldg(&r->op);
-          double ptx, pty;
-          max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4x + 4.0, r4y, r4y + 4.0,
-                    ptx, pty);
-          if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
-                         A.cfg.eps)) {
-            double d0, d1, d2;
-            ray_dir(A.cam, ptx, pty, d0, d1, d2);
-            d = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-            id = sid;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (s ? !prod1 : !prod0) continue;
+            const double r4x = (double)(sx0 + 4 * s);
+            double ptx, pty;
+            max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4x + 4.0, r4y,
+                      r4y + 4.0, ptx, pty);
+            if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
+                           A.cfg.eps)) {
+              double d0, d1, d2;
+              ray_dir(A.cam, ptx, pty, d0, d1, d2);
+              d[s] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+              ids[s] = sid;
+            }
           }
         }
         pos += 32;
-        const int nk = __popc(__ballot_sync(kFull, id != kNoId));
+        int nk[2];
+        nk[0] = __popc(__ballot_sync(kFull, ids[0] != kNoId));
+        nk[1] = __popc(__ballot_sync(kFull, ids[1] != kNoId));
         PROF_ADD(0);
-        if (nk == 0) continue;
-        warp_sort(d, id, lane);
-        // ---- merge the sorted batch into the tail (heap_merge, :201)
-        Q.bd()[lane] = d;
-        Q.bi()[lane] = id;
-        __syncwarp();
-        const double* td = Q.td(cur) + th;
-        const uint32_t* ti = Q.ti(cur) + th;
-        double* od = Q.td(cur ^ 1);
-        uint32_t* oi = Q.ti(cur ^ 1);
-        if (lane < nk) {
-          const int rk = count_below(td, ti, nt, d, id);
-          od[lane + rk] = d;
-          oi[lane + rk] = id;
+        if (nk[0] + nk[1] == 0) continue;
+        warp_sort2(d[0], ids[0], d[1], ids[1], lane);
+        // ---- merge each sorted batch into its tail (heap_merge, :201)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (nk[s] == 0) continue;
+          const SubQ Q = subq(s);
+          const int cur = s ? cur1 : cur0, th = s ? th1 : th0, nt = s ? nt1 : nt0;
+          Q.bd()[lane] = d[s];
+          Q.bi()[lane] = ids[s];
+          __syncwarp();
+          const double* td = Q.td(cur) + th;
+          const uint32_t* ti = Q.ti(cur) + th;
+          double* od = Q.td(cur ^ 1);
+          uint32_t* oi = Q.ti(cur ^ 1);
+          if (lane < nk[s]) {
+            const int rk = count_below(td, ti, nt, d[s], ids[s]);
+            od[lane + rk] = d[s];
+            oi[lane + rk] = ids[s];
+          }
+          for (int t = lane; t < nt; t += 32) {
+            const int rk = count_below(Q.bd(), Q.bi(), nk[s], td[t], ti[t]);
+            od[t + rk] = td[t];
+            oi[t + rk] = ti[t];
+          }
+          __syncwarp();
+          if (s) {
+            cur1 ^= 1;
+            th1 = 0;
+            nt1 += nk[s];
+          } else {
+            cur0 ^= 1;
+            th0 = 0;
+            nt0 += nk[s];
+          }
         }
-        for (int t = lane; t < nt; t += 32) {
-          const int rk = count_below(Q.bd(), Q.bi(), nk, td[t], ti[t]);
-          od[t + rk] = td[t];
-          oi[t + rk] = ti[t];
-        }
-        cur ^= 1;
-        th = 0;
-        nt += nk;
-        __syncwarp();
         PROF_ADD(1);
         continue;
       }
-
-      if (action == 1) {
-        // ---- push_mid(chunk of c = min(16, len(tail))) (hierarchy.py:147-169)
-        const int c = min(16, nt);
-        const uint32_t* tip = Q.ti(cur) + th;
-        double gd[4];
-        uint32_t gi[4];
-        // this lane re-keys entries 4*mg + 2*mh + {0,1} at quad mq's 2x2 rect
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int e = 4 * mg + 2 * mh + u;
-          gd[u] = INFINITY;
-          gi[u] = kNoId;
-          if (e < c) {
-            const uint32_t sid = tip[e];
-            const SplatRec* r = A.recs + sid;
-            double ptx, pty;
-            if (A.cfg.mid_center) {
-              ptx = r2x + 1.0;
-              pty = r2y + 1.0;
-            } else {
-              max_point(r->mx, r->my, r->ca, r->cb, r->cc, r->inv_a, r->inv_c, r2x, r2x + 2.0,
-                        r2y, r2y + 2.0, ptx, pty);
-            }
-            double d0, d1, d2;
-            ray_dir(A.cam, ptx, pty, d0, d1, d2);
-            gd[u] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-            gi[u] = sid;
-          }
-        }
-        // the partner lane holds the other half of the group
-        gd[2] = shfl_xor_d(gd[0], 1);
-        gi[2] = __shfl_xor_sync(kFull, gi[0], 1);
-        gd[3] = shfl_xor_d(gd[1], 1);
-        gi[3] = __shfl_xor_sync(kFull, gi[1], 1);
-#define CSWAP(a, b)                                       \
-  if (lt(gd[b], gi[b], gd[a], gi[a])) {                   \
-    const double td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_;  \
-    const uint32_t ti_ = gi[a]; gi[a] = gi[b]; gi[b] = ti_; \
-  }
-        CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
-#undef CSWAP
-        th += c;
-        nt -= c;
-        // stage the sorted groups: lane pair (mg, mh) holds group mg of quad mq
-        Q.gd(mq)[4 * mg + 2 * mh] = gd[2 * mh];
-        Q.gi(mq)[4 * mg + 2 * mh] = gi[2 * mh];
-        Q.gd(mq)[4 * mg + 2 * mh + 1] = gd[2 * mh + 1];
-        Q.gi(mq)[4 * mg + 2 * mh + 1] = gi[2 * mh + 1];
-        __syncwarp();
-        // groups merge into the quad's mid queue in order (:161-169): each
-        // step is a rank-parallel merge, 8 lanes per quad
-        {
-          const double* md = Q.md(mq);
-          const uint32_t* mi = Q.mi(mq);
-          double* sd = Q.sd(mq);
-          uint32_t* si = Q.si(mq);
-          uint32_t* em = Q.em(mq);
-          const int slot0 = lane & 7;
-          for (int gg = 0; 4 * gg < c; ++gg) {
-            const int ng = min(4, c - 4 * gg);
-            const int L = nm + ng;
-            const double* g_d = Q.gd(mq) + 4 * gg;
-            const uint32_t* g_i = Q.gi(mq) + 4 * gg;
-#pragma unroll
-            for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
-              for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
-                double x;
-                uint32_t xi;
-                int rk;
-                if (sl < nm) {
-                  x = md[sl];
-                  xi = mi[sl];
-                  rk = sl;
-#pragma unroll
-                  for (int u = 0; u < 4; ++u)
-                    if (u < ng) rk += lt(g_d[u], g_i[u], x, xi);
-                } else {
-                  x = g_d[sl - nm];
-                  xi = g_i[sl - nm];
-                  rk = sl - nm;
-                  if (QMX) {
-#pragma unroll
-                    for (int u = 0; u < (QMX ? QMX : 1); ++u)
-                      if (u < nm) rk += lt(md[u], mi[u], x, xi);
-                  } else {
-                    for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
-                  }
-                }
-                sd[rk] = x;
-                si[rk] = xi;
-                if (QMX) break;
-              }
-            }
-            __syncwarp();
-            const int h0 = (L >= qm) ? 4 : 0;  // flush_mid pops 4 (:168-176)
-#pragma unroll
-            for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
-              for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
-                if (sl < h0) em[ne + sl] = si[sl];
-                else {
-                  Q.md(mq)[sl - h0] = sd[sl];
-                  Q.mi(mq)[sl - h0] = si[sl];
-                }
-                if (QMX) break;
-              }
-            }
-            ne += h0;
-            nm = L - h0;
-            __syncwarp();
-          }
-        }
-      } else {
-        // ---- end of stream: every mid queue flushes completely, in order
-        for (int sl = lane & 7; sl < nm; sl += 8) Q.em(mq)[ne + sl] = Q.mi(mq)[sl];
-        ne += nm;
-        nm = 0;
-        __syncwarp();
-      }
-
-      PROF_ADD(2);
-      // ---- pixel phase: consume the emitted streams (equal length per quad)
+      // ---- end of the bin, tails empty: flush a sub-tile's mid queues
       {
-        const uint32_t* em = Q.em(pq);
-        const double Tp = __shfl_sync(kFull, P.T, pp);  // the pixel's T, both lanes
-        for (int i = 0; i < ne; i += 2) {
-          const int e = i + ph;
-          double t = 0.0, al = 0.0;
-          uint32_t id = kNoId;
-          bool ok = false;
-          if (e < ne && Tp >= term) {
-            id = em[e];
-            ok = emit_eval(P, A, id, s_tab, t, al);
-          }
-          const double t1 = __shfl_down_sync(kFull, t, 16);
-          const double al1 = __shfl_down_sync(kFull, al, 16);
-          const uint32_t id1 = __shfl_down_sync(kFull, id, 16);
-          const bool ok1 = __shfl_down_sync(kFull, (int)ok, 16) != 0;
-          if (ph == 0) {
-            if (ok) head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
-            if (ok1) head_push<QH, EXACT>(P, H, A, qh_rt, t1, al1, id1);
-          }
+        const int fs = prod0 ? 0 : 1;
+        const SubQ Q = subq(fs);
+        const int nm = fs ? nm1 : nm0, rt = fs ? rt1 : rt0;
+        const uint32_t* mi = Q.i + Q.o_mid(mq);
+        uint32_t* ring = Q.ring(mq, R);
+        for (int sl = lane & 7; sl < nm; sl += 8) ring[(rt + sl) & (R - 1)] = mi[sl];
+        __syncwarp();
+        if (fs) {
+          rt1 += nm;
+          nm1 = 0;
+          prod1 = false;
+        } else {
+          rt0 += nm;
+          nm0 = 0;
+          prod0 = false;
         }
-      }
-      ne = 0;
-      __syncwarp();
-      PROF_ADD(3);
-      if (action == 2) {
-        // heads drain in ascending (t, rank) (hierarchy.py:215-217)
-        if (ph == 0) {
-#pragma unroll
-          for (int i = 0; i < QH; ++i)
-            if (i < H.n) blend(P, A, H.t[i], H.a[i], H.id[i]);
-        }
-        break;
       }
     }
-
+    // heads drain in ascending (t, rank) (hierarchy.py:215-217); no-ops for
+    // terminated sub-tiles
+#pragma unroll
+    for (int i = 0; i < QH; ++i)
+      if (i < H.n) blend(P, A, H.t[i], H.a[i], H.id[i]);
     PROF_ADD(4);
-    if (ph == 0 && P.pix >= 0) {
+
+    if (P.pix >= 0) {
       const float T = (float)P.T;
       const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
       const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
@@ -647,7 +742,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  const int want = (A.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = min(want, n_sm * blocks_per_sm);
   if (grid > 0) k_render<QH, EXACT, QMX><<<grid, kRenderThreads, smem, s>>>(A);
 }
@@ -660,7 +755,7 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.cam = f.cam;
   A.cfg = f.cfg;
   A.gw = f.gw;
-  A.n_items = f.n_tiles * 16;
+  A.n_items = f.n_tiles;
   A.out = out;
   A.counters = f.counters;
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
