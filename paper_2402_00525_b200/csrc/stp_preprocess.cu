@@ -8,14 +8,14 @@
 // id) in Gaussian order (rasterizer.py:328-350), so a stable LSD sort breaks
 // key ties by rank exactly like np.lexsort((rank, key, tile)).
 //
-// Rects larger than kLoadBalance tiles are enumerated cooperatively by the
-// whole warp (PAPER.md:589-599 load balancing, threshold 32).
+// The (splat, tile) pairs of a warp's 32 splats are enumerated cooperatively
+// (warp_expand), so lanes stay busy whatever the rect sizes (the paper's
+// load balancing, applied to every splat).
 #include "stp_common.cuh"
 
 namespace stp {
 
 constexpr int kPreThreads = 256;
-constexpr int kLoadBalance = 32;
 
 __constant__ double c_SH_C0 = 0.28209479177387814;
 __constant__ double c_SH_C1 = 0.4886025119029199;
@@ -71,22 +71,17 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, do
   }
   double acc[3] = {0.0, 0.0, 0.0};
   if (K == 16) {
-    // 192 B per Gaussian: 12 x float4
+    // 192 B per Gaussian: 12 x float4, consumed as they arrive
     const float4* p = reinterpret_cast<const float4*>(sh);
-    float v[48];
 #pragma unroll
     for (int u = 0; u < 12; ++u) {
       const float4 f = __ldg(p + u);
-      v[4 * u + 0] = f.x;
-      v[4 * u + 1] = f.y;
-      v[4 * u + 2] = f.z;
-      v[4 * u + 3] = f.w;
-    }
+      const float fv[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      acc[0] += b[k] * (double)v[3 * k + 0];
-      acc[1] += b[k] * (double)v[3 * k + 1];
-      acc[2] += b[k] * (double)v[3 * k + 2];
+      for (int w = 0; w < 4; ++w) {
+        const int idx = 4 * u + w;  // coefficient idx / 3, channel idx % 3
+        acc[idx % 3] += b[idx / 3] * (double)fv[w];
+      }
     }
   } else {
     for (int k = 0; k < K; ++k) {
@@ -101,23 +96,45 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, do
   out[2] = (float)fmax(acc[2] + 0.5, 0.0);
 }
 
-// Count (or, with kWrite, emit) the exact-culled tiles of one splat whose
-// rect is small enough to be walked by its own thread.
+// Culling geometry of one splat, staged in shared memory for the warp-level
+// load-balanced tile enumeration.
 struct SplatGeo {
   double mx, my, a, b, c, ia, ic, thr;
   float op;
   int rx0, rx1, ry0, ry1;
 };
+struct StagedGeo {
+  double mx, my, a, b, c, ia, ic, thr;
+  float op;
+  int rx0, ry0, wx;
+};
 
-__device__ __forceinline__ uint32_t count_serial(const SplatGeo& g, const DevCfg& cfg) {
-  uint32_t n = 0;
-  for (int ty = g.ry0; ty <= g.ry1; ++ty)
-    for (int tx = g.rx0; tx <= g.rx1; ++tx) {
-      double px, py;
-      if (!cfg.exact || tile_survives(g.mx, g.my, g.a, g.b, g.c, g.ia, g.ic, g.thr, g.op, cfg.eps, tx, ty, px, py))
-        ++n;
-    }
-  return n;
+// Warp-cooperative enumeration of the coarse (splat, tile) pairs of the 32
+// splats held by the warp's lanes (area = pairs of this lane's splat): every
+// round gives each lane one pair, so work is balanced whatever the rect sizes
+// (PAPER.md:589-599 load balancing, generalised).  fn(valid, owner, local)
+// is called warp-uniformly once per round; owner = lane owning the pair,
+// local = index of the pair in the owner's rect (row-major, rasterizer.py:331-332).
+template <class F>
+__device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
+  int incl = area;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  const int excl = incl - area;
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (__shfl_sync(kFull, incl, lo + step - 1) <= k) lo += step;
+    const int owner = lo < 31 ? lo : 31;
+    const int local = k - __shfl_sync(kFull, excl, owner);
+    fn(k < total, owner, local);
+  }
 }
 
 __global__ void __launch_bounds__(kPreThreads) k_preprocess(
@@ -302,31 +319,44 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     }
   }
 
-  // exact-culled tile count
+  // exact-culled tile count (rasterizer.py:334-339), load-balanced per warp
+  __shared__ StagedGeo s_geo[kPreThreads];
+  __shared__ uint32_t s_cnt[kPreThreads];
   const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
   const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
-  uint32_t cnt = 0;
-  if (area > 0 && area <= kLoadBalance) cnt = count_serial(g, cfg);
-  unsigned big = __ballot_sync(kFull, area > kLoadBalance);
-  while (big) {
-    const int src = __ffs(big) - 1;
-    big &= big - 1;
-    const double mx = shfl_d(g.mx, src), my = shfl_d(g.my, src);
-    const double a = shfl_d(g.a, src), b = shfl_d(g.b, src), c = shfl_d(g.c, src);
-    const double ia = shfl_d(g.ia, src), ic = shfl_d(g.ic, src);
-    const double thr = shfl_d(g.thr, src);
-    const float op = __shfl_sync(kFull, g.op, src);
-    const int rx0 = __shfl_sync(kFull, g.rx0, src), ry0 = __shfl_sync(kFull, g.ry0, src);
-    const int ww = __shfl_sync(kFull, wx, src), ar = __shfl_sync(kFull, area, src);
-    int c_local = 0;
-    for (int t = lane; t < ar; t += 32) {
-      const int tx = rx0 + t % ww, ty = ry0 + t / ww;
-      double px, py;
-      if (!cfg.exact || tile_survives(mx, my, a, b, c, ia, ic, thr, op, cfg.eps, tx, ty, px, py)) ++c_local;
-    }
-    c_local = warp_sum(c_local);
-    if (lane == src) cnt = (uint32_t)c_local;
+  {
+    StagedGeo& sg = s_geo[threadIdx.x];
+    sg.mx = g.mx;
+    sg.my = g.my;
+    sg.a = g.a;
+    sg.b = g.b;
+    sg.c = g.c;
+    sg.ia = g.ia;
+    sg.ic = g.ic;
+    sg.thr = g.thr;
+    sg.op = g.op;
+    sg.rx0 = g.rx0;
+    sg.ry0 = g.ry0;
+    sg.wx = wx;
+    s_cnt[threadIdx.x] = 0;
   }
+  __syncwarp();
+  const int wbase = threadIdx.x & ~31;
+  warp_expand(area, lane, [&](bool v, int owner, int local) {
+    bool keep = false;
+    if (v) {
+      const StagedGeo& o = s_geo[wbase + owner];
+      const int tx = o.rx0 + local % o.wx, ty = o.ry0 + local / o.wx;
+      double px, py;
+      keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
+                                          cfg.eps, tx, ty, px, py);
+    }
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned kb = __ballot_sync(kFull, keep);
+    if (v && lane == __ffs(peers) - 1 && (kb & peers)) s_cnt[wbase + owner] += __popc(kb & peers);
+    __syncwarp();
+  });
+  const uint32_t cnt = s_cnt[threadIdx.x];
   if (valid) {
     counts[i] = cnt;
     if (state) state[i] = (uint8_t)reason;
@@ -429,73 +459,56 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
 // ---------------------------------------------------------------------------
 // K3 duplicate.
 
-__device__ __forceinline__ void emit_entry(const SplatRec& r, const DevCam& cam, int tx, int ty,
-                                           double ptx, double pty, int gw, uint32_t id,
-                                           uint32_t pos, int64_t ecap, uint64_t* keys,
-                                           uint32_t* vals) {
-  double d0, d1, d2;
-  ray_dir(cam, ptx, pty, d0, d1, d2);  // rasterizer.py:349-350
-  const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
-  if ((int64_t)pos < ecap) {
-    keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << 32) | depth_key(depth);
-    vals[pos] = id;
-  }
-}
-
-__device__ __forceinline__ bool dup_test(const SplatRec& r, const DevCfg& cfg, int tx, int ty,
-                                         double& ptx, double& pty) {
-  const bool keep =
-      tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op, cfg.eps, tx, ty,
-                    ptx, pty);
-  return !cfg.exact || keep;
-}
-
 __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec* __restrict__ recs, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
     int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  __shared__ SplatRec s_rec[kPreThreads];
+  __shared__ uint32_t s_pos[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const uint32_t cnt = (i < n) ? counts[i] : 0;
-  int area = 0, wx = 1;
-  SplatRec r;
-  uint32_t base = 0;
+  int area = 0;
   if (cnt > 0) {
-    r = recs[i];
-    wx = r.rx1 - r.rx0 + 1;
-    area = wx * (r.ry1 - r.ry0 + 1);
-    base = offsets[i];
-    if (area <= kLoadBalance) {
-      uint32_t pos = base;
-      for (int ty = r.ry0; ty <= r.ry1; ++ty)
-        for (int tx = r.rx0; tx <= r.rx1; ++tx) {
-          double ptx, pty;
-          if (dup_test(r, cfg, tx, ty, ptx, pty))
-            emit_entry(r, cam, tx, ty, ptx, pty, gw, (uint32_t)i, pos++, ecap, keys, vals);
-        }
-    }
+    const SplatRec r = recs[i];
+    s_rec[threadIdx.x] = r;
+    area = (r.rx1 - r.rx0 + 1) * (r.ry1 - r.ry0 + 1);
+    s_pos[threadIdx.x] = offsets[i];
   }
-  unsigned big = __ballot_sync(kFull, area > kLoadBalance);
-  while (big) {
-    const int src = __ffs(big) - 1;
-    big &= big - 1;
-    const int64_t sid = __shfl_sync(kFull, i, src);
-    const SplatRec rs = recs[sid];  // broadcast load
-    const int ww = rs.rx1 - rs.rx0 + 1;
-    const int ar = ww * (rs.ry1 - rs.ry0 + 1);
-    uint32_t pos = __shfl_sync(kFull, base, src);
-    for (int t0 = 0; t0 < ar; t0 += 32) {
-      const int t = t0 + lane;
-      const int tx = rs.rx0 + t % ww, ty = rs.ry0 + t / ww;
-      double ptx = 0, pty = 0;
-      const bool keep = (t < ar) && dup_test(rs, cfg, tx, ty, ptx, pty);
-      const unsigned m = __ballot_sync(kFull, keep);
-      if (keep)
-        emit_entry(rs, cam, tx, ty, ptx, pty, gw, (uint32_t)sid,
-                   pos + __popc(m & ((1u << lane) - 1)), ecap, keys, vals);
-      pos += __popc(m);
+  __syncwarp();
+  const int wbase = threadIdx.x & ~31;
+  const unsigned lt_mask = (1u << lane) - 1;
+  warp_expand(area, lane, [&](bool v, int owner, int local) {
+    const SplatRec& r = s_rec[wbase + owner];
+    bool keep = false;
+    int tx = 0, ty = 0;
+    double ptx = 0.0, pty = 0.0;
+    if (v) {
+      const int w = r.rx1 - r.rx0 + 1;
+      tx = r.rx0 + local % w;
+      ty = r.ry0 + local / w;
+      keep = tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op, cfg.eps,
+                           tx, ty, ptx, pty);
+      if (!cfg.exact) keep = true;
     }
-  }
+    // deterministic slot: rank among this round's survivors of the same splat
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned kb = __ballot_sync(kFull, keep) & peers;
+    const uint32_t base = v ? s_pos[wbase + owner] : 0;
+    __syncwarp();
+    if (keep) {
+      double d0, d1, d2;
+      ray_dir(cam, ptx, pty, d0, d1, d2);  // rasterizer.py:349-350
+      const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+      const uint32_t pos = base + __popc(kb & lt_mask);
+      if ((int64_t)pos < ecap) {
+        keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << 32) | depth_key(depth);
+        vals[pos] = (uint32_t)(blockIdx.x * kPreThreads + wbase + owner);
+      }
+    }
+    if (v && lane == __ffs(peers) - 1 && kb) s_pos[wbase + owner] = base + __popc(kb);
+    __syncwarp();
+  });
 }
 
 // ---------------------------------------------------------------------------
