@@ -243,11 +243,13 @@ __device__ __forceinline__ void warp_sort(double& d, uint32_t& id, int lane) {
 }
 
 // Bitonic sort of two (d, id) arrays, one pair per lane each, ascending.
+// Rolled loops: the kernel is instruction-fetch bound, code size matters more
+// than the loop overhead here.
 __device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1, uint32_t& i1,
                                            int lane) {
-#pragma unroll
+#pragma unroll 1
   for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
       const double od0 = shfl_xor_d(d0, j);
       const uint32_t oi0 = __shfl_xor_sync(kFull, i0, j);
@@ -417,11 +419,11 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
       const double r2x = (double)(sx0 + 4 * s) + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
       double gd[4];
       uint32_t gi[4];
-#pragma unroll
+      gd[0] = gd[1] = INFINITY;
+      gi[0] = gi[1] = kNoId;
+#pragma unroll 1
       for (int u = 0; u < 2; ++u) {
         const int e = 4 * mg + 2 * mh + u;
-        gd[u] = INFINITY;
-        gi[u] = kNoId;
         if (e < c) {
           const uint32_t sid = tip[e];
           const SplatRec* r = A.recs + sid;
@@ -439,8 +441,14 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
           }
           double d0, d1, d2;
           ray_dir(A.cam, ptx, pty, d0, d1, d2);
-          gd[u] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-          gi[u] = sid;
+          const double dv = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+          if (u) {
+            gd[1] = dv;
+            gi[1] = sid;
+          } else {
+            gd[0] = dv;
+            gi[0] = sid;
+          }
         }
       }
       gd[2] = shfl_xor_d(gd[0], 1);
@@ -495,9 +503,10 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
           continue;
         }
         const int L = nm + ng;
-#pragma unroll
-        for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
-          for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
+#pragma unroll 1
+        for (int k = 0; k < 1; ++k) {
+#pragma unroll 1
+          for (int sl = slot0; sl < L; sl += 8) {
             double x;
             uint32_t xi;
             int rk;
@@ -505,37 +514,27 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
               x = md[sl];
               xi = mi[sl];
               rk = sl;
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (u < ng) rk += lt(g_d[u], g_i[u], x, xi);
+#pragma unroll 1
+              for (int u = 0; u < ng; ++u) rk += lt(g_d[u], g_i[u], x, xi);
             } else {
               x = g_d[sl - nm];
               xi = g_i[sl - nm];
               rk = sl - nm;
-              if (QMX) {
-#pragma unroll
-                for (int u = 0; u < (QMX ? QMX : 1); ++u)
-                  if (u < nm) rk += lt(md[u], mi[u], x, xi);
-              } else {
-                for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
-              }
+#pragma unroll 1
+              for (int u = 0; u < nm; ++u) rk += lt(md[u], mi[u], x, xi);
             }
             sd[rk] = x;
             si[rk] = xi;
-            if (QMX) break;
           }
         }
         __syncwarp();
         const int h0 = (L >= qm) ? 4 : 0;  // flush_mid pops 4 (:168-176)
-#pragma unroll
-        for (int k = 0; k < (QMX ? (QMX + 3 + 7) / 8 : 1); ++k) {
-          for (int sl = slot0 + 8 * k; sl < L; sl += 8) {
-            if (sl < h0) ring[(rt + sl) & (R - 1)] = si[sl];
-            else {
-              md[sl - h0] = sd[sl];
-              mi[sl - h0] = si[sl];
-            }
-            if (QMX) break;
+#pragma unroll 1
+        for (int sl = slot0; sl < L; sl += 8) {
+          if (sl < h0) ring[(rt + sl) & (R - 1)] = si[sl];
+          else {
+            md[sl - h0] = sd[sl];
+            mi[sl - h0] = si[sl];
           }
         }
         rt += h0;
@@ -611,8 +610,8 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
         if (!prod0 && !prod1) continue;
         // ---- load + 4x4 cull + d4 for both sub-tiles (hierarchy.py:190-199)
         const int j = pos + lane;
-        double d[2] = {INFINITY, INFINITY};
-        uint32_t ids[2] = {kNoId, kNoId};
+        double dA = INFINITY, dB = INFINITY;
+        uint32_t iA = kNoId, iB = kNoId;
         if (j < k_total) {
           const uint32_t sid = A.vals[start + j];
           const SplatRec* r = A.recs + sid;
@@ -621,7 +620,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
           const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
           const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
           const float op = __ldg(&r->op);
-#pragma unroll
+#pragma unroll 1
           for (int s = 0; s < 2; ++s) {
             if (s ? !prod1 : !prod0) continue;
             const double r4x = (double)(sx0 + 4 * s);
@@ -632,38 +631,46 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
                            A.cfg.eps)) {
               double d0, d1, d2;
               ray_dir(A.cam, ptx, pty, d0, d1, d2);
-              d[s] = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
-              ids[s] = sid;
+              const double dv = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+              if (s) {
+                dB = dv;
+                iB = sid;
+              } else {
+                dA = dv;
+                iA = sid;
+              }
             }
           }
         }
         pos += 32;
-        int nk[2];
-        nk[0] = __popc(__ballot_sync(kFull, ids[0] != kNoId));
-        nk[1] = __popc(__ballot_sync(kFull, ids[1] != kNoId));
+        const int nkA = __popc(__ballot_sync(kFull, iA != kNoId));
+        const int nkB = __popc(__ballot_sync(kFull, iB != kNoId));
         PROF_ADD(0);
-        if (nk[0] + nk[1] == 0) continue;
-        warp_sort2(d[0], ids[0], d[1], ids[1], lane);
+        if (nkA + nkB == 0) continue;
+        warp_sort2(dA, iA, dB, iB, lane);
         // ---- merge each sorted batch into its tail (heap_merge, :201)
-#pragma unroll
+#pragma unroll 1
         for (int s = 0; s < 2; ++s) {
-          if (nk[s] == 0) continue;
+          const int nks = s ? nkB : nkA;
+          if (nks == 0) continue;
+          const double ds = s ? dB : dA;
+          const uint32_t is = s ? iB : iA;
           const SubQ Q = subq(s);
           const int cur = s ? cur1 : cur0, th = s ? th1 : th0, nt = s ? nt1 : nt0;
-          Q.bd()[lane] = d[s];
-          Q.bi()[lane] = ids[s];
+          Q.bd()[lane] = ds;
+          Q.bi()[lane] = is;
           __syncwarp();
           const double* td = Q.td(cur) + th;
           const uint32_t* ti = Q.ti(cur) + th;
           double* od = Q.td(cur ^ 1);
           uint32_t* oi = Q.ti(cur ^ 1);
-          if (lane < nk[s]) {
-            const int rk = count_below(td, ti, nt, d[s], ids[s]);
-            od[lane + rk] = d[s];
-            oi[lane + rk] = ids[s];
+          if (lane < nks) {
+            const int rk = count_below(td, ti, nt, ds, is);
+            od[lane + rk] = ds;
+            oi[lane + rk] = is;
           }
           for (int t = lane; t < nt; t += 32) {
-            const int rk = count_below(Q.bd(), Q.bi(), nk[s], td[t], ti[t]);
+            const int rk = count_below(Q.bd(), Q.bi(), nks, td[t], ti[t]);
             od[t + rk] = td[t];
             oi[t + rk] = ti[t];
           }
@@ -671,11 +678,11 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
           if (s) {
             cur1 ^= 1;
             th1 = 0;
-            nt1 += nk[s];
+            nt1 += nks;
           } else {
             cur0 ^= 1;
             th0 = 0;
-            nt0 += nk[s];
+            nt0 += nks;
           }
         }
         PROF_ADD(1);
