@@ -100,13 +100,15 @@ __device__ __forceinline__ double frsqrt(double x) {
   return y * fma(-hx * y, y, 1.5);
 }
 
-// max_points, tile_culling.py:55-88, for one splat and one closed rect.
-// The two edge searches divide by (dyy * c) and (dxx * a); with the rect
-// extents powers of two (16, 4, 2) this is a multiply by 1/c (1/a) and an
-// exact power-of-two scale.
+// max_points, tile_culling.py:55-88, for one splat and one closed square
+// rect [xmin, xmin + w] x [ymin, ymin + w] (w = 16, 4 or 2; iw = 1/w exact).
+// The two edge searches divide by (dyy * c) and (dxx * a); with dxx, dyy =
+// +-w this is a multiply by 1/c (1/a) and by +-1/w, the latter exact, so the
+// results match the reference's divisions up to the 1/c (1/a) rounding.
 __device__ __forceinline__ void max_point(double mx, double my, double a, double b, double c,
-                                          double inv_a, double inv_c, double xmin, double xmax,
-                                          double ymin, double ymax, double& ox, double& oy) {
+                                          double inv_a, double inv_c, double xmin, double ymin,
+                                          double w, double iw, double& ox, double& oy) {
+  const double xmax = xmin + w, ymax = ymin + w;
   const bool inside_x = (mx >= xmin) && (mx <= xmax);
   const bool inside_y = (my >= ymin) && (my <= ymax);
   if (inside_x && inside_y) {
@@ -114,14 +116,15 @@ __device__ __forceinline__ void max_point(double mx, double my, double a, double
     oy = my;
     return;
   }
-  const double px = (mx <= 0.5 * (xmin + xmax)) ? xmin : xmax;
-  const double py = (my <= 0.5 * (ymin + ymax)) ? ymin : ymax;
-  const double dxx = (px == xmin) ? (xmax - xmin) : (xmin - xmax);
-  const double dyy = (py == ymin) ? (ymax - ymin) : (ymin - ymax);
+  const bool lo_x = mx <= 0.5 * (xmin + xmax), lo_y = my <= 0.5 * (ymin + ymax);
+  const double px = lo_x ? xmin : xmax;
+  const double py = lo_y ? ymin : ymax;
+  const double dxx = lo_x ? w : -w, idxx = lo_x ? iw : -iw;
+  const double dyy = lo_y ? w : -w, idyy = lo_y ? iw : -iw;
   const double rx = mx - px;
   const double ry = my - py;
-  double t_y = (b * rx + c * ry) * inv_c / dyy;
-  double t_x = (a * rx + b * ry) * inv_a / dxx;
+  double t_y = (b * rx + c * ry) * inv_c * idyy;
+  double t_x = (a * rx + b * ry) * inv_a * idxx;
   t_y = fmin(fmax(t_y, 0.0), 1.0);
   t_x = fmin(fmax(t_x, 0.0), 1.0);
   if (inside_x) t_y = 0.0;
@@ -129,6 +132,48 @@ __device__ __forceinline__ void max_point(double mx, double my, double a, double
   ox = px + t_x * dxx;
   oy = py + t_y * dyy;
 }
+
+// ---------------------------------------------------------------------------
+// float64 exp(-p), p >= 0: exp(-p) = 2^-(k/64) * exp(-r), |r| <= ln2/128,
+// degree-6 Taylor (error < 3e-20) and a 64-entry table of 2^(-j/64).
+static __device__ const double kExp2Tab[64] = {
+    0x1.0000000000000p+0, 0x1.fa7c1819e90d8p-1, 0x1.f50765b6e4540p-1, 0x1.efa1bee615a27p-1,
+    0x1.ea4afa2a490dap-1, 0x1.e502ee78b3ff6p-1, 0x1.dfc97337b9b5fp-1, 0x1.da9e603db3285p-1,
+    0x1.d5818dcfba487p-1, 0x1.d072d4a07897cp-1, 0x1.cb720dcef9069p-1, 0x1.c67f12e57d14bp-1,
+    0x1.c199bdd85529cp-1, 0x1.bcc1e904bc1d2p-1, 0x1.b7f76f2fb5e47p-1, 0x1.b33a2b84f15fbp-1,
+    0x1.ae89f995ad3adp-1, 0x1.a9e6b5579fdbfp-1, 0x1.a5503b23e255dp-1, 0x1.a0c667b5de565p-1,
+    0x1.9c49182a3f090p-1, 0x1.97d829fde4e50p-1, 0x1.93737b0cdc5e5p-1, 0x1.8f1ae99157736p-1,
+    0x1.8ace5422aa0dbp-1, 0x1.868d99b4492edp-1, 0x1.82589994cce13p-1, 0x1.7e2f336cf4e62p-1,
+    0x1.7a11473eb0187p-1, 0x1.75feb564267c9p-1, 0x1.71f75e8ec5f74p-1, 0x1.6dfb23c651a2fp-1,
+    0x1.6a09e667f3bcdp-1, 0x1.6623882552225p-1, 0x1.6247eb03a5585p-1, 0x1.5e76f15ad2148p-1,
+    0x1.5ab07dd485429p-1, 0x1.56f4736b527dap-1, 0x1.5342b569d4f82p-1, 0x1.4f9b2769d2ca7p-1,
+    0x1.4bfdad5362a27p-1, 0x1.486a2b5c13cd0p-1, 0x1.44e086061892dp-1, 0x1.4160a21f72e2ap-1,
+    0x1.3dea64c123422p-1, 0x1.3a7db34e59ff7p-1, 0x1.371a7373aa9cbp-1, 0x1.33c08b26416ffp-1,
+    0x1.306fe0a31b715p-1, 0x1.2d285a6e4030bp-1, 0x1.29e9df51fdee1p-1, 0x1.26b4565e27cddp-1,
+    0x1.2387a6e756238p-1, 0x1.2063b88628cd6p-1, 0x1.1d4873168b9aap-1, 0x1.1a35beb6fcb75p-1,
+    0x1.172b83c7d517bp-1, 0x1.1429aaea92de0p-1, 0x1.11301d0125b51p-1, 0x1.0e3ec32d3d1a2p-1,
+    0x1.0b5586cf9890fp-1, 0x1.0874518759bc8p-1, 0x1.059b0d3158574p-1, 0x1.02c9a3e778061p-1};
+
+__device__ __forceinline__ double exp_neg(double p, const double* tab) {
+  if (p > 700.0) return 0.0;
+  const double kd = rint(p * 0x1.71547652b82fep+6);  // p * 64 / ln2
+  const int k = (int)kd;
+  double r = fma(-kd, 0x1.62e42fefa39efp-7, p);  // p - k ln2/64 (hi)
+  r = fma(-kd, 0x1.abc9e3b39803fp-62, r);       // (lo)
+  // exp(-r), |r| <= ln2/128
+  double e = 1.0 / 720.0;
+  e = fma(e, -r, 1.0 / 120.0);
+  e = fma(e, -r, 1.0 / 24.0);
+  e = fma(e, -r, 1.0 / 6.0);
+  e = fma(e, -r, 0.5);
+  e = fma(e, -r, 1.0);
+  e = fma(e, -r, 1.0);
+  const int j = k & 63, ex = k >> 6;
+  // 2^-ex by exponent construction (ex <= 1010 here)
+  const double scale = __hiloint2double((1023 - ex) << 20, 0);
+  return tab[j] * e * scale;
+}
+
 
 // exponent of gauss2d (tile_culling.py:96)
 __device__ __forceinline__ double gpower(double a, double b, double c, double dx, double dy) {
@@ -141,7 +186,7 @@ __device__ __forceinline__ double gpower(double a, double b, double c, double dx
 __device__ __forceinline__ bool alpha_keep(double power, double thr, float op, double eps) {
   if (power > thr + 1e-9) return false;
   if (power < thr - 1e-9) return true;
-  return (double)op * exp(-power) >= eps;
+  return (double)op * exp_neg(power, kExp2Tab) >= eps;
 }
 
 // rays_through_points (tile_culling.py:161-173): normalize(v @ R).
@@ -195,9 +240,8 @@ __device__ __forceinline__ bool tile_survives(double mx, double my, double a, do
                                               double inv_a, double inv_c, double thr, float op,
                                               double eps, int tx, int ty, double& ptx,
                                               double& pty) {
-  const double x0 = (double)(tx * kTile), x1 = (double)((tx + 1) * kTile);
-  const double y0 = (double)(ty * kTile), y1 = (double)((ty + 1) * kTile);
-  max_point(mx, my, a, b, c, inv_a, inv_c, x0, x1, y0, y1, ptx, pty);
+  max_point(mx, my, a, b, c, inv_a, inv_c, (double)(tx * kTile), (double)(ty * kTile), 16.0,
+            0.0625, ptx, pty);
   return alpha_keep(gpower(a, b, c, ptx - mx, pty - my), thr, op, eps);
 }
 

@@ -56,47 +56,6 @@ __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t i
   return da < db || (da == db && ia < ib);
 }
 
-// ---------------------------------------------------------------------------
-// float64 exp(-p), p >= 0: exp(-p) = 2^-(k/64) * exp(-r), |r| <= ln2/128,
-// degree-6 Taylor (error < 3e-20) and a 64-entry table of 2^(-j/64).
-__device__ const double kExp2Tab[64] = {
-    0x1.0000000000000p+0, 0x1.fa7c1819e90d8p-1, 0x1.f50765b6e4540p-1, 0x1.efa1bee615a27p-1,
-    0x1.ea4afa2a490dap-1, 0x1.e502ee78b3ff6p-1, 0x1.dfc97337b9b5fp-1, 0x1.da9e603db3285p-1,
-    0x1.d5818dcfba487p-1, 0x1.d072d4a07897cp-1, 0x1.cb720dcef9069p-1, 0x1.c67f12e57d14bp-1,
-    0x1.c199bdd85529cp-1, 0x1.bcc1e904bc1d2p-1, 0x1.b7f76f2fb5e47p-1, 0x1.b33a2b84f15fbp-1,
-    0x1.ae89f995ad3adp-1, 0x1.a9e6b5579fdbfp-1, 0x1.a5503b23e255dp-1, 0x1.a0c667b5de565p-1,
-    0x1.9c49182a3f090p-1, 0x1.97d829fde4e50p-1, 0x1.93737b0cdc5e5p-1, 0x1.8f1ae99157736p-1,
-    0x1.8ace5422aa0dbp-1, 0x1.868d99b4492edp-1, 0x1.82589994cce13p-1, 0x1.7e2f336cf4e62p-1,
-    0x1.7a11473eb0187p-1, 0x1.75feb564267c9p-1, 0x1.71f75e8ec5f74p-1, 0x1.6dfb23c651a2fp-1,
-    0x1.6a09e667f3bcdp-1, 0x1.6623882552225p-1, 0x1.6247eb03a5585p-1, 0x1.5e76f15ad2148p-1,
-    0x1.5ab07dd485429p-1, 0x1.56f4736b527dap-1, 0x1.5342b569d4f82p-1, 0x1.4f9b2769d2ca7p-1,
-    0x1.4bfdad5362a27p-1, 0x1.486a2b5c13cd0p-1, 0x1.44e086061892dp-1, 0x1.4160a21f72e2ap-1,
-    0x1.3dea64c123422p-1, 0x1.3a7db34e59ff7p-1, 0x1.371a7373aa9cbp-1, 0x1.33c08b26416ffp-1,
-    0x1.306fe0a31b715p-1, 0x1.2d285a6e4030bp-1, 0x1.29e9df51fdee1p-1, 0x1.26b4565e27cddp-1,
-    0x1.2387a6e756238p-1, 0x1.2063b88628cd6p-1, 0x1.1d4873168b9aap-1, 0x1.1a35beb6fcb75p-1,
-    0x1.172b83c7d517bp-1, 0x1.1429aaea92de0p-1, 0x1.11301d0125b51p-1, 0x1.0e3ec32d3d1a2p-1,
-    0x1.0b5586cf9890fp-1, 0x1.0874518759bc8p-1, 0x1.059b0d3158574p-1, 0x1.02c9a3e778061p-1};
-
-__device__ __forceinline__ double exp_neg(double p, const double* tab) {
-  if (p > 700.0) return 0.0;
-  const double kd = rint(p * 0x1.71547652b82fep+6);  // p * 64 / ln2
-  const int k = (int)kd;
-  double r = fma(-kd, 0x1.62e42fefa39efp-7, p);  // p - k ln2/64 (hi)
-  r = fma(-kd, 0x1.abc9e3b39803fp-62, r);       // (lo)
-  // exp(-r), |r| <= ln2/128
-  double e = 1.0 / 720.0;
-  e = fma(e, -r, 1.0 / 120.0);
-  e = fma(e, -r, 1.0 / 24.0);
-  e = fma(e, -r, 1.0 / 6.0);
-  e = fma(e, -r, 0.5);
-  e = fma(e, -r, 1.0);
-  e = fma(e, -r, 1.0);
-  const int j = k & 63, ex = k >> 6;
-  // 2^-ex by exponent construction (ex <= 1010 here)
-  const double scale = __hiloint2double((1023 - ex) << 20, 0);
-  return tab[j] * e * scale;
-}
-
 template <int QH>
 struct Head {
   double t[QH];
@@ -125,6 +84,17 @@ struct RenderArgs {
   unsigned long long* counters;
 };
 
+// debug blend-record capture (cold path, kept out of line)
+__device__ __noinline__ void write_record(StpOutputs out, int cap, int64_t pix, int rc, double t,
+                                          double al, uint32_t id) {
+  if (rc < cap && pix >= 0) {
+    const int64_t o = pix * cap + rc;
+    out.rec_splat[o] = (int32_t)id;
+    out.rec_t[o] = (float)t;
+    out.rec_alpha[o] = (float)al;
+  }
+}
+
 // blend (hierarchy.py:81-91)
 __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, double al,
                                       uint32_t id) {
@@ -136,15 +106,7 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.C1 += oc.z * wf;
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
-  if (A.cfg.rec_cap > 0) {
-    if (P.rc < A.cfg.rec_cap && P.pix >= 0) {
-      const int64_t o = P.pix * A.cfg.rec_cap + P.rc;
-      A.out.rec_splat[o] = (int32_t)id;
-      A.out.rec_t[o] = (float)t;
-      A.out.rec_alpha[o] = (float)al;
-    }
-    P.rc++;
-  }
+  if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
   P.T = P.T * (1.0 - al);
 }
 
@@ -436,8 +398,7 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
             const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
             const double cc = __ldg(&r->cc);
             const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
-            max_point(mxy.x, mxy.y, ab.x, ab.y, cc, inv.x, inv.y, r2x, r2x + 2.0, r2y, r2y + 2.0,
-                      ptx, pty);
+            max_point(mxy.x, mxy.y, ab.x, ab.y, cc, inv.x, inv.y, r2x, r2y, 2.0, 0.5, ptx, pty);
           }
           double d0, d1, d2;
           ray_dir(A.cam, ptx, pty, d0, d1, d2);
@@ -625,8 +586,8 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
             if (s ? !prod1 : !prod0) continue;
             const double r4x = (double)(sx0 + 4 * s);
             double ptx, pty;
-            max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4x + 4.0, r4y,
-                      r4y + 4.0, ptx, pty);
+            max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4y, 4.0, 0.25, ptx,
+                      pty);
             if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
                            A.cfg.eps)) {
               double d0, d1, d2;
