@@ -55,15 +55,19 @@ int64_t max_capacity(int64_t n, int32_t W, int32_t H, size_t ws_bytes) {
   StpLayout L0;
   plan(n, W, H, 0, L0);
   if (ws_bytes < L0.total) return -1;
+  // largest e with plan(e).total <= ws_bytes (monotone in e): binary search
+  // from the per-entry estimate, so stp_workspace_bytes(.., e) round-trips
   const double per = 24.0 + (double)L0.sort_passes * 256 * 8 / kSortTile;
-  int64_t e = (int64_t)((double)(ws_bytes - L0.total) / per);
-  // shrink until it fits (alignment slack)
+  int64_t hi = (int64_t)((double)(ws_bytes - L0.total) / per) + kSortTile + 1;
+  int64_t lo = 0;
   StpLayout L;
-  while (e > 0) {
-    plan(n, W, H, e, L);
-    if (L.total <= ws_bytes) break;
-    e -= 1 + e / 1000;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    plan(n, W, H, mid, L);
+    if (L.total <= ws_bytes) lo = mid;
+    else hi = mid - 1;
   }
+  int64_t e = lo;
   // look-back words hold 30-bit counts; offsets are uint32
   const int64_t lim = (1ll << 30) - 1;
   if (e > lim) e = lim;
