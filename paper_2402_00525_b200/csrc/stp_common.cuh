@@ -68,6 +68,7 @@ enum Counter {
   C_WORK = 24,      // render work counter
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
   C_TILE = 40,      // render: global tile counter
+  C_STAT = 48,      // 8 work counters (STP_PHASE_PROF builds)
   C_SM = 64,        // render: per-SM sub-tile counters [256]
   C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
   C_COUNT = 320 + 256 * 16

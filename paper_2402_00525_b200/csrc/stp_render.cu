@@ -47,9 +47,15 @@ constexpr unsigned kNoId = 0xffffffffu;
     if (lane == 0) atomicAdd(A.counters + C_PROF + (slot), (unsigned long long)(_pn - _pt)); \
     _pt = _pn;                                                                      \
   } while (0)
+#define STAT_ADD(slot, pred)                                                        \
+  do {                                                                              \
+    const unsigned _b = __ballot_sync(kFull, (pred));                               \
+    if (lane == 0 && _b) atomicAdd(A.counters + C_STAT + (slot), (unsigned long long)__popc(_b)); \
+  } while (0)
 #else
 #define PROF_T0() (void)0
 #define PROF_ADD(slot) (void)0
+#define STAT_ADD(slot, pred) (void)0
 #endif
 
 __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t ib) {
@@ -534,12 +540,16 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
           const int base = ps ? rh1 : rh0;
           const uint32_t* ring = subq(ps).ring(pq, R);
           for (int e = 0; e < rounds; ++e) {
+            STAT_ADD(4, e < pend);
+            STAT_ADD(5, e < pend && P.T >= term);
+            bool pass = false;
             if (e < pend && P.T >= term) {
               const uint32_t id = ring[(base + e) & (R - 1)];
               double t, al;
-              if (emit_eval(P, A, id, s_tab, t, al))
-                head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
+              pass = emit_eval(P, A, id, s_tab, t, al);
+              if (pass) head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
             }
+            STAT_ADD(6, pass);
           }
         }
         rh0 += min(rounds, pa);
@@ -603,10 +613,16 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
             }
           }
         }
+        STAT_ADD(0, j < k_total && prod0);
+        STAT_ADD(0, j < k_total && prod1);
+        STAT_ADD(1, iA != kNoId);
+        STAT_ADD(1, iB != kNoId);
         pos += 32;
         const int nkA = __popc(__ballot_sync(kFull, iA != kNoId));
         const int nkB = __popc(__ballot_sync(kFull, iB != kNoId));
         PROF_ADD(0);
+        STAT_ADD(2, lane == 0);
+        STAT_ADD(3, lane == 0 && nkA + nkB > 0);
         if (nkA + nkB == 0) continue;
         warp_sort2(dA, iA, dB, iB, lane);
         // ---- merge each sorted batch into its tail (heap_merge, :201)

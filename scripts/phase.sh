@@ -1,0 +1,7 @@
+#!/bin/bash
+# K6 per-phase warp-cycle split (instrumented build, never a bench number).
+mkdir -p gpurun_out
+STP_NVCC_EXTRA=-DSTP_PHASE_PROF python paper_2402_00525_b200/build.py --force > /dev/null 2>&1
+timeout 300 python scripts/phase_prof.py ${CFG:-C3} > gpurun_out/phase_${TAG:-x}.log 2>&1
+cat gpurun_out/phase_${TAG:-x}.log
+python paper_2402_00525_b200/build.py --force > /dev/null 2>&1
