@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--gaussians", type=int, default=None, help="override N (debug)")
     p.add_argument("--views", type=int, default=256)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--fast32", action="store_true",
+                   help="K6 via the fp32-state certified kernel (A/B against the float64 one)")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--cpu-seconds", type=float, default=120.0,
                    help="wall budget of the reference arm's timed steps")
@@ -212,7 +214,7 @@ def run_ours(args):
     gs = GaussianScene(dev_t["means"], dev_t["quats"], dev_t["scales"], dev_t["opacity"],
                        dev_t["sh"], dev)
     mode, cfg = Hierarchical(), RenderConfig()
-    r = Renderer(gs, mode, cfg, dev)
+    r = Renderer(gs, mode, cfg, dev, fast32=args.fast32)
     lib = _lib.load()
     W, H = cams[0].width, cams[0].height
     n_views = len(cams)
@@ -224,12 +226,13 @@ def run_ours(args):
     stat = {}
     for v in sorted(set(my_views)):
         st = r.render_into(cams[v], outs, stats=True)
-        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles))
-    need = max(e for _, e, _ in stat.values())
+        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles), int(st.exact_items),
+                   int(st.resolves))
+    need = max(s_[1] for s_ in stat.values())
     r.ws.ensure(gs.n, W, H, int(need * 1.1) + 4096)
 
     c_scene = r.c_scene
-    c_cfg = make_config(cfg, mode)
+    c_cfg = make_config(cfg, mode, fast32=args.fast32)
     c_out = r.outputs_struct(outs)
     c_cams = [make_camera(c) for c in cams]
     stream = torch.cuda.current_stream(dev)
@@ -329,7 +332,9 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_steps / (float(e2e_ms.item()) / 1e3)
 
-    launches_per_view = 1 + 1 + 3 + 1 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 1 + 1
+    # K0, K1, 3 x K2, K3, K4 histogram + passes, K5, K6 (fast + float64 list pass)
+    launches_per_view = (1 + 1 + 3 + 1 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 1 +
+                         (2 if args.fast32 else 1))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": max_ms / steps, "higher_is_better": True,
@@ -341,7 +346,11 @@ def run_ours(args):
                    "parallelism": f"views sharded over {world} GPU(s), no hot-path collective",
                    "mode": "hierarchical:64/8/4", "l2": "inputs larger than L2 "
                    f"(scene {sum(x.numel() for x in dev_t.values()) * 4 / 1e6:.0f} MB > 126 MB)",
-                   "mean_kept": float(n_v), "mean_entries": float(e)},
+                   "mean_kept": float(n_v), "mean_entries": float(e),
+                   "k6_path": "fp32-state certified + float64 list pass" if args.fast32
+                   else "float64",
+                   "mean_exact_items": float(np.mean([stat[v][3] for v in timed_views])),
+                   "mean_resolves": float(np.mean([stat[v][4] for v in timed_views]))},
         "stage_ms": {nm: float(x) for nm, x in zip(names, stage_mean)},
         "roofline": {"bound": "hbm", "kernel": "K6 render (k_render)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

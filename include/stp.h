@@ -81,6 +81,12 @@ typedef struct {
 } StpConfig;
 
 #define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
+#define STP_FLAG_FAST32 2   /* K6 through the fp32-state certified kernel
+                               (float64 keys, fp32 queues / alpha / T), with the
+                               float64 kernel for the sub-tile pairs it cannot
+                               certify; default: the float64 kernel throughout */
+#define STP_FLAG_FB_TEST 4  /* testing (with FAST32): hand every odd sub-tile pair
+                               to the float64 pass (exercises its list mode) */
 
 /* Output buffers (device).  Colour is HWC float32 composited over the
  * background (rasterizer.py:680); depth is the unnormalised expected depth
@@ -107,6 +113,8 @@ typedef struct {
   int64_t tiles;            /* non-empty tiles                             */
   int64_t nonfinite_pixels;
   int64_t tie_runs;         /* equal fp32 keys re-ordered by fp64 depth    */
+  int64_t exact_items;      /* K6 sub-tile pairs re-rendered in float64    */
+  int64_t resolves;         /* K6 fast path: comparisons settled in float64 */
   int64_t entry_capacity;   /* workspace capacity used for this frame      */
   float ms_project, ms_duplicate, ms_sort, ms_blend, ms_total;
   int32_t overflow;         /* 1 if bin_entries > entry_capacity           */
@@ -114,7 +122,7 @@ typedef struct {
 
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
-  size_t recs, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
+  size_t recs, recs32, fb_items, camera, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
       counters, hist, lookback, scan_scratch, total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;

@@ -14,6 +14,8 @@ LIB_PATH = os.path.join(HERE, "libstp_b200.so")
 
 STP_OK, STP_ERR_CONFIG, STP_ERR_DATA, STP_ERR_WORKSPACE_TOO_SMALL, STP_ERR_CUDA = range(5)
 STP_FLAG_TIMINGS = 1
+STP_FLAG_FAST32 = 2
+STP_FLAG_FB_TEST = 4
 
 EXPORTS = ("stp_abi_version", "stp_error_string", "stp_validate_config", "stp_workspace_bytes",
            "stp_workspace_layout", "stp_render", "stp_render_views", "stp_read_stats",
@@ -59,7 +61,8 @@ class StpStats(ctypes.Structure):
                 ("guard", ctypes.c_int64), ("degenerate", ctypes.c_int64),
                 ("kept", ctypes.c_int64), ("bin_entries", ctypes.c_int64),
                 ("tiles", ctypes.c_int64), ("nonfinite_pixels", ctypes.c_int64),
-                ("tie_runs", ctypes.c_int64), ("entry_capacity", ctypes.c_int64),
+                ("tie_runs", ctypes.c_int64), ("exact_items", ctypes.c_int64),
+                ("resolves", ctypes.c_int64), ("entry_capacity", ctypes.c_int64),
                 ("ms_project", ctypes.c_float), ("ms_duplicate", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_blend", ctypes.c_float),
                 ("ms_total", ctypes.c_float), ("overflow", ctypes.c_int32)]
@@ -67,7 +70,7 @@ class StpStats(ctypes.Structure):
 
 class StpLayout(ctypes.Structure):
     _fields_ = [(n, ctypes.c_size_t) for n in (
-        "recs", "state", "counts", "offsets", "keys0", "keys1", "vals0", "vals1", "ranges",
+        "recs", "recs32", "fb_items", "camera", "state", "counts", "offsets", "keys0", "keys1", "vals0", "vals1", "ranges",
         "counters", "hist", "lookback", "scan_scratch", "total")] + [
         ("entry_capacity", ctypes.c_int64), ("n_tiles", ctypes.c_int32),
         ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32),

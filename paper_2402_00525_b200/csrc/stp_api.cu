@@ -39,6 +39,9 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.ranges = o;       o = align_up(o + (size_t)L.n_tiles * 8);
   L.scan_scratch = o; o = align_up(o + (size_t)(nb + 1) * 4);
   L.recs = o;         o = align_up(o + (size_t)n * sizeof(SplatRec));
+  L.recs32 = o;       o = align_up(o + (size_t)n * sizeof(SplatRec32));
+  L.fb_items = o;     o = align_up(o + (size_t)L.n_tiles * 8 * 4);
+  L.camera = o;       o = align_up(o + sizeof(DevCam));
   L.state = o;        o = align_up(o + (size_t)n);
   L.counts = o;       o = align_up(o + (size_t)n * 4);
   L.offsets = o;      o = align_up(o + (size_t)n * 4);
@@ -103,6 +106,11 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
   plan(sc->n, cam->width, cam->height, ecap, L);
   unsigned char* b = static_cast<unsigned char*>(ws);
   f.recs = reinterpret_cast<SplatRec*>(b + L.recs);
+  f.recs32 = reinterpret_cast<SplatRec32*>(b + L.recs32);
+  f.fb_items = reinterpret_cast<uint32_t*>(b + L.fb_items);
+  f.camp = reinterpret_cast<DevCam*>(b + L.camera);
+  f.exact_only = (cfg->flags & STP_FLAG_FAST32) ? 0 : 1;
+  f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);
   f.offsets = reinterpret_cast<uint32_t*>(b + L.offsets);
@@ -213,6 +221,17 @@ int fill_stats(const void* ws, size_t ws_bytes, int64_t n, int32_t W, int32_t H,
   st->tiles = (int64_t)c[C_TILES];
   st->nonfinite_pixels = (int64_t)c[C_NONFINITE];
   st->tie_runs = (int64_t)c[C_TIES];
+  st->exact_items = (int64_t)c[C_FB];
+  {
+    unsigned long long res[256];
+    if (cudaMemcpyAsync(res, static_cast<const unsigned char*>(ws) + L.counters + C_RES * 8,
+                        sizeof(res), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return STP_ERR_CUDA;
+    int64_t tot = 0;
+    for (int i = 0; i < 256; ++i) tot += (int64_t)res[i];
+    st->resolves = tot;
+  }
   st->entry_capacity = ecap;
   st->overflow = st->bin_entries > ecap ? 1 : 0;
   return STP_OK;

@@ -37,6 +37,24 @@ struct __align__(16) SplatRec {
 };
 static_assert(sizeof(SplatRec) == 160, "SplatRec must be 160 B");
 
+// Camera-space record of the K6 fast path (128 B, one cache line), written
+// by K1 next to SplatRec.  With the camera ray v = ((x-cx)/fx, (y-cy)/fy, 1),
+//   t_opt = |v| (v . q') / (v^T M' v),   M' = R Sigma^-1 R^T,  q' = M' p_view,
+// the same real number as the reference's (d . Sigma^-1 (mu - o)) /
+// (d^T Sigma^-1 d) with d = R^T v / |v| (tile_culling.py:161-195), in 2+5
+// float64 FMAs instead of a rotation, a normalisation and two dot products.
+struct __align__(16) SplatRec32 {
+  double mx, my;           // mean2d (pixels)                                  0
+  double ca, cb;           // conic a, b                                       16
+  double cc, q0;           // conic c, q'_x                                    32
+  double q1, q2;           // q'_y, q'_z                                       48
+  double m00, m11;         // M'                                               64
+  double m22, m01x2;       //                                                  80
+  double m02x2, m12x2;     //                                                  96
+  float op, c0, c1, c2;    // opacity, colour                                  112
+};
+static_assert(sizeof(SplatRec32) == 128, "SplatRec32 must be 128 B");
+
 struct DevCam {
   double R[9];
   double pos[3];
@@ -68,10 +86,14 @@ enum Counter {
   C_WORK = 24,      // render work counter
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
   C_TILE = 40,      // render: global tile counter
+  C_FB = 41,        // render: items handed to the exact (fp64) pass
+  C_FBWORK = 42,    // render: exact-pass work counter
+  C_RESOLVE = 43,   // (unused: per-SM slots at C_RES)
   C_STAT = 48,      // 8 work counters (STP_PHASE_PROF builds)
   C_SM = 64,        // render: per-SM sub-tile counters [256]
   C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
-  C_COUNT = 320 + 256 * 16
+  C_RES = 320 + 256 * 16,   // render: per-SM float64 resolution counts [256]
+  C_COUNT = C_RES + 256
 };
 
 // ---------------------------------------------------------------------------
@@ -253,6 +275,9 @@ namespace stp {
 struct Frame {
   // device pointers carved from the workspace
   SplatRec* recs;
+  SplatRec32* recs32;
+  DevCam* camp;           // device copy of `cam` (written by K0)
+  uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;
   uint32_t* counts;
   uint32_t* offsets;
@@ -267,6 +292,8 @@ struct Frame {
   int64_t ecap;
   int gw, gh, n_tiles;
   int passes, partitions;
+  int exact_only;         // no STP_FLAG_FAST32: every item through the fp64 kernel
+  int fb_test;            // STP_FLAG_FB_TEST
   DevCam cam;
   DevCfg cfg;
 };

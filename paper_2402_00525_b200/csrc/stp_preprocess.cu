@@ -29,10 +29,13 @@ __constant__ double c_SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.457
 // K0: zero the per-frame counters / histograms / tile ranges, bump the epoch
 // that tags the sort's look-back words (so they never need clearing).
 __global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n, uint2* ranges,
-                       int n_tiles) {
+                       int n_tiles, DevCam cam, DevCam* camp) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
-  if (tid == 0) counters[C_EPOCH] += 1;
+  if (tid == 0) {
+    counters[C_EPOCH] += 1;
+    *camp = cam;
+  }
   for (int i = tid; i < C_COUNT; i += stride)
     if (i != C_EPOCH) counters[i] = 0;
   for (int i = tid; i < hist_n; i += stride) hist[i] = 0;
@@ -139,6 +142,7 @@ __device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
 
 __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
+    SplatRec32* __restrict__ recs32,
     uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
@@ -301,6 +305,43 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.ry0 = (int16_t)y0;
           r.ry1 = (int16_t)y1;
           recs[i] = r;
+          {
+            // camera-space record (see SplatRec32): M' = W inv3 W^T, q' = M' p_view
+            SplatRec32 f;
+            f.mx = r.mx;
+            f.my = r.my;
+            f.ca = r.ca;
+            f.cb = r.cb;
+            f.cc = r.cc;
+            double WI[9];  // W inv3
+#pragma unroll
+            for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc)
+                WI[aa * 3 + cc] = W[aa * 3 + 0] * inv3[0 * 3 + cc] + W[aa * 3 + 1] * inv3[1 * 3 + cc] +
+                                  W[aa * 3 + 2] * inv3[2 * 3 + cc];
+            double Mc[9];  // (W inv3) W^T
+#pragma unroll
+            for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc)
+                Mc[aa * 3 + cc] = WI[aa * 3 + 0] * W[cc * 3 + 0] + WI[aa * 3 + 1] * W[cc * 3 + 1] +
+                                  WI[aa * 3 + 2] * W[cc * 3 + 2];
+            f.m00 = Mc[0];
+            f.m11 = Mc[4];
+            f.m22 = Mc[8];
+            f.m01x2 = Mc[1] + Mc[3];
+            f.m02x2 = Mc[2] + Mc[6];
+            f.m12x2 = Mc[5] + Mc[7];
+            f.q0 = Mc[0] * pv0 + Mc[1] * pv1 + Mc[2] * z;
+            f.q1 = Mc[3] * pv0 + Mc[4] * pv1 + Mc[5] * z;
+            f.q2 = Mc[6] * pv0 + Mc[7] * pv1 + Mc[8] * z;
+            f.op = opf;
+            f.c0 = col[0];
+            f.c1 = col[1];
+            f.c2 = col[2];
+            recs32[i] = f;
+          }
           g.mx = r.mx;
           g.my = r.my;
           g.a = r.ca;
@@ -518,13 +559,14 @@ void launch_init(const Frame& f, cudaStream_t s) {
   const int hist_n = f.passes * 256;
   const int work = max(max(hist_n, f.n_tiles), (int)C_COUNT);
   const int blocks = min((work + 255) / 256, 1024);
-  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles);
+  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp);
 }
 
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
+                                                      f.recs32,
                                                       f.counts, f.state, f.counters);
 }
 

@@ -88,6 +88,7 @@ struct RenderArgs {
   int gw, n_items;
   StpOutputs out;
   unsigned long long* counters;
+  const uint32_t* list;   // list mode: (tile*8 + pair) items handed over by the fast path
 };
 
 // debug blend-record capture (cold path, kept out of line)
@@ -318,7 +319,19 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
   for (;;) {
     // ---- work item: (tile, pair) with the 8 pairs of a tile on one SM
     int tile = -1, pair = 0;
-    if (lane == 0) {
+    if (A.list) {
+      // list mode: the items the fp32 fast path could not certify
+      if (lane == 0) {
+        const unsigned long long g = atomicAdd(A.counters + C_FBWORK, 1ull);
+        const unsigned long long n = *reinterpret_cast<volatile unsigned long long*>(
+            A.counters + C_FB);
+        if (g < n) {
+          const uint32_t it = A.list[g];
+          tile = (int)(it >> 3);
+          pair = (int)(it & 7);
+        }
+      }
+    } else if (lane == 0) {
       const unsigned long long i = atomicAdd(sm_cnt, 1ull);
       const unsigned long long tl = i >> 3;
       pair = (int)(i & 7);
@@ -731,8 +744,15 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   if (grid > 0) k_render<QH, EXACT, QMX><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
+void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
+
+// K6: the float64 kernel over every (tile, pair) item; with STP_FLAG_FAST32
+// the fp32-state certified kernel first, then the float64 kernel over the
+// items it handed over (list mode).
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
+  if (!f.exact_only) launch_render_fast(f, buf, out, s);
   RenderArgs A;
+  A.list = f.exact_only ? nullptr : f.fb_items;
   A.recs = f.recs;
   A.vals = f.vals[buf];
   A.ranges = f.ranges;

@@ -122,7 +122,8 @@ def make_camera(cam) -> _lib.StpCamera:
     return c
 
 
-def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = False):
+def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = False,
+                fast32: bool = False, fb_test: bool = False):
     c = _lib.StpConfig()
     c.eps = float(cfg.opacity_eps)
     c.termination = float(cfg.termination)
@@ -141,7 +142,8 @@ def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = Fa
     c.with_depth = int(bool(cfg.with_depth))
     c.exact_culling = int(bool(cfg.exact_culling(mode)))
     c.record_cap = int(record_cap)
-    c.flags = _lib.STP_FLAG_TIMINGS if timings else 0
+    c.flags = ((_lib.STP_FLAG_TIMINGS if timings else 0) |
+               (_lib.STP_FLAG_FAST32 if fast32 else 0) | (_lib.STP_FLAG_FB_TEST if fb_test else 0))
     return c
 
 
@@ -199,7 +201,8 @@ class Renderer:
     """
 
     def __init__(self, scene, mode=None, cfg: RenderConfig | None = None, device=None,
-                 entry_capacity: int | None = None):
+                 entry_capacity: int | None = None, fast32: bool = False,
+                 fb_test: bool = False):
         self.scene = GaussianScene.from_any(scene, device)
         self.device = self.scene.device
         self.mode = mode if mode is not None else Hierarchical()
@@ -211,6 +214,8 @@ class Renderer:
         self.lib = _lib.load()
         self.ws = Workspace(self.device)
         self.entry_capacity = entry_capacity
+        self.fast32 = bool(fast32)    # K6 via the fp32-state certified kernel (see stp.h)
+        self.fb_test = bool(fb_test)  # testing: route odd pairs through the float64 pass
         self.c_scene = self.scene.struct()
         rc = self.lib.stp_validate_config(ctypes.byref(make_config(self.cfg, self.mode)))
         if rc != _lib.STP_OK:
@@ -250,7 +255,7 @@ class Renderer:
         ``stats`` (synchronising), else None (asynchronous)."""
         c_cam = make_camera(cam)
         self._ensure(cam)
-        c_cfg = make_config(self.cfg, self.mode, record_cap, timings)
+        c_cfg = make_config(self.cfg, self.mode, record_cap, timings, self.fast32, self.fb_test)
         c_out = self.outputs_struct(outs)
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         st = _lib.StpStats() if stats else None
@@ -295,6 +300,8 @@ class Renderer:
             "timings": timings,
             "nonfinite_pixels": [],
             "tie_runs": int(st.tie_runs),
+            "exact_items": int(st.exact_items),
+            "resolves": int(st.resolves),
         }
         if device_output:
             out = FrameOutput(color=outs["color"], transmittance=outs["transmittance"],
