@@ -235,6 +235,30 @@ __device__ __forceinline__ double blend_depth(const double* m, double q0, double
   return fdiv(num, den);
 }
 
+// t_opt along the camera ray v = (u, w, 1), |v| = vn, in the SplatRec32
+// camera-space form: |v| (v . q') / (v^T M' v) (same real number as
+// blend_depth on the unit world ray R^T v / |v|).
+__device__ __forceinline__ double key_cam(const SplatRec32* __restrict__ r, double u, double w,
+                                          double vn) {
+  const double2 qa = __ldg(reinterpret_cast<const double2*>(&r->cc));     // cc q0
+  const double2 qb = __ldg(reinterpret_cast<const double2*>(&r->q1));     // q1 q2
+  const double2 ma = __ldg(reinterpret_cast<const double2*>(&r->m00));    // m00 m11
+  const double2 mb = __ldg(reinterpret_cast<const double2*>(&r->m22));    // m22 m01x2
+  const double2 mc = __ldg(reinterpret_cast<const double2*>(&r->m02x2));  // m02x2 m12x2
+  const double N = fma(u, qa.y, fma(w, qb.x, qb.y));
+  const double D = fma(u, fma(ma.x, u, fma(mb.y, w, mc.x)), fma(w, fma(ma.y, w, mc.y), mb.x));
+  return vn * fdiv(N, D);
+}
+
+// camera ray of a float64 image point and the key along it
+__device__ __forceinline__ double key_at_point(const DevCam& cam, const SplatRec32* __restrict__ r,
+                                               double x, double y) {
+  const double u = (x - cam.cx) * cam.inv_fx;
+  const double w = (y - cam.cy) * cam.inv_fy;
+  const double vv = fma(u, u, fma(w, w, 1.0));
+  return key_cam(r, u, w, vv * frsqrt(vv));
+}
+
 // Monotone fp32 sort key of a float64 depth: round-to-nearest, -0 -> +0,
 // then the usual order-preserving bit flip.
 __device__ __forceinline__ uint32_t depth_key(double d) {

@@ -33,6 +33,9 @@
 
 namespace stp {
 
+#ifndef STP_EXACT_MINB
+#define STP_EXACT_MINB 4
+#endif
 constexpr int kWarpsPerBlock = 4;
 constexpr int kRenderThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kNoId = 0xffffffffu;
@@ -250,14 +253,26 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
 }
 
 // ---------------------------------------------------------------------------
-// Shared-memory queues of one sub-tile, addressed arithmetically:
-// doubles [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4) |
-// groups 64], ids [same layout | ring 4*R].
-__host__ __device__ inline int sub_nd(int qt, int qm) {
-  return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64;
-}
+// Shared-memory queues of one sub-tile, addressed arithmetically (units of
+// one element: doubles in the key region, uint32 in the id region):
+//   [tail0 qt | tail1 qt | batch 32 | mid 4 x MS | scratch 4 x SS | pad |
+//    groups 4 x GS]  and, ids only, [rings 4 x RS].
+// The per-quad strides are odd (MS = qm+1, SS = qm+5, GS = 17, RS = R+1)
+// and the group base sits 4 elements past a 16-element boundary relative to
+// the mids, so the 4 quads' arrays -- read by the same instruction in the
+// mid merge and the pixel stage -- fall on distinct shared-memory banks.
 __host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? 64 : 128; }
-__host__ __device__ inline int sub_ni(int qt, int qm) { return sub_nd(qt, qm) + 4 * ring_size(qm); }
+__host__ __device__ inline int q_mid0(int qt) { return 2 * qt + 32; }
+__host__ __device__ inline int q_scr0(int qt, int qm) { return q_mid0(qt) + 4 * (qm + 1); }
+__host__ __device__ inline int q_grp0(int qt, int qm) {
+  const int b = q_scr0(qt, qm) + 4 * (qm + 5);
+  return b + ((q_mid0(qt) + 4 - b) & 15);
+}
+__host__ __device__ inline int q_ring0(int qt, int qm) { return q_grp0(qt, qm) + 4 * 17; }
+__host__ __device__ inline int sub_nd(int qt, int qm) { return q_ring0(qt, qm); }
+__host__ __device__ inline int sub_ni(int qt, int qm) {
+  return q_ring0(qt, qm) + 4 * (ring_size(qm) + 1);
+}
 __host__ __device__ inline size_t warp_smem_bytes(int qt, int qm) {
   return ((size_t)2 * sub_nd(qt, qm) * 8 + (size_t)2 * sub_ni(qt, qm) * 4 + 15) & ~(size_t)15;
 }
@@ -270,19 +285,17 @@ struct SubQ {
   __device__ __forceinline__ uint32_t* ti(int c) const { return i + c * qt; }
   __device__ __forceinline__ double* bd() const { return d + 2 * qt; }
   __device__ __forceinline__ uint32_t* bi() const { return i + 2 * qt; }
-  __device__ __forceinline__ int o_mid(int q) const { return 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ int o_scr(int q) const { return 2 * qt + 32 + 4 * qm + q * (qm + 4); }
-  __device__ __forceinline__ int o_grp(int q) const {
-    return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
-  }
+  __device__ __forceinline__ int o_mid(int q) const { return q_mid0(qt) + q * (qm + 1); }
+  __device__ __forceinline__ int o_scr(int q) const { return q_scr0(qt, qm) + q * (qm + 5); }
+  __device__ __forceinline__ int o_grp(int q) const { return q_grp0(qt, qm) + 17 * q; }
   __device__ __forceinline__ uint32_t* ring(int q, int R) const {
-    return i + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64 + q * R;
+    return i + q_ring0(qt, qm) + q * (R + 1);
   }
 };
 
 // QMX = 8: mid queues of at most 8 (loops statically bounded); 0: generic.
 template <int QH, bool EXACT, int QMX>
-__global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
   const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh_rt = A.cfg.q_head;
@@ -444,10 +457,11 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderArgs A) {
 #undef CSWAP
       double* gdp = Q.d + Q.o_grp(mq);
       uint32_t* gip = Q.i + Q.o_grp(mq);
-      gdp[4 * mg + 2 * mh] = gd[2 * mh];
-      gip[4 * mg + 2 * mh] = gi[2 * mh];
-      gdp[4 * mg + 2 * mh + 1] = gd[2 * mh + 1];
-      gip[4 * mg + 2 * mh + 1] = gi[2 * mh + 1];
+      // lane half mh stores sorted slots 2mh, 2mh+1 (selects: no local memory)
+      gdp[4 * mg + 2 * mh] = mh ? gd[2] : gd[0];
+      gip[4 * mg + 2 * mh] = mh ? gi[2] : gi[0];
+      gdp[4 * mg + 2 * mh + 1] = mh ? gd[3] : gd[1];
+      gip[4 * mg + 2 * mh + 1] = mh ? gi[3] : gi[1];
       __syncwarp();
       double* md = Q.d + Q.o_mid(mq);
       uint32_t* mi = Q.i + Q.o_mid(mq);

@@ -153,25 +153,9 @@ __device__ __forceinline__ bool cless(Key x, uint32_t ix, Key y, uint32_t iy, co
 }
 
 // ---------------------------------------------------------------------------
-// t_opt along the camera ray (u, w, 1), |(u, w, 1)| = vn (SplatRec32 form)
-__device__ __forceinline__ double key_cam(const SplatRec32* __restrict__ r, double u, double w,
-                                          double vn) {
-  const double2 qa = __ldg(reinterpret_cast<const double2*>(&r->cc));     // cc q0
-  const double2 qb = __ldg(reinterpret_cast<const double2*>(&r->q1));     // q1 q2
-  const double2 ma = __ldg(reinterpret_cast<const double2*>(&r->m00));    // m00 m11
-  const double2 mb = __ldg(reinterpret_cast<const double2*>(&r->m22));    // m22 m01x2
-  const double2 mc = __ldg(reinterpret_cast<const double2*>(&r->m02x2));  // m02x2 m12x2
-  const double N = fma(u, qa.y, fma(w, qb.x, qb.y));
-  const double D = fma(u, fma(ma.x, u, fma(mb.y, w, mc.x)), fma(w, fma(ma.y, w, mc.y), mb.x));
-  return vn * fdiv(N, D);
-}
-
 // key at a float64 point (peak / quad centre)
 __device__ __forceinline__ Key key_at(const FastArgs& A, uint32_t id, double x, double y) {
-  const double u = (x - A.cam.cx) * A.cam.inv_fx;
-  const double w = (y - A.cam.cy) * A.cam.inv_fy;
-  const double vv = fma(u, u, fma(w, w, 1.0));
-  return f2key(__double2float_rn(key_cam(A.r32 + id, u, w, vv * frsqrt(vv))));
+  return f2key(__double2float_rn(key_at_point(A.cam, A.r32 + id, x, y)));
 }
 
 template <int QH>
