@@ -122,12 +122,13 @@ typedef struct {
 
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
-  size_t recs, recs32, fb_items, camera, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
+  size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
       counters, hist, lookback, scan_scratch, total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;
   int32_t splat_record_bytes;
   int32_t final_buffer;     /* 0: sorted keys/vals in keys0/vals0, 1: keys1/vals1 */
+  int32_t depth_bits;       /* key = tile << depth_bits | depth key >> (32 - depth_bits) */
 } StpLayout;
 
 int stp_abi_version(void);

@@ -26,7 +26,19 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.grid_w = (W + kTile - 1) / kTile;
   L.grid_h = (H + kTile - 1) / kTile;
   L.n_tiles = L.grid_w * L.grid_h;
-  L.sort_bits = 32 + tile_bits(L.n_tiles);
+  // key = tile << depth_bits | top depth_bits of the fp32-orderable depth:
+  // the depth part fills the last 8-bit digit (>= 24 bits), so a 1080p frame
+  // sorts 40 bits in 5 passes; K5 re-orders runs of equal keys by the
+  // float64 depth, which makes the truncation invisible in the final order.
+  {
+    const int tb = tile_bits(L.n_tiles);
+    L.sort_bits = ((tb + 24 + 7) / 8) * 8;
+    L.depth_bits = L.sort_bits - tb;
+    if (L.depth_bits > 32) {
+      L.depth_bits = 32;
+      L.sort_bits = tb + 32;
+    }
+  }
   L.sort_passes = (L.sort_bits + 7) / 8;
   L.entry_capacity = ecap;
   L.partitions = (int32_t)((ecap + kSortTile - 1) / kSortTile);
@@ -42,6 +54,7 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.recs32 = o;       o = align_up(o + (size_t)n * sizeof(SplatRec32));
   L.fb_items = o;     o = align_up(o + (size_t)L.n_tiles * 8 * 4);
   L.camera = o;       o = align_up(o + sizeof(DevCam));
+  L.masks = o;        o = align_up(o + (size_t)n * 8);
   L.state = o;        o = align_up(o + (size_t)n);
   L.counts = o;       o = align_up(o + (size_t)n * 4);
   L.offsets = o;      o = align_up(o + (size_t)n * 4);
@@ -109,6 +122,7 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
   f.recs32 = reinterpret_cast<SplatRec32*>(b + L.recs32);
   f.fb_items = reinterpret_cast<uint32_t*>(b + L.fb_items);
   f.camp = reinterpret_cast<DevCam*>(b + L.camera);
+  f.masks = reinterpret_cast<uint64_t*>(b + L.masks);
   f.exact_only = (cfg->flags & STP_FLAG_FAST32) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
@@ -129,6 +143,7 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
   f.gh = L.grid_h;
   f.n_tiles = L.n_tiles;
   f.passes = L.sort_passes;
+  f.depth_bits = L.depth_bits;
   f.partitions = L.partitions;
   memcpy(f.cam.R, cam->R, sizeof(f.cam.R));
   memcpy(f.cam.pos, cam->pos, sizeof(f.cam.pos));

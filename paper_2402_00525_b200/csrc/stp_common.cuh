@@ -300,6 +300,7 @@ struct Frame {
   // device pointers carved from the workspace
   SplatRec* recs;
   SplatRec32* recs32;
+  uint64_t* masks;        // per Gaussian: surviving tiles of a <= 64-tile coarse rect
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;
@@ -316,6 +317,7 @@ struct Frame {
   int64_t ecap;
   int gw, gh, n_tiles;
   int passes, partitions;
+  int depth_bits;         // sort key = tile << depth_bits | truncated depth key
   int exact_only;         // no STP_FLAG_FAST32: every item through the fp64 kernel
   int fb_test;            // STP_FLAG_FB_TEST
   DevCam cam;

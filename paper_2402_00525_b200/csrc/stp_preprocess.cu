@@ -45,34 +45,37 @@ __global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n,
 // ---------------------------------------------------------------------------
 // K1 preprocess.
 
-__device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, double x, double y,
-                                         double z, float out[3]) {
-  double b[16];
-  const double xx = x * x, yy = y * y, zz = z * z;
-  const double xy = x * y, yz = y * z, xz = x * z;
-  b[0] = c_SH_C0;
+// SH colour (gaussian_math.py:152-175, 415-419) in fp32: the colour feeds
+// only the blended pixel values (no decision), where fp32 rounding (~1e-7)
+// is far inside the 1e-4 output tolerance.
+__device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, float x, float y,
+                                         float z, float out[3]) {
+  float b[16];
+  const float xx = x * x, yy = y * y, zz = z * z;
+  const float xy = x * y, yz = y * z, xz = x * z;
+  b[0] = (float)c_SH_C0;
   if (K > 1) {
-    b[1] = -c_SH_C1 * y;
-    b[2] = c_SH_C1 * z;
-    b[3] = -c_SH_C1 * x;
+    b[1] = -(float)c_SH_C1 * y;
+    b[2] = (float)c_SH_C1 * z;
+    b[3] = -(float)c_SH_C1 * x;
   }
   if (K > 4) {
-    b[4] = c_SH_C2[0] * xy;
-    b[5] = c_SH_C2[1] * yz;
-    b[6] = c_SH_C2[2] * (2.0 * zz - xx - yy);
-    b[7] = c_SH_C2[3] * xz;
-    b[8] = c_SH_C2[4] * (xx - yy);
+    b[4] = (float)c_SH_C2[0] * xy;
+    b[5] = (float)c_SH_C2[1] * yz;
+    b[6] = (float)c_SH_C2[2] * (2.0f * zz - xx - yy);
+    b[7] = (float)c_SH_C2[3] * xz;
+    b[8] = (float)c_SH_C2[4] * (xx - yy);
   }
   if (K > 9) {
-    b[9] = c_SH_C3[0] * y * (3.0 * xx - yy);
-    b[10] = c_SH_C3[1] * xy * z;
-    b[11] = c_SH_C3[2] * y * (4.0 * zz - xx - yy);
-    b[12] = c_SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    b[13] = c_SH_C3[4] * x * (4.0 * zz - xx - yy);
-    b[14] = c_SH_C3[5] * z * (xx - yy);
-    b[15] = c_SH_C3[6] * x * (xx - 3.0 * yy);
+    b[9] = (float)c_SH_C3[0] * y * (3.0f * xx - yy);
+    b[10] = (float)c_SH_C3[1] * xy * z;
+    b[11] = (float)c_SH_C3[2] * y * (4.0f * zz - xx - yy);
+    b[12] = (float)c_SH_C3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = (float)c_SH_C3[4] * x * (4.0f * zz - xx - yy);
+    b[14] = (float)c_SH_C3[5] * z * (xx - yy);
+    b[15] = (float)c_SH_C3[6] * x * (xx - 3.0f * yy);
   }
-  double acc[3] = {0.0, 0.0, 0.0};
+  float acc[3] = {0.5f, 0.5f, 0.5f};
   if (K == 16) {
     // 192 B per Gaussian: 12 x float4, consumed as they arrive
     const float4* p = reinterpret_cast<const float4*>(sh);
@@ -83,20 +86,42 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, do
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const int idx = 4 * u + w;  // coefficient idx / 3, channel idx % 3
-        acc[idx % 3] += b[idx / 3] * (double)fv[w];
+        acc[idx % 3] = fmaf(b[idx / 3], fv[w], acc[idx % 3]);
       }
     }
   } else {
     for (int k = 0; k < K; ++k) {
-      acc[0] += b[k] * (double)__ldg(sh + 3 * k + 0);
-      acc[1] += b[k] * (double)__ldg(sh + 3 * k + 1);
-      acc[2] += b[k] * (double)__ldg(sh + 3 * k + 2);
+      acc[0] = fmaf(b[k], __ldg(sh + 3 * k + 0), acc[0]);
+      acc[1] = fmaf(b[k], __ldg(sh + 3 * k + 1), acc[1]);
+      acc[2] = fmaf(b[k], __ldg(sh + 3 * k + 2), acc[2]);
     }
   }
-  // np.clip(basis @ sh + 0.5, 0, None): lower clamp only (gaussian_math.py:417-419)
-  out[0] = (float)fmax(acc[0] + 0.5, 0.0);
-  out[1] = (float)fmax(acc[1] + 0.5, 0.0);
-  out[2] = (float)fmax(acc[2] + 0.5, 0.0);
+  // np.clip(basis @ sh + 0.5, 0, None): lower clamp only
+  out[0] = fmaxf(acc[0], 0.0f);
+  out[1] = fmaxf(acc[1], 0.0f);
+  out[2] = fmaxf(acc[2], 0.0f);
+}
+
+// k-th (0-based) set bit of a 64-bit mask
+__device__ __forceinline__ int select_bit64(uint64_t m, int k) {
+  uint32_t w = (uint32_t)m;
+  int pos = 0;
+  const int pl = __popc(w);
+  if (k >= pl) {
+    k -= pl;
+    w = (uint32_t)(m >> 32);
+    pos = 32;
+  }
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    const int c = __popc(w & ((1u << s) - 1u));
+    if (k >= c) {
+      k -= c;
+      w >>= s;
+      pos += s;
+    }
+  }
+  return pos;
 }
 
 // Culling geometry of one splat, staged in shared memory for the warp-level
@@ -142,7 +167,7 @@ __device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
 
 __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
-    SplatRec32* __restrict__ recs32,
+    SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
     uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
@@ -274,8 +299,8 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           // SH colour along (mean - origin) / |mean - origin| (:415-419)
           const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
           float col[3];
-          sh_color(sc.sh + (int64_t)i * sc.sh_coeffs * 3, sc.sh_coeffs, rel0 / dist, rel1 / dist,
-                   rel2 / dist, col);
+          sh_color(sc.sh + (int64_t)i * sc.sh_coeffs * 3, sc.sh_coeffs, (float)(rel0 / dist),
+                   (float)(rel1 / dist), (float)(rel2 / dist), col);
           r.c0 = col[0];
           r.c1 = col[1];
           r.c2 = col[2];
@@ -305,7 +330,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.ry0 = (int16_t)y0;
           r.ry1 = (int16_t)y1;
           recs[i] = r;
-          {
+          if (recs32) {
             // camera-space record (see SplatRec32): M' = W inv3 W^T, q' = M' p_view
             SplatRec32 f;
             f.mx = r.mx;
@@ -363,6 +388,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
   // exact-culled tile count (rasterizer.py:334-339), load-balanced per warp
   __shared__ StagedGeo s_geo[kPreThreads];
   __shared__ uint32_t s_cnt[kPreThreads];
+  __shared__ unsigned long long s_mask[kPreThreads];
   const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
   const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
   {
@@ -380,6 +406,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     sg.ry0 = g.ry0;
     sg.wx = wx;
     s_cnt[threadIdx.x] = 0;
+    s_mask[threadIdx.x] = 0ull;
   }
   __syncwarp();
   const int wbase = threadIdx.x & ~31;
@@ -394,12 +421,21 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     }
     const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
     const unsigned kb = __ballot_sync(kFull, keep);
-    if (v && lane == __ffs(peers) - 1 && (kb & peers)) s_cnt[wbase + owner] += __popc(kb & peers);
+    if (v && lane == __ffs(peers) - 1 && (kb & peers)) {
+      s_cnt[wbase + owner] += __popc(kb & peers);
+      // survivors' rect positions (consecutive locals of this round) for K3
+      if (local < 64) {
+        const unsigned first = __ffs(peers) - 1;
+        const unsigned long long bits = (unsigned long long)((kb & peers) >> first) << local;
+        s_mask[wbase + owner] |= bits;
+      }
+    }
     __syncwarp();
   });
   const uint32_t cnt = s_cnt[threadIdx.x];
   if (valid) {
     counts[i] = cnt;
+    if (cnt) masks[i] = s_mask[threadIdx.x];
     if (state) state[i] = (uint8_t)reason;
   }
   const int n_behind = __syncthreads_count(reason == 1);
@@ -501,11 +537,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
 // K3 duplicate.
 
 __global__ void __launch_bounds__(kPreThreads) k_duplicate(
-    const SplatRec* __restrict__ recs, const uint32_t* __restrict__ counts,
+    const SplatRec* __restrict__ recs, const uint64_t* __restrict__ masks,
+    const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
-    int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    int depth_bits, int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   __shared__ SplatRec s_rec[kPreThreads];
   __shared__ uint32_t s_pos[kPreThreads];
+  __shared__ unsigned long long s_m[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const uint32_t cnt = (i < n) ? counts[i] : 0;
@@ -514,6 +552,10 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec r = recs[i];
     s_rec[threadIdx.x] = r;
     area = (r.rx1 - r.rx0 + 1) * (r.ry1 - r.ry0 + 1);
+    // rects of <= 64 tiles: K1 left the survivors' positions in a mask, so
+    // only surviving pairs are enumerated (no second cull)
+    if (area <= 64) area = (int)cnt;
+    s_m[threadIdx.x] = masks[i];
     s_pos[threadIdx.x] = offsets[i];
   }
   __syncwarp();
@@ -526,11 +568,20 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     double ptx = 0.0, pty = 0.0;
     if (v) {
       const int w = r.rx1 - r.rx0 + 1;
-      tx = r.rx0 + local % w;
-      ty = r.ry0 + local / w;
-      keep = tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op, cfg.eps,
-                           tx, ty, ptx, pty);
-      if (!cfg.exact) keep = true;
+      if (w * (r.ry1 - r.ry0 + 1) <= 64) {
+        const int b = select_bit64(s_m[wbase + owner], local);
+        tx = r.rx0 + b % w;
+        ty = r.ry0 + b / w;
+        max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
+                  (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
+        keep = true;
+      } else {
+        tx = r.rx0 + local % w;
+        ty = r.ry0 + local / w;
+        keep = tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op,
+                             cfg.eps, tx, ty, ptx, pty);
+        if (!cfg.exact) keep = true;
+      }
     }
     // deterministic slot: rank among this round's survivors of the same splat
     const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
@@ -543,7 +594,8 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
       const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
-        keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << 32) | depth_key(depth);
+        keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
+                    (depth_key(depth) >> (32 - depth_bits));
         vals[pos] = (uint32_t)(blockIdx.x * kPreThreads + wbase + owner);
       }
     }
@@ -566,7 +618,7 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
-                                                      f.recs32,
+                                                      f.exact_only ? nullptr : f.recs32, f.masks,
                                                       f.counts, f.state, f.counters);
 }
 
@@ -581,8 +633,10 @@ void launch_scan(const Frame& f, cudaStream_t s) {
 void launch_duplicate(const Frame& f, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
-  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.counts, f.offsets, f.n, f.cam,
-                                                     f.cfg, f.gw, f.ecap, f.keys[0], f.vals[0]);
+  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
+                                                     f.cam,
+                                                     f.cfg, f.gw, f.depth_bits, f.ecap, f.keys[0],
+                                                     f.vals[0]);
 }
 
 }  // namespace stp

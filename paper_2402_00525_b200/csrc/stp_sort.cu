@@ -1,5 +1,5 @@
 // K4: hand-written onesweep LSD radix sort (Adinets & Merrill 2022 scheme)
-//     over the 64-bit (tile << 32 | depth-key) keys with uint32 Gaussian-id
+//     over the 64-bit (tile << depth_bits | truncated depth key) keys with uint32 Gaussian-id
 //     values; replaces np.lexsort((rank, key, tile_id)) (rasterizer.py:353-357).
 //     8-bit digits, ceil((32 + tile_bits) / 8) passes, one global-histogram
 //     pass up front, per-partition decoupled look-back with epoch-tagged
@@ -204,19 +204,23 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
                                                 unsigned long long* counters, int64_t ecap,
                                                 uint2* __restrict__ ranges,
                                                 const SplatRec* __restrict__ recs, DevCam cam,
-                                                int gw) {
+                                                int gw, int depth_bits) {
   const int64_t E = n_entries(counters, ecap);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= E) return;
-  const uint64_t k = keys[i];
-  const uint32_t tile = (uint32_t)(k >> 32);
-  const uint64_t kp = (i > 0) ? keys[i - 1] : ~k;
-  const uint64_t kn = (i + 1 < E) ? keys[i + 1] : ~k;
-  if (i == 0 || (uint32_t)(kp >> 32) != tile) {
-    ranges[tile].x = (uint32_t)i;
-    atomicAdd(counters + C_TILES, 1ull);
-  }
-  if (i + 1 == E || (uint32_t)(kn >> 32) != tile) ranges[tile].y = (uint32_t)(i + 1);
+  const bool in = i < E;
+  const uint64_t k = in ? keys[i] : 0;
+  const uint32_t tile = (uint32_t)(k >> depth_bits);
+  const uint64_t kp = (in && i > 0) ? keys[i - 1] : ~k;
+  const uint64_t kn = (in && i + 1 < E) ? keys[i + 1] : ~k;
+  const bool head = in && (i == 0 || (uint32_t)(kp >> depth_bits) != tile);
+  if (head) ranges[tile].x = (uint32_t)i;
+  if (in && (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile))
+    ranges[tile].y = (uint32_t)(i + 1);
+  // non-empty tiles: one atomic per block (a per-entry atomic on one counter
+  // serialises ~8k updates per frame)
+  const int nh = __syncthreads_count(head);
+  if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
+  if (!in) return;
   // run head of equal full keys (same tile, same fp32 depth key)
   if (kn == k && (i == 0 || kp != k)) {
     int64_t L = 2;
@@ -289,7 +293,7 @@ void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
   const int64_t blocks = (f.ecap + 255) / 256;
   if (blocks == 0) return;
   k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], f.counters, f.ecap,
-                                            f.ranges, f.recs, f.cam, f.gw);
+                                            f.ranges, f.recs, f.cam, f.gw, f.depth_bits);
 }
 
 }  // namespace stp

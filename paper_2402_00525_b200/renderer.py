@@ -342,8 +342,9 @@ class Renderer:
         vo = L.vals1 if L.final_buffer else L.vals0
         keys = self.ws.buf[ko: ko + 8 * E].view(torch.int64).cpu().numpy().view(np.uint64)
         vals = self.ws.buf[vo: vo + 4 * E].view(torch.int32).cpu().numpy()
-        return (keys >> np.uint64(32)).astype(np.int64), vals.astype(np.int64), \
-            (keys & np.uint64(0xffffffff)).astype(np.uint32)
+        db = np.uint64(L.depth_bits)
+        return (keys >> db).astype(np.int64), vals.astype(np.int64), \
+            ((keys & ((np.uint64(1) << db) - np.uint64(1))) << (np.uint64(32) - db)).astype(np.uint32)
 
     @staticmethod
     def _records(outs, src, cam):

@@ -121,8 +121,10 @@ def test_workspace_layout(lib):
     assert lib.stp_workspace_layout(n, W, H, b1, ctypes.byref(L)) == _lib.STP_OK
     assert L.entry_capacity >= 100_000 and L.total <= b1
     assert (L.grid_w, L.grid_h, L.n_tiles) == (120, 68, 8160)
-    assert L.sort_bits == 32 + 13 and L.sort_passes == 6
-    regions = sorted((getattr(L, k), k) for k in ("recs", "state", "counts", "offsets", "keys0",
+    # 13 tile bits + 27 depth bits: 5 eight-bit passes
+    assert (L.sort_bits, L.depth_bits, L.sort_passes) == (40, 27, 5)
+    regions = sorted((getattr(L, k), k) for k in ("recs", "recs32", "fb_items", "camera", "masks",
+                                                    "state", "counts", "offsets", "keys0",
                                                     "keys1", "vals0", "vals1", "ranges",
                                                     "counters", "hist", "lookback",
                                                     "scan_scratch"))
@@ -133,7 +135,7 @@ def test_workspace_layout(lib):
     # 4K frame: 32,400 tiles -> 47-bit keys
     b = lib.stp_workspace_bytes(n, 3840, 2160, 1000)
     assert lib.stp_workspace_layout(n, 3840, 2160, b, ctypes.byref(L)) == _lib.STP_OK
-    assert L.n_tiles == 32400 and L.sort_bits == 47
+    assert L.n_tiles == 32400 and (L.sort_bits, L.depth_bits) == (40, 25)
 
 
 def test_host_mode_validation_mirrors_reference():
