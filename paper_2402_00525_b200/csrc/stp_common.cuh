@@ -177,18 +177,26 @@ static __device__ const double kExp2Tab[64] = {
     0x1.172b83c7d517bp-1, 0x1.1429aaea92de0p-1, 0x1.11301d0125b51p-1, 0x1.0e3ec32d3d1a2p-1,
     0x1.0b5586cf9890fp-1, 0x1.0874518759bc8p-1, 0x1.059b0d3158574p-1, 0x1.02c9a3e778061p-1};
 
+// Reduction and polynomial constants in the constant bank: DFMA takes them
+// as c[][] operands instead of two UMOVs per 64-bit immediate.
+__constant__ double c_exp_k[9] = {
+    0x1.71547652b82fep+6,  // 64 / ln2
+    0x1.62e42fefa39efp-7,  // ln2 / 64 (hi)
+    0x1.abc9e3b39803fp-62, // ln2 / 64 (lo)
+    1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 700.0};
+
 __device__ __forceinline__ double exp_neg(double p, const double* tab) {
-  if (p > 700.0) return 0.0;
-  const double kd = rint(p * 0x1.71547652b82fep+6);  // p * 64 / ln2
+  if (p > c_exp_k[8]) return 0.0;
+  const double kd = rint(p * c_exp_k[0]);  // p * 64 / ln2
   const int k = (int)kd;
-  double r = fma(-kd, 0x1.62e42fefa39efp-7, p);  // p - k ln2/64 (hi)
-  r = fma(-kd, 0x1.abc9e3b39803fp-62, r);       // (lo)
+  double r = fma(-kd, c_exp_k[1], p);      // p - k ln2/64 (hi)
+  r = fma(-kd, c_exp_k[2], r);             // (lo)
   // exp(-r), |r| <= ln2/128
-  double e = 1.0 / 720.0;
-  e = fma(e, -r, 1.0 / 120.0);
-  e = fma(e, -r, 1.0 / 24.0);
-  e = fma(e, -r, 1.0 / 6.0);
-  e = fma(e, -r, 0.5);
+  double e = c_exp_k[3];
+  e = fma(e, -r, c_exp_k[4]);
+  e = fma(e, -r, c_exp_k[5]);
+  e = fma(e, -r, c_exp_k[6]);
+  e = fma(e, -r, c_exp_k[7]);
   e = fma(e, -r, 1.0);
   e = fma(e, -r, 1.0);
   const int j = k & 63, ex = k >> 6;

@@ -132,19 +132,22 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
   const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
   if (pw > ct.y + 1e-9) return false;  // alpha < eps, away from the boundary
   const float op = __ldg(&r->op);
-  al = (double)op * exp_neg(pw, tab);
-  if (al < A.cfg.eps) return false;
-  if (al > A.cfg.cap) al = A.cfg.cap;
   const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
   const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
   const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
   const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
   const double q2 = __ldg(&r->q2);
-  // t_opt = (d.q) / (f(d).m6), ray_features (rasterizer.py:406) folded in
+  // t_opt = (d.q) / (f(d).m6), ray_features (rasterizer.py:406) folded in.
+  // Evaluated before the alpha test: the exp chain and this chain are
+  // independent, so the two float64 dependency chains overlap (alpha < eps
+  // after the early-out above is rare).
   const double num = P.d0 * q01.x + P.d1 * q01.y + P.d2 * q2;
   const double den = P.d0 * (P.d0 * m01.x + 2.0 * (P.d1 * m23.y + P.d2 * m45.x)) +
                      P.d1 * (P.d1 * m01.y + 2.0 * P.d2 * m45.y) + P.d2 * P.d2 * m23.x;
   t = fdiv(num, den);
+  al = (double)op * exp_neg(pw, tab);
+  if (al < A.cfg.eps) return false;
+  if (al > A.cfg.cap) al = A.cfg.cap;
   return true;
 }
 
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       uint32_t gi[4];
       gd[0] = gd[1] = INFINITY;
       gi[0] = gi[1] = kNoId;
-#pragma unroll 1
+#pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int e = 4 * mg + 2 * mh + u;
         if (e < c) {
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
           const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
           const float op = __ldg(&r->op);
-#pragma unroll 1
+#pragma unroll
           for (int s = 0; s < 2; ++s) {
             if (s ? !prod1 : !prod0) continue;
             const double r4x = (double)(sx0 + 4 * s);
