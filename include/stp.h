@@ -52,6 +52,22 @@ typedef struct {
   int32_t reserved;
 } StpScene;
 
+/* An already-projected SplatBatch (gaussian_math.py:260-307), the other
+ * input render() accepts (rasterizer.py:616-618): float64 device arrays, the
+ * batch index is the rank.  Opacity and colour are rounded to float32 (they
+ * only scale alpha and the blended colour; every geometric decision uses the
+ * float64 fields). */
+typedef struct {
+  const double* mean2d;          /* [n,2]                                      */
+  const double* conic;           /* [n,3] a, b, c                              */
+  const double* color;           /* [n,3]                                      */
+  const double* opacity;         /* [n]                                        */
+  const double* radius;          /* [n]                                        */
+  const double* inv_cov3;        /* [n,6] packed m00, m11, m22, m01, m02, m12  */
+  const double* inv_cov_center;  /* [n,3]                                      */
+  int64_t n;
+} StpSplatBatch;
+
 /* Pinhole camera (scene_io.py:84-129): world->view rotation, row-major. */
 typedef struct {
   double R[9];
@@ -151,6 +167,12 @@ int stp_workspace_layout(int64_t n, int32_t width, int32_t height, size_t ws_byt
 int stp_render(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
                void* workspace, size_t workspace_bytes, const StpOutputs* out,
                StpStats* stats, void* stream);
+
+/* Render an already-projected SplatBatch (projection skipped, as in
+ * rasterizer.py:616-618); otherwise identical to stp_render. */
+int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
+                     void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                     StpStats* stats, void* stream);
 
 /* Render n_views cameras back to back on one stream (one workspace, outputs
  * per view); never synchronises. */

@@ -8,13 +8,15 @@ Importing the package does not need a GPU; rendering does (no CPU fallback).
 
 from .types import (  # noqa: F401
     Camera, ConfigError, DataError, FrameOutput, FullPerPixel, Gaussian3D, GlobalZ,
-    Hierarchical, PixelRecords, RenderConfig, SceneFormatError, SortMode, TileBin, Window,
+    Hierarchical, PixelRecords, RenderConfig, SceneFormatError, SortMode, SplatBatch, TileBin,
+    Window,
     mode_name, parse_mode, validate_mode,
 )
 
 __all__ = [
     "Camera", "ConfigError", "DataError", "FrameOutput", "FullPerPixel", "Gaussian3D",
     "GlobalZ", "Hierarchical", "PixelRecords", "RenderConfig", "SceneFormatError", "SortMode",
+    "SplatBatch",
     "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
     "render_trajectory", "Renderer", "GaussianScene",
 ]

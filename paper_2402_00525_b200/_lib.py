@@ -18,7 +18,8 @@ STP_FLAG_FAST32 = 2
 STP_FLAG_FB_TEST = 4
 
 EXPORTS = ("stp_abi_version", "stp_error_string", "stp_validate_config", "stp_workspace_bytes",
-           "stp_workspace_layout", "stp_render", "stp_render_views", "stp_read_stats",
+           "stp_workspace_layout", "stp_render", "stp_render_batch", "stp_render_views",
+           "stp_read_stats",
            "stp_render_events", "stp_events_create", "stp_events_destroy",
            "stp_event_elapsed_ms")
 
@@ -28,6 +29,13 @@ class StpScene(ctypes.Structure):
                 ("scales", ctypes.c_void_p), ("opacity", ctypes.c_void_p),
                 ("sh", ctypes.c_void_p), ("n", ctypes.c_int64), ("sh_coeffs", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+class StpSplatBatch(ctypes.Structure):
+    _fields_ = [("mean2d", ctypes.c_void_p), ("conic", ctypes.c_void_p),
+                ("color", ctypes.c_void_p), ("opacity", ctypes.c_void_p),
+                ("radius", ctypes.c_void_p), ("inv_cov3", ctypes.c_void_p),
+                ("inv_cov_center", ctypes.c_void_p), ("n", ctypes.c_int64)]
 
 
 class StpCamera(ctypes.Structure):
@@ -107,6 +115,10 @@ def load(build_if_missing: bool = True):
                              ctypes.POINTER(StpConfig), ctypes.c_void_p, ctypes.c_size_t,
                              ctypes.POINTER(StpOutputs), ctypes.POINTER(StpStats),
                              ctypes.c_void_p]
+    L.stp_render_batch.argtypes = [ctypes.POINTER(StpSplatBatch), ctypes.POINTER(StpCamera),
+                                   ctypes.POINTER(StpConfig), ctypes.c_void_p, ctypes.c_size_t,
+                                   ctypes.POINTER(StpOutputs), ctypes.POINTER(StpStats),
+                                   ctypes.c_void_p]
     L.stp_render_views.argtypes = [ctypes.POINTER(StpScene), ctypes.POINTER(StpCamera),
                                    ctypes.c_int32, ctypes.POINTER(StpConfig), ctypes.c_void_p,
                                    ctypes.c_size_t, ctypes.POINTER(StpOutputs), ctypes.c_void_p]

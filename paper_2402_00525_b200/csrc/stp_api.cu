@@ -112,11 +112,11 @@ int cfg_check(const StpConfig* c) {
   return STP_OK;
 }
 
-bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg, void* ws,
+bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws,
                  size_t ws_bytes, Frame& f, StpLayout& L) {
-  const int64_t ecap = max_capacity(sc->n, cam->width, cam->height, ws_bytes);
+  const int64_t ecap = max_capacity(n, cam->width, cam->height, ws_bytes);
   if (ecap < 0) return false;
-  plan(sc->n, cam->width, cam->height, ecap, L);
+  plan(n, cam->width, cam->height, ecap, L);
   unsigned char* b = static_cast<unsigned char*>(ws);
   f.recs = reinterpret_cast<SplatRec*>(b + L.recs);
   f.recs32 = reinterpret_cast<SplatRec32*>(b + L.recs32);
@@ -137,7 +137,7 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
   f.hist = reinterpret_cast<uint32_t*>(b + L.hist);
   f.lookback = reinterpret_cast<unsigned long long*>(b + L.lookback);
   f.scan_scratch = reinterpret_cast<uint32_t*>(b + L.scan_scratch);
-  f.n = sc->n;
+  f.n = n;
   f.ecap = ecap;
   f.gw = L.grid_w;
   f.gh = L.grid_h;
@@ -176,12 +176,13 @@ bool carve_frame(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg,
 // One view.  `ev` (5 events or null) is recorded at the stage boundaries
 // [init+K1 | K2+K3 | K4+K5 | K6]; with `ms` the stream is synchronised and the
 // stage times returned.
-int render_one(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg, void* ws,
-               size_t ws_bytes, const StpOutputs* out, cudaStream_t s, cudaEvent_t* ev,
-               float* ms) {
+int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* cam,
+               const StpConfig* cfg, void* ws, size_t ws_bytes, const StpOutputs* out,
+               cudaStream_t s, cudaEvent_t* ev, float* ms) {
   Frame f;
   StpLayout L;
-  if (!carve_frame(sc, cam, cfg, ws, ws_bytes, f, L)) return STP_ERR_WORKSPACE_TOO_SMALL;
+  if (!carve_frame(batch ? batch->n : sc->n, cam, cfg, ws, ws_bytes, f, L))
+    return STP_ERR_WORKSPACE_TOO_SMALL;
   if ((size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024) return STP_ERR_CONFIG;
   cudaEvent_t own[5];
   if (ms && !ev) {
@@ -192,7 +193,8 @@ int render_one(const StpScene* sc, const StpCamera* cam, const StpConfig* cfg, v
   launch_init(f, s);
   StpOutputs o = *out;
   if (o.state) f.state = o.state;
-  launch_preprocess(f, *sc, s);
+  if (batch) launch_ingest(f, *batch, s);
+  else launch_preprocess(f, *sc, s);
   if (ev) cudaEventRecord(ev[1], s);
   launch_scan(f, s);
   launch_duplicate(f, s);
@@ -312,12 +314,49 @@ int stp_render(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float ms[4] = {0, 0, 0, 0};
   const bool timed = stats && (cfg->flags & STP_FLAG_TIMINGS);
-  rc = render_one(scene, cam, cfg, workspace, workspace_bytes, out, s, nullptr,
+  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr,
                   timed ? ms : nullptr);
   if (rc != STP_OK) return rc;
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     rc = fill_stats(workspace, workspace_bytes, scene->n, cam->width, cam->height, stats, s);
+    if (rc != STP_OK) return rc;
+    stats->ms_project = ms[0];
+    stats->ms_duplicate = ms[1];
+    stats->ms_sort = ms[2];
+    stats->ms_blend = ms[3];
+    stats->ms_total = ms[0] + ms[1] + ms[2] + ms[3];
+    if (stats->overflow) return STP_ERR_WORKSPACE_TOO_SMALL;
+  }
+  return STP_OK;
+}
+
+int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
+                     void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                     StpStats* stats, void* stream) {
+  if (!batch || !cam || !cfg || !out) return STP_ERR_CONFIG;
+  int rc = cfg_check(cfg);
+  if (rc != STP_OK) return rc;
+  if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
+    return STP_ERR_DATA;
+  if (batch->n < 0 || batch->n >= (int64_t)0x7fffffff) return STP_ERR_DATA;
+  if (batch->n > 0 && (!batch->mean2d || !batch->conic || !batch->color || !batch->opacity ||
+                       !batch->radius || !batch->inv_cov3 || !batch->inv_cov_center))
+    return STP_ERR_DATA;
+  if (!out->color || !out->transmittance) return STP_ERR_DATA;
+  if (cfg->with_depth && !out->depth) return STP_ERR_DATA;
+  if (cfg->record_cap > 0 && (!out->rec_count || !out->rec_splat || !out->rec_t ||
+                              !out->rec_alpha))
+    return STP_ERR_DATA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float ms[4] = {0, 0, 0, 0};
+  const bool timed = stats && (cfg->flags & STP_FLAG_TIMINGS);
+  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr,
+                  timed ? ms : nullptr);
+  if (rc != STP_OK) return rc;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    rc = fill_stats(workspace, workspace_bytes, batch->n, cam->width, cam->height, stats, s);
     if (rc != STP_OK) return rc;
     stats->ms_project = ms[0];
     stats->ms_duplicate = ms[1];
@@ -336,7 +375,7 @@ int stp_render_views(const StpScene* scene, const StpCamera* cams, int32_t n_vie
   for (int v = 0; v < n_views; ++v) {
     int rc = check_inputs(scene, cams + v, cfg, outs + v);
     if (rc != STP_OK) return rc;
-    rc = render_one(scene, cams + v, cfg, workspace, workspace_bytes, outs + v,
+    rc = render_one(scene, nullptr, cams + v, cfg, workspace, workspace_bytes, outs + v,
                     static_cast<cudaStream_t>(stream), nullptr, nullptr);
     if (rc != STP_OK) return rc;
   }
@@ -351,7 +390,7 @@ int stp_render_events(const StpScene* scene, const StpCamera* cam, const StpConf
   if (!events) return STP_ERR_CONFIG;
   cudaEvent_t ev[5];
   for (int i = 0; i < 5; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
-  return render_one(scene, cam, cfg, workspace, workspace_bytes, out,
+  return render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out,
                     static_cast<cudaStream_t>(stream), ev, nullptr);
 }
 

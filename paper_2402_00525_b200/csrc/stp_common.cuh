@@ -334,6 +334,7 @@ struct Frame {
 
 void launch_init(const Frame& f, cudaStream_t s);
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s);
+void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s);
 void launch_scan(const Frame& f, cudaStream_t s);
 void launch_duplicate(const Frame& f, cudaStream_t s);
 int launch_sort(const Frame& f, cudaStream_t s);  // returns the buffer holding the result

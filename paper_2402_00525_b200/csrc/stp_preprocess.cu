@@ -165,6 +165,108 @@ __device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
   }
 }
 
+// coarse tile rect (rasterizer.py:307-321), clamped in double first; empty
+// rects come back as x0 > x1.
+__device__ __forceinline__ void coarse_rect(double px, double py, double radius, int gw, int gh,
+                                            int& x0, int& x1, int& y0, int& y1) {
+  const double ts = (double)kTile;
+  const double lo = -2.0;
+  const double fx0 = fmin(fmax(floor((px - radius) / ts), lo), (double)gw + 1);
+  const double fy0 = fmin(fmax(floor((py - radius) / ts), lo), (double)gh + 1);
+  const double fx1 =
+      fmin(fmax(fmax(ceil((px + radius) / ts) - 1.0, floor(px / ts)), lo), (double)gw + 1);
+  const double fy1 =
+      fmin(fmax(fmax(ceil((py + radius) / ts) - 1.0, floor(py / ts)), lo), (double)gh + 1);
+  x0 = max((int)fx0, 0);
+  y0 = max((int)fy0, 0);
+  x1 = min((int)fx1, gw - 1);
+  y1 = min((int)fy1, gh - 1);
+  if (!(radius == radius)) {  // NaN radius: no tiles
+    x0 = 1;
+    x1 = 0;
+  }
+  if (x1 < x0 || y1 < y0) {
+    x0 = 1;
+    x1 = 0;
+    y0 = 1;
+    y1 = 0;
+  }
+}
+
+// Exact-culled tile count (rasterizer.py:334-339) of the block's splats,
+// load-balanced per warp, plus the survivors' positions in <= 64-tile rects
+// (masks, for K3) and the projection stats.  Called by K1 and the SplatBatch
+// ingest kernel with reason 0 (kept) .. 4 (out of range).
+__device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64_t i, bool valid,
+                                            const DevCfg& cfg, uint64_t* __restrict__ masks,
+                                            uint32_t* __restrict__ counts,
+                                            uint8_t* __restrict__ state,
+                                            unsigned long long* __restrict__ counters) {
+  const int lane = threadIdx.x & 31;
+  __shared__ StagedGeo s_geo[kPreThreads];
+  __shared__ uint32_t s_cnt[kPreThreads];
+  __shared__ unsigned long long s_mask[kPreThreads];
+  const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
+  const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
+  {
+    StagedGeo& sg = s_geo[threadIdx.x];
+    sg.mx = g.mx;
+    sg.my = g.my;
+    sg.a = g.a;
+    sg.b = g.b;
+    sg.c = g.c;
+    sg.ia = g.ia;
+    sg.ic = g.ic;
+    sg.thr = g.thr;
+    sg.op = g.op;
+    sg.rx0 = g.rx0;
+    sg.ry0 = g.ry0;
+    sg.wx = wx;
+    s_cnt[threadIdx.x] = 0;
+    s_mask[threadIdx.x] = 0ull;
+  }
+  __syncwarp();
+  const int wbase = threadIdx.x & ~31;
+  warp_expand(area, lane, [&](bool v, int owner, int local) {
+    bool keep = false;
+    if (v) {
+      const StagedGeo& o = s_geo[wbase + owner];
+      const int tx = o.rx0 + local % o.wx, ty = o.ry0 + local / o.wx;
+      double px, py;
+      keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
+                                          cfg.eps, tx, ty, px, py);
+    }
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned kb = __ballot_sync(kFull, keep);
+    if (v && lane == __ffs(peers) - 1 && (kb & peers)) {
+      s_cnt[wbase + owner] += __popc(kb & peers);
+      // survivors' rect positions (consecutive locals of this round) for K3
+      if (local < 64) {
+        const unsigned first = __ffs(peers) - 1;
+        const unsigned long long bits = (unsigned long long)((kb & peers) >> first) << local;
+        s_mask[wbase + owner] |= bits;
+      }
+    }
+    __syncwarp();
+  });
+  const uint32_t cnt = s_cnt[threadIdx.x];
+  if (valid) {
+    counts[i] = cnt;
+    if (cnt) masks[i] = s_mask[threadIdx.x];
+    if (state) state[i] = (uint8_t)reason;
+  }
+  const int n_behind = __syncthreads_count(reason == 1);
+  const int n_guard = __syncthreads_count(reason == 2);
+  const int n_degen = __syncthreads_count(reason == 3);
+  const int n_kept = __syncthreads_count(reason == 0);
+  if (threadIdx.x == 0) {
+    if (n_behind) atomicAdd(counters + C_BEHIND, (unsigned long long)n_behind);
+    if (n_guard) atomicAdd(counters + C_GUARD, (unsigned long long)n_guard);
+    if (n_degen) atomicAdd(counters + C_DEGEN, (unsigned long long)n_degen);
+    if (n_kept) atomicAdd(counters + C_KEPT, (unsigned long long)n_kept);
+  }
+}
+
 __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
@@ -304,27 +406,8 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.c0 = col[0];
           r.c1 = col[1];
           r.c2 = col[2];
-          // coarse tile rect (rasterizer.py:307-321), clamped in double first
-          const double ts = (double)kTile;
-          const double lo = -2.0;
-          const double fx0 = fmin(fmax(floor((px - radius) / ts), lo), (double)gw + 1);
-          const double fy0 = fmin(fmax(floor((py - radius) / ts), lo), (double)gh + 1);
-          const double fx1 = fmin(fmax(fmax(ceil((px + radius) / ts) - 1.0, floor(px / ts)), lo),
-                                  (double)gw + 1);
-          const double fy1 = fmin(fmax(fmax(ceil((py + radius) / ts) - 1.0, floor(py / ts)), lo),
-                                  (double)gh + 1);
-          int x0 = max((int)fx0, 0), y0 = max((int)fy0, 0);
-          int x1 = min((int)fx1, gw - 1), y1 = min((int)fy1, gh - 1);
-          if (!(radius == radius)) {  // NaN radius: no tiles
-            x0 = 1;
-            x1 = 0;
-          }
-          if (x1 < x0 || y1 < y0) {
-            x0 = 1;
-            x1 = 0;
-            y0 = 1;
-            y1 = 0;
-          }
+          int x0, x1, y0, y1;
+          coarse_rect(px, py, radius, gw, gh, x0, x1, y0, y1);
           r.rx0 = (int16_t)x0;
           r.rx1 = (int16_t)x1;
           r.ry0 = (int16_t)y0;
@@ -385,69 +468,101 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
     }
   }
 
-  // exact-culled tile count (rasterizer.py:334-339), load-balanced per warp
-  __shared__ StagedGeo s_geo[kPreThreads];
-  __shared__ uint32_t s_cnt[kPreThreads];
-  __shared__ unsigned long long s_mask[kPreThreads];
-  const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
-  const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
-  {
-    StagedGeo& sg = s_geo[threadIdx.x];
-    sg.mx = g.mx;
-    sg.my = g.my;
-    sg.a = g.a;
-    sg.b = g.b;
-    sg.c = g.c;
-    sg.ia = g.ia;
-    sg.ic = g.ic;
-    sg.thr = g.thr;
-    sg.op = g.op;
-    sg.rx0 = g.rx0;
-    sg.ry0 = g.ry0;
-    sg.wx = wx;
-    s_cnt[threadIdx.x] = 0;
-    s_mask[threadIdx.x] = 0ull;
-  }
-  __syncwarp();
-  const int wbase = threadIdx.x & ~31;
-  warp_expand(area, lane, [&](bool v, int owner, int local) {
-    bool keep = false;
-    if (v) {
-      const StagedGeo& o = s_geo[wbase + owner];
-      const int tx = o.rx0 + local % o.wx, ty = o.ry0 + local / o.wx;
-      double px, py;
-      keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
-                                          cfg.eps, tx, ty, px, py);
-    }
-    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
-    const unsigned kb = __ballot_sync(kFull, keep);
-    if (v && lane == __ffs(peers) - 1 && (kb & peers)) {
-      s_cnt[wbase + owner] += __popc(kb & peers);
-      // survivors' rect positions (consecutive locals of this round) for K3
-      if (local < 64) {
-        const unsigned first = __ffs(peers) - 1;
-        const unsigned long long bits = (unsigned long long)((kb & peers) >> first) << local;
-        s_mask[wbase + owner] |= bits;
-      }
-    }
-    __syncwarp();
-  });
-  const uint32_t cnt = s_cnt[threadIdx.x];
+  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
+}
+
+// ---------------------------------------------------------------------------
+// SplatBatch ingest: the K1 outputs from an already-projected batch
+// (rasterizer.py:616-618 skips project_scene); every batch splat is kept.
+__global__ void __launch_bounds__(kPreThreads) k_ingest(
+    StpSplatBatch b, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
+    SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
+    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    unsigned long long* __restrict__ counters) {
+  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
+  const bool valid = i < b.n;
+  int reason = valid ? 0 : 4;
+  SplatGeo g;
+  g.rx0 = 1;
+  g.rx1 = 0;
+  g.ry0 = 1;
+  g.ry1 = 0;
+  g.mx = g.my = g.a = g.b = g.c = g.ia = g.ic = g.thr = 0.0;
+  g.op = 0.f;
   if (valid) {
-    counts[i] = cnt;
-    if (cnt) masks[i] = s_mask[threadIdx.x];
-    if (state) state[i] = (uint8_t)reason;
+    SplatRec r;
+    r.mx = b.mean2d[2 * i];
+    r.my = b.mean2d[2 * i + 1];
+    r.ca = b.conic[3 * i];
+    r.cb = b.conic[3 * i + 1];
+    r.cc = b.conic[3 * i + 2];
+    r.inv_a = 1.0 / r.ca;
+    r.inv_c = 1.0 / r.cc;
+    const double op = b.opacity[i];
+    r.thr = (op > 0.0) ? log(op / cfg.eps) : -INFINITY;
+    r.op = (float)op;
+    for (int k = 0; k < 6; ++k) r.m[k] = b.inv_cov3[6 * i + k];
+    r.q0 = b.inv_cov_center[3 * i];
+    r.q1 = b.inv_cov_center[3 * i + 1];
+    r.q2 = b.inv_cov_center[3 * i + 2];
+    r.c0 = (float)b.color[3 * i];
+    r.c1 = (float)b.color[3 * i + 1];
+    r.c2 = (float)b.color[3 * i + 2];
+    int x0, x1, y0, y1;
+    coarse_rect(r.mx, r.my, b.radius[i], gw, gh, x0, x1, y0, y1);
+    r.rx0 = (int16_t)x0;
+    r.rx1 = (int16_t)x1;
+    r.ry0 = (int16_t)y0;
+    r.ry1 = (int16_t)y1;
+    recs[i] = r;
+    if (recs32) {
+      // camera space: M' = R M R^T, q' = R q
+      const double* W = cam.R;
+      const double M[9] = {r.m[0], r.m[3], r.m[4], r.m[3], r.m[1], r.m[5], r.m[4], r.m[5], r.m[2]};
+      double WM[9], Mc[9];
+      for (int aa = 0; aa < 3; ++aa)
+        for (int cc = 0; cc < 3; ++cc)
+          WM[aa * 3 + cc] = W[aa * 3] * M[cc] + W[aa * 3 + 1] * M[3 + cc] + W[aa * 3 + 2] * M[6 + cc];
+      for (int aa = 0; aa < 3; ++aa)
+        for (int cc = 0; cc < 3; ++cc)
+          Mc[aa * 3 + cc] =
+              WM[aa * 3] * W[cc * 3] + WM[aa * 3 + 1] * W[cc * 3 + 1] + WM[aa * 3 + 2] * W[cc * 3 + 2];
+      SplatRec32 f;
+      f.mx = r.mx;
+      f.my = r.my;
+      f.ca = r.ca;
+      f.cb = r.cb;
+      f.cc = r.cc;
+      f.m00 = Mc[0];
+      f.m11 = Mc[4];
+      f.m22 = Mc[8];
+      f.m01x2 = Mc[1] + Mc[3];
+      f.m02x2 = Mc[2] + Mc[6];
+      f.m12x2 = Mc[5] + Mc[7];
+      f.q0 = W[0] * r.q0 + W[1] * r.q1 + W[2] * r.q2;
+      f.q1 = W[3] * r.q0 + W[4] * r.q1 + W[5] * r.q2;
+      f.q2 = W[6] * r.q0 + W[7] * r.q1 + W[8] * r.q2;
+      f.op = r.op;
+      f.c0 = r.c0;
+      f.c1 = r.c1;
+      f.c2 = r.c2;
+      recs32[i] = f;
+    }
+    g.mx = r.mx;
+    g.my = r.my;
+    g.a = r.ca;
+    g.b = r.cb;
+    g.c = r.cc;
+    g.ia = r.inv_a;
+    g.ic = r.inv_c;
+    g.thr = r.thr;
+    g.op = r.op;
+    g.rx0 = x0;
+    g.rx1 = x1;
+    g.ry0 = y0;
+    g.ry1 = y1;
   }
-  const int n_behind = __syncthreads_count(reason == 1);
-  const int n_guard = __syncthreads_count(reason == 2);
-  const int n_degen = __syncthreads_count(reason == 3);
-  const int n_kept = __syncthreads_count(reason == 0);
-  if (threadIdx.x == 0) {
-    if (n_behind) atomicAdd(counters + C_BEHIND, (unsigned long long)n_behind);
-    if (n_guard) atomicAdd(counters + C_GUARD, (unsigned long long)n_guard);
-    if (n_degen) atomicAdd(counters + C_DEGEN, (unsigned long long)n_degen);
-    if (n_kept) atomicAdd(counters + C_KEPT, (unsigned long long)n_kept);
-  }
+  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -620,6 +735,14 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                       f.exact_only ? nullptr : f.recs32, f.masks,
                                                       f.counts, f.state, f.counters);
+}
+
+void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
+  if (f.n == 0) return;
+  const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
+  k_ingest<<<(unsigned)blocks, kPreThreads, 0, s>>>(b, f.cam, f.cfg, f.gw, f.gh, f.recs,
+                                                  f.exact_only ? nullptr : f.recs32, f.masks,
+                                                  f.counts, f.state, f.counters);
 }
 
 void launch_scan(const Frame& f, cudaStream_t s) {

@@ -6,8 +6,10 @@
 //     status words (no per-frame clearing).  Stable: partitions are ranked in
 //     input order with warp-striped items and match.any peer ranking.
 // K5: tile ranges (rasterizer.py:358-372) and the float64 tie fix-up: runs of
-//     equal fp32 keys inside a tile are re-ordered by the float64 depth and
-//     then rank, so the final order equals the reference's float64 lexsort.
+//     equal (truncated) keys inside a tile are re-ordered by the float64 depth
+//     and then rank, so the final order equals the reference's float64
+//     lexsort (k_ranges computes the run members' depths in parallel, k_ties
+//     sorts each run).
 #include "stp_common.cuh"
 
 namespace stp {
@@ -199,39 +201,76 @@ __device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ rec
 
 constexpr int kTieLocal = 32;
 
+// sum over a 256-thread block (all threads call it)
+__device__ __forceinline__ int block_sum(int v) {
+  __shared__ int s_part[8];
+  v += __shfl_xor_sync(kFull, v, 16);
+  v += __shfl_xor_sync(kFull, v, 8);
+  v += __shfl_xor_sync(kFull, v, 4);
+  v += __shfl_xor_sync(kFull, v, 2);
+  v += __shfl_xor_sync(kFull, v, 1);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int t = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w];
+  __syncthreads();
+  return t;
+}
+
+// Grid-stride over the sorted entries; per-block counts are reduced in
+// registers / shared memory and added with one atomic per block (a per-entry
+// or per-warp atomic on one counter serialises tens of thousands of updates).
 __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys,
-                                                uint32_t* __restrict__ vals,
+                                                const uint32_t* __restrict__ vals,
                                                 unsigned long long* counters, int64_t ecap,
                                                 uint2* __restrict__ ranges,
                                                 const SplatRec* __restrict__ recs, DevCam cam,
-                                                int gw, int depth_bits) {
+                                                int gw, int depth_bits,
+                                                double* __restrict__ d64) {
   const int64_t E = n_entries(counters, ecap);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = i < E;
-  const uint64_t k = in ? keys[i] : 0;
-  const uint32_t tile = (uint32_t)(k >> depth_bits);
-  const uint64_t kp = (in && i > 0) ? keys[i - 1] : ~k;
-  const uint64_t kn = (in && i + 1 < E) ? keys[i + 1] : ~k;
-  const bool head = in && (i == 0 || (uint32_t)(kp >> depth_bits) != tile);
-  if (head) ranges[tile].x = (uint32_t)i;
-  if (in && (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile))
-    ranges[tile].y = (uint32_t)(i + 1);
-  // non-empty tiles: one atomic per block (a per-entry atomic on one counter
-  // serialises ~8k updates per frame)
-  const int nh = __syncthreads_count(head);
+  int heads = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint32_t tile = (uint32_t)(k >> depth_bits);
+    const uint64_t kp = (i > 0) ? keys[i - 1] : ~k;
+    const uint64_t kn = (i + 1 < E) ? keys[i + 1] : ~k;
+    if (i == 0 || (uint32_t)(kp >> depth_bits) != tile) {
+      ranges[tile].x = (uint32_t)i;
+      ++heads;
+    }
+    if (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile) ranges[tile].y = (uint32_t)(i + 1);
+    // members of a run of equal keys (same tile, same truncated depth key):
+    // their float64 depths, computed in parallel, go to the free ping-pong
+    // buffer for k_ties
+    if (kn == k || (i > 0 && kp == k))
+      d64[i] = entry_depth64(recs, cam, vals[i], (int)tile, gw);
+  }
+  const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
   if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
-  if (!in) return;
-  // run head of equal full keys (same tile, same fp32 depth key)
-  if (kn == k && (i == 0 || kp != k)) {
+}
+
+// K5b: each run of equal keys is re-ordered by (float64 depth, rank); the
+// depths were computed by k_ranges.
+__global__ void __launch_bounds__(256) k_ties(const uint64_t* __restrict__ keys,
+                                              uint32_t* __restrict__ vals,
+                                              double* __restrict__ d64,
+                                              unsigned long long* counters, int64_t ecap) {
+  const int64_t E = n_entries(counters, ecap);
+  int runs = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    if (!((i + 1 < E && keys[i + 1] == k) && (i == 0 || keys[i - 1] != k))) continue;
+    ++runs;
     int64_t L = 2;
     while (i + L < E && keys[i + L] == k) ++L;
-    atomicAdd(counters + C_TIES, 1ull);
     if (L <= kTieLocal) {
       double d[kTieLocal];
       uint32_t id[kTieLocal];
       for (int m = 0; m < L; ++m) {
         id[m] = vals[i + m];
-        d[m] = entry_depth64(recs, cam, id[m], (int)tile, gw);
+        d[m] = d64[i + m];
       }
       // insertion sort by (depth, rank); members arrive in rank order
       for (int m = 1; m < L; ++m) {
@@ -248,22 +287,26 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
       }
       for (int m = 0; m < L; ++m) vals[i + m] = id[m];
     } else {
-      // long runs (coincident splats): in-place insertion sort, recomputing depths
+      // long runs (coincident splats): in-place insertion sort through memory
       for (int64_t m = 1; m < L; ++m) {
         const uint32_t iv = vals[i + m];
-        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw);
+        const double dv = d64[i + m];
         int64_t p = m - 1;
         while (p >= 0) {
           const uint32_t ip = vals[i + p];
-          const double dp = entry_depth64(recs, cam, ip, (int)tile, gw);
+          const double dp = d64[i + p];
           if (!(dp > dv || (dp == dv && ip > iv))) break;
           vals[i + p + 1] = ip;
+          d64[i + p + 1] = dp;
           --p;
         }
         vals[i + p + 1] = iv;
+        d64[i + p + 1] = dv;
       }
     }
   }
+  const int nr = __syncthreads_count(runs > 0) ? block_sum(runs) : 0;
+  if (threadIdx.x == 0 && nr) atomicAdd(counters + C_TIES, (unsigned long long)nr);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,10 +333,13 @@ int launch_sort(const Frame& f, cudaStream_t s) {
 }
 
 void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
-  const int64_t blocks = (f.ecap + 255) / 256;
-  if (blocks == 0) return;
+  if (f.ecap == 0) return;
+  const int64_t blocks = min((int64_t)148 * 8, (f.ecap + 255) / 256);
+  // the other ping-pong key buffer (E x 8 B) is free: float64 depths of tie runs
+  double* d64 = reinterpret_cast<double*>(f.keys[buf ^ 1]);
   k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], f.counters, f.ecap,
-                                            f.ranges, f.recs, f.cam, f.gw, f.depth_bits);
+                                            f.ranges, f.recs, f.cam, f.gw, f.depth_bits, d64);
+  k_ties<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], d64, f.counters, f.ecap);
 }
 
 }  // namespace stp

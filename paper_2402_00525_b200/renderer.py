@@ -81,9 +81,6 @@ class GaussianScene:
         if isinstance(scene, dict):
             return cls(scene["means"], scene["quats"], scene["scales"], scene["opacity"],
                        scene["sh"], device)
-        if hasattr(scene, "mean2d") and hasattr(scene, "inv_cov3"):
-            raise ConfigError("pre-projected SplatBatch input is not supported by the B200 "
-                              "path yet; pass Gaussians")
         gs = list(scene)
         if not gs:
             z = np.zeros
@@ -105,6 +102,45 @@ class GaussianScene:
         s.n = self.n
         s.sh_coeffs = self.sh_coeffs
         return s
+
+
+class BatchScene:
+    """Device copy (float64) of an already-projected SplatBatch
+    (gaussian_math.py:260-307; duck-typed: the reference's own SplatBatch or
+    this package's).  Rendered through stp_render_batch, which skips the
+    projection like rasterizer.py:616-618."""
+
+    FIELDS = ("mean2d", "conic", "color", "opacity", "radius", "inv_cov3", "inv_cov_center")
+
+    def __init__(self, batch, device=None):
+        dev = _require_cuda(device)
+        n = len(batch.opacity)
+        shapes = {"mean2d": (n, 2), "conic": (n, 3), "color": (n, 3), "opacity": (n,),
+                  "radius": (n,), "inv_cov3": (n, 6), "inv_cov_center": (n, 3)}
+        self.t = {}
+        for k in self.FIELDS:
+            a = torch.as_tensor(np.ascontiguousarray(getattr(batch, k), dtype=np.float64))
+            if tuple(a.shape) != shapes[k]:
+                raise DataError(f"SplatBatch.{k} has shape {tuple(a.shape)}, expected {shapes[k]}")
+            self.t[k] = a.to(dev).contiguous()
+        self.source_index = np.asarray(batch.source_index, dtype=np.int64).copy()
+        self.device = dev
+
+    @property
+    def n(self) -> int:
+        return int(self.t["opacity"].shape[0])
+
+    def struct(self) -> _lib.StpSplatBatch:
+        b = _lib.StpSplatBatch()
+        for k in self.FIELDS:
+            setattr(b, k, self.t[k].data_ptr())
+        b.n = self.n
+        return b
+
+
+def _is_batch(scene) -> bool:
+    return isinstance(scene, BatchScene) or (hasattr(scene, "mean2d") and
+                                             hasattr(scene, "inv_cov3"))
 
 
 def make_camera(cam) -> _lib.StpCamera:
@@ -203,7 +239,11 @@ class Renderer:
     def __init__(self, scene, mode=None, cfg: RenderConfig | None = None, device=None,
                  entry_capacity: int | None = None, fast32: bool = False,
                  fb_test: bool = False):
-        self.scene = GaussianScene.from_any(scene, device)
+        if _is_batch(scene):
+            self.scene = scene if isinstance(scene, BatchScene) else BatchScene(scene, device)
+        else:
+            self.scene = GaussianScene.from_any(scene, device)
+        self.batch = isinstance(self.scene, BatchScene)
         self.device = self.scene.device
         self.mode = mode if mode is not None else Hierarchical()
         validate_mode(self.mode)
@@ -260,11 +300,12 @@ class Renderer:
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         st = _lib.StpStats() if stats else None
         for attempt in range(3):
-            rc = self.lib.stp_render(ctypes.byref(self.c_scene), ctypes.byref(c_cam),
-                                     ctypes.byref(c_cfg), ctypes.c_void_p(self.ws.ptr),
-                                     self.ws.nbytes, ctypes.byref(c_out),
-                                     ctypes.byref(st) if st is not None else None,
-                                     ctypes.c_void_p(s))
+            fn = self.lib.stp_render_batch if self.batch else self.lib.stp_render
+            rc = fn(ctypes.byref(self.c_scene), ctypes.byref(c_cam),
+                    ctypes.byref(c_cfg), ctypes.c_void_p(self.ws.ptr),
+                    self.ws.nbytes, ctypes.byref(c_out),
+                    ctypes.byref(st) if st is not None else None,
+                    ctypes.c_void_p(s))
             if rc == _lib.STP_ERR_WORKSPACE_TOO_SMALL and st is not None:
                 need = int(st.bin_entries * 1.25) + 4096
                 self.entry_capacity = need
@@ -286,15 +327,20 @@ class Renderer:
                 rec_cap = int(outs["rec_count"].max().item())
                 continue
             break
-        state = outs["state"][: self.scene.n]
-        kept = torch.nonzero(state == 0).flatten()
+        if self.batch:
+            kept = torch.as_tensor(self.scene.source_index, device=self.device)
+        else:
+            state = outs["state"][: self.scene.n]
+            kept = torch.nonzero(state == 0).flatten()
         timings = {"project": st.ms_project / 1e3, "duplicate": st.ms_duplicate / 1e3,
                    "sort": st.ms_sort / 1e3, "blend": st.ms_blend / 1e3}
         stats = {
             "mode": mode_name(self.mode),
-            "projection": {"input": int(st.input), "behind": int(st.behind),
-                           "guard": int(st.guard), "degenerate": int(st.degenerate),
-                           "kept": int(st.kept)},
+            # a SplatBatch input reports only "kept" (rasterizer.py:616-618)
+            "projection": ({"kept": int(st.kept)} if self.batch else
+                           {"input": int(st.input), "behind": int(st.behind),
+                            "guard": int(st.guard), "degenerate": int(st.degenerate),
+                            "kept": int(st.kept)}),
             "bin_entries": int(st.bin_entries),
             "tiles": int(st.tiles),
             "timings": timings,
@@ -314,14 +360,14 @@ class Renderer:
         color = outs["color"].double().cpu().numpy()
         tn = outs["transmittance"].double().cpu().numpy()
         depth = outs["depth"].double().cpu().numpy() if cfg.with_depth else None
-        src = kept.cpu().numpy().astype(np.int64)
+        src = self.scene.source_index if self.batch else kept.cpu().numpy().astype(np.int64)
         if st.nonfinite_pixels:
             bad = ~(np.isfinite(color).all(axis=2) & np.isfinite(tn))
             ys, xs = np.nonzero(bad)
             stats["nonfinite_pixels"] = [(int(x), int(y)) for y, x in zip(ys, xs)]
         records = None
         if rec_cap:
-            records = self._records(outs, src, cam)
+            records = self._records(outs, None if self.batch else src, cam)
         timings["total"] = time.perf_counter() - t0
         return FrameOutput(color=color, transmittance=tn, depth=depth, records=records,
                            source_index=src, stats=stats)
@@ -352,8 +398,9 @@ class Renderer:
         spl = outs["rec_splat"].cpu().numpy()
         tt = outs["rec_t"].double().cpu().numpy()
         aa = outs["rec_alpha"].double().cpu().numpy()
-        # Gaussian id -> batch rank (projection preserves source order)
-        rank = np.searchsorted(src, spl)
+        # Gaussian id -> batch rank (projection preserves source order);
+        # a SplatBatch input is indexed by rank already
+        rank = spl if src is None else np.searchsorted(src, spl)
         recs = []
         for y in range(cam.height):
             row = []
@@ -370,8 +417,10 @@ _SCENE_CACHE: dict = {}
 
 def _scene_for(scene, device):
     """Cache the device copy of a host scene (uploaded once, like weights)."""
-    if isinstance(scene, GaussianScene):
+    if isinstance(scene, (GaussianScene, BatchScene)):
         return scene
+    if _is_batch(scene):
+        return BatchScene(scene, device)
     key = (id(scene), len(scene) if hasattr(scene, "__len__") else None)
     hit = _SCENE_CACHE.get(key)
     if hit is not None and hit[0] is scene:

@@ -247,6 +247,29 @@ class RenderConfig:
 
 
 @dataclass
+class SplatBatch:
+    """Projected splats of one camera in SoA form (gaussian_math.py:260-307);
+    ``render`` accepts one in place of Gaussians and skips projection
+    (rasterizer.py:616-618).  conic = (a, b, c); inv_cov3 packed
+    (m00, m11, m22, m01, m02, m12); the batch index is the rank."""
+
+    mean2d: np.ndarray
+    conic: np.ndarray
+    color: np.ndarray
+    opacity: np.ndarray
+    radius: np.ndarray
+    global_depth: np.ndarray
+    inv_cov3: np.ndarray
+    inv_cov_center: np.ndarray
+    mean3d: np.ndarray
+    center_dist: np.ndarray
+    source_index: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.opacity)
+
+
+@dataclass
 class TileBin:
     """rasterizer.py:215-231."""
 

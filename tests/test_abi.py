@@ -51,7 +51,8 @@ def test_struct_layouts_match_header(tmp_path):
     cc = shutil.which("gcc") or shutil.which("cc")
     if cc is None:
         pytest.skip("no C compiler")
-    structs = {"StpScene": _lib.StpScene, "StpCamera": _lib.StpCamera,
+    structs = {"StpScene": _lib.StpScene, "StpSplatBatch": _lib.StpSplatBatch,
+               "StpCamera": _lib.StpCamera,
                "StpConfig": _lib.StpConfig, "StpOutputs": _lib.StpOutputs,
                "StpStats": _lib.StpStats, "StpLayout": _lib.StpLayout}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "stp.h"', 'int main(void){']

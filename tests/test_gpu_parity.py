@@ -154,3 +154,64 @@ def test_dropin_render_matches_reference_api():
     assert out.color.dtype == np.float64 and out.color.shape == (cam.height, cam.width, 3)
     np.testing.assert_allclose(out.color, d["color"], atol=TOL)
     assert out.stats["bin_entries"] == len(d["bin_splat"])
+
+
+def _golden_batch(scene, d):
+    """The reference's own SplatBatch of a golden fixture (gaussian_math.py:260-307)."""
+    from paper_2402_00525_b200 import SplatBatch
+    src = d["source_index"].astype(np.int64)
+    n = len(src)
+    z = np.zeros(n)
+    return SplatBatch(mean2d=d["b_mean2d"], conic=d["b_conic"], color=d["b_color"],
+                      opacity=scene["opacity"][src].astype(np.float64), radius=d["b_radius"],
+                      global_depth=z, inv_cov3=d["b_inv_cov3"],
+                      inv_cov_center=d["b_inv_cov_center"], mean3d=np.zeros((n, 3)),
+                      center_dist=z, source_index=src)
+
+
+@PATHS
+@pytest.mark.parametrize("name", [n for n in golden_io.names() if n != "c1"])
+def test_splatbatch_input_golden(name, exact):
+    """render() on an already-projected SplatBatch (rasterizer.py:616-618),
+    built from the reference's own projection: same tile lists, order, blend
+    sequences and pixels as the reference's Gaussian render."""
+    from dataclasses import replace
+    scene, cam, cfg, mode, d = golden_io.load(name)
+    batch = _golden_batch(scene, d)
+    r = _renderer(batch, mode, replace(cfg, capture_records=True), exact)
+    out = r.frame(cam)
+    assert out.stats["projection"] == {"kept": len(batch)}
+    np.testing.assert_array_equal(out.source_index, d["source_index"])
+    tile, rank, _ = r.debug_bins(cam)                       # batch index = rank
+    np.testing.assert_array_equal(tile, d["bin_tile"])
+    np.testing.assert_array_equal(rank, d["bin_splat"])
+    np.testing.assert_allclose(out.color, d["color"], atol=TOL, rtol=0)
+    np.testing.assert_allclose(out.transmittance, d["transmittance"], atol=TOL, rtol=0)
+    if "depth" in d:
+        np.testing.assert_allclose(out.depth, d["depth"], atol=TOL, rtol=1e-5)
+    for i, (y, x) in enumerate(d["rec_pixels"]):
+        s, t, a = golden_io.records_of(d, i)
+        np.testing.assert_array_equal(out.records[y][x].splat, s)
+
+
+def test_splatbatch_input_oracle_scaled():
+    """SplatBatch path at 40k splats (C2 law) against the oracle's own
+    render of the same batch."""
+    import oracle
+    from paper_2402_00525_b200 import (Camera, Hierarchical, RenderConfig, SplatBatch, render,
+                                       scenes)
+    arrs = scenes.to_f32_scene(scenes.frustum_cloud(40_000, 11, 480, 270, 275.0))
+    cam = Camera(rotation=np.eye(3), position=np.zeros(3), fx=275.0, fy=275.0, width=480,
+                 height=270)
+    cfg = RenderConfig(with_depth=True)
+    ob, _ = oracle.project(arrs, cam, cfg, Hierarchical())
+    batch = SplatBatch(**{k: getattr(ob, k) for k in (
+        "mean2d", "conic", "color", "opacity", "radius", "global_depth", "inv_cov3",
+        "inv_cov_center", "mean3d", "center_dist", "source_index")})
+    out = render(batch, cam, Hierarchical(), cfg)
+    tid, spl, _ = oracle.bin_and_sort(ob, cam, cfg, Hierarchical())
+    ref = oracle.render_bins(ob, cam, tid, spl, cfg, Hierarchical())
+    assert out.stats["bin_entries"] == len(spl)
+    np.testing.assert_allclose(out.color, ref["color"], atol=TOL, rtol=0)
+    np.testing.assert_allclose(out.transmittance, ref["transmittance"], atol=TOL, rtol=0)
+    np.testing.assert_allclose(out.depth, ref["depth"], atol=TOL, rtol=1e-5)
