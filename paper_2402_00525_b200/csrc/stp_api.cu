@@ -230,10 +230,19 @@ int fill_stats(const void* ws, size_t ws_bytes, int64_t n, int32_t W, int32_t H,
     return STP_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return STP_ERR_CUDA;
   st->input = n;
-  st->behind = (int64_t)c[C_BEHIND];
-  st->guard = (int64_t)c[C_GUARD];
-  st->degenerate = (int64_t)c[C_DEGEN];
-  st->kept = (int64_t)c[C_KEPT];
+  {
+    unsigned long long ps[256 * 4];
+    if (cudaMemcpyAsync(ps, static_cast<const unsigned char*>(ws) + L.counters + C_PSTAT * 8,
+                        sizeof(ps), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return STP_ERR_CUDA;
+    int64_t t[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 256 * 4; ++i) t[i & 3] += (int64_t)ps[i];
+    st->behind = t[0];
+    st->guard = t[1];
+    st->degenerate = t[2];
+    st->kept = t[3];
+  }
   st->bin_entries = (int64_t)c[C_ENTRIES];
   st->tiles = (int64_t)c[C_TILES];
   st->nonfinite_pixels = (int64_t)c[C_NONFINITE];

@@ -93,7 +93,8 @@ enum Counter {
   C_SM = 64,        // render: per-SM sub-tile counters [256]
   C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
   C_RES = 320 + 256 * 16,   // render: per-SM float64 resolution counts [256]
-  C_COUNT = C_RES + 256
+  C_PSTAT = C_RES + 256,    // K1: per-SM projection stats [256][4] (behind, guard, degenerate, kept)
+  C_COUNT = C_PSTAT + 256 * 4
 };
 
 // ---------------------------------------------------------------------------

@@ -16,6 +16,12 @@
 namespace stp {
 
 constexpr int kPreThreads = 256;
+#ifndef STP_K1_MINB
+#define STP_K1_MINB 3
+#endif
+#ifndef STP_SPLIT_SH
+#define STP_SPLIT_SH 0
+#endif
 
 __constant__ double c_SH_C0 = 0.28209479177387814;
 __constant__ double c_SH_C1 = 0.4886025119029199;
@@ -255,19 +261,36 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
     if (cnt) masks[i] = s_mask[threadIdx.x];
     if (state) state[i] = (uint8_t)reason;
   }
-  const int n_behind = __syncthreads_count(reason == 1);
-  const int n_guard = __syncthreads_count(reason == 2);
-  const int n_degen = __syncthreads_count(reason == 3);
-  const int n_kept = __syncthreads_count(reason == 0);
+  // projection stats: warp ballots into shared counters, one barrier
+  __shared__ int s_st[4];
+  if (threadIdx.x < 4) s_st[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    const unsigned b1 = __ballot_sync(kFull, reason == 1), b2 = __ballot_sync(kFull, reason == 2);
+    const unsigned b3 = __ballot_sync(kFull, reason == 3), b0 = __ballot_sync(kFull, reason == 0);
+    if (lane == 0) {
+      if (b1) atomicAdd(&s_st[0], __popc(b1));
+      if (b2) atomicAdd(&s_st[1], __popc(b2));
+      if (b3) atomicAdd(&s_st[2], __popc(b3));
+      if (b0) atomicAdd(&s_st[3], __popc(b0));
+    }
+  }
+  __syncthreads();
+  const int n_behind = s_st[0], n_guard = s_st[1], n_degen = s_st[2], n_kept = s_st[3];
   if (threadIdx.x == 0) {
-    if (n_behind) atomicAdd(counters + C_BEHIND, (unsigned long long)n_behind);
-    if (n_guard) atomicAdd(counters + C_GUARD, (unsigned long long)n_guard);
-    if (n_degen) atomicAdd(counters + C_DEGEN, (unsigned long long)n_degen);
-    if (n_kept) atomicAdd(counters + C_KEPT, (unsigned long long)n_kept);
+    // per-SM slots: one global counter per stat would take ~12k serialised
+    // atomics per frame
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* ps = counters + C_PSTAT + (smid & 255) * 4;
+    if (n_behind) atomicAdd(ps + 0, (unsigned long long)n_behind);
+    if (n_guard) atomicAdd(ps + 1, (unsigned long long)n_guard);
+    if (n_degen) atomicAdd(ps + 2, (unsigned long long)n_degen);
+    if (n_kept) atomicAdd(ps + 3, (unsigned long long)n_kept);
   }
 }
 
-__global__ void __launch_bounds__(kPreThreads) k_preprocess(
+__global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
     uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
@@ -398,6 +421,11 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.q0 = inv3[0] * rel0 + inv3[1] * rel1 + inv3[2] * rel2;
           r.q1 = inv3[3] * rel0 + inv3[4] * rel1 + inv3[5] * rel2;
           r.q2 = inv3[6] * rel0 + inv3[7] * rel1 + inv3[8] * rel2;
+#if STP_SPLIT_SH
+          // SH colour: K1b (k_shade), for the splats that reach a tile
+          r.c0 = r.c1 = r.c2 = 0.f;
+          const float col[3] = {0.f, 0.f, 0.f};
+#else
           // SH colour along (mean - origin) / |mean - origin| (:415-419)
           const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
           float col[3];
@@ -406,6 +434,7 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
           r.c0 = col[0];
           r.c1 = col[1];
           r.c2 = col[2];
+#endif
           int x0, x1, y0, y1;
           coarse_rect(px, py, radius, gw, gh, x0, x1, y0, y1);
           r.rx0 = (int16_t)x0;
@@ -469,6 +498,34 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(
   }
 
   count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
+}
+
+// ---------------------------------------------------------------------------
+// K1b: SH colour (gaussian_math.py:152-175, 415-419) of the splats that reach
+// at least one tile, as a separate streaming kernel: keeping the 192 B of SH
+// coefficients out of K1 leaves K1 fewer registers and the loads here all
+// in flight at full occupancy.
+__global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
+                                               const uint32_t* __restrict__ counts,
+                                               SplatRec* __restrict__ recs,
+                                               SplatRec32* __restrict__ recs32) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= sc.n || counts[i] == 0) return;
+  const double rel0 = (double)__ldg(sc.means + 3 * i + 0) - cam.pos[0];
+  const double rel1 = (double)__ldg(sc.means + 3 * i + 1) - cam.pos[1];
+  const double rel2 = (double)__ldg(sc.means + 3 * i + 2) - cam.pos[2];
+  const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
+  float col[3];
+  sh_color(sc.sh + i * sc.sh_coeffs * 3, sc.sh_coeffs, (float)(rel0 / dist),
+           (float)(rel1 / dist), (float)(rel2 / dist), col);
+  recs[i].c0 = col[0];
+  recs[i].c1 = col[1];
+  recs[i].c2 = col[2];
+  if (recs32) {
+    recs32[i].c0 = col[0];
+    recs32[i].c1 = col[1];
+    recs32[i].c2 = col[2];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -656,7 +713,6 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
     int depth_bits, int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  __shared__ SplatRec s_rec[kPreThreads];
   __shared__ uint32_t s_pos[kPreThreads];
   __shared__ unsigned long long s_m[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
@@ -664,9 +720,8 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
   const uint32_t cnt = (i < n) ? counts[i] : 0;
   int area = 0;
   if (cnt > 0) {
-    const SplatRec r = recs[i];
-    s_rec[threadIdx.x] = r;
-    area = (r.rx1 - r.rx0 + 1) * (r.ry1 - r.ry0 + 1);
+    const short4 rc = *reinterpret_cast<const short4*>(&recs[i].rx0);
+    area = (rc.y - rc.x + 1) * (rc.w - rc.z + 1);
     // rects of <= 64 tiles: K1 left the survivors' positions in a mask, so
     // only surviving pairs are enumerated (no second cull)
     if (area <= 64) area = (int)cnt;
@@ -677,7 +732,8 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
   const int wbase = threadIdx.x & ~31;
   const unsigned lt_mask = (1u << lane) - 1;
   warp_expand(area, lane, [&](bool v, int owner, int local) {
-    const SplatRec& r = s_rec[wbase + owner];
+    // the owner's record straight from L1/L2 (lanes of one owner broadcast)
+    const SplatRec& r = recs[(int64_t)blockIdx.x * kPreThreads + wbase + owner];
     bool keep = false;
     int tx = 0, ty = 0;
     double ptx = 0.0, pty = 0.0;
@@ -735,6 +791,10 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                       f.exact_only ? nullptr : f.recs32, f.masks,
                                                       f.counts, f.state, f.counters);
+#if STP_SPLIT_SH
+  k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs,
+                                           f.exact_only ? nullptr : f.recs32);
+#endif
 }
 
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
