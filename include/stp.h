@@ -138,13 +138,14 @@ typedef struct {
 
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
-  size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals0, vals1, ranges,
+  size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
       counters, hist, lookback, scan_scratch, total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;
   int32_t splat_record_bytes;
-  int32_t final_buffer;     /* 0: sorted keys/vals in keys0/vals0, 1: keys1/vals1 */
-  int32_t depth_bits;       /* key = tile << depth_bits | depth key >> (32 - depth_bits) */
+  int32_t final_buffer;     /* sorted entry words in keys0 (0) or keys1 (1)     */
+  int32_t depth_bits;       /* entry word = (tile << depth_bits |               */
+  int32_t id_bits;          /*   depth key >> (32 - depth_bits)) << id_bits | id */
 } StpLayout;
 
 int stp_abi_version(void);

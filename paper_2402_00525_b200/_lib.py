@@ -78,13 +78,14 @@ class StpStats(ctypes.Structure):
 
 class StpLayout(ctypes.Structure):
     _fields_ = [(n, ctypes.c_size_t) for n in (
-        "recs", "recs32", "fb_items", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals0", "vals1", "ranges",
+        "recs", "recs32", "fb_items", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals", "ranges",
         "counters", "hist", "lookback", "scan_scratch", "total")] + [
         ("entry_capacity", ctypes.c_int64), ("n_tiles", ctypes.c_int32),
         ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32),
         ("sort_passes", ctypes.c_int32), ("sort_bits", ctypes.c_int32),
         ("partitions", ctypes.c_int32), ("splat_record_bytes", ctypes.c_int32),
-        ("final_buffer", ctypes.c_int32), ("depth_bits", ctypes.c_int32)]
+        ("final_buffer", ctypes.c_int32), ("depth_bits", ctypes.c_int32),
+        ("id_bits", ctypes.c_int32)]
 
 
 _lib = None

@@ -26,18 +26,24 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.grid_w = (W + kTile - 1) / kTile;
   L.grid_h = (H + kTile - 1) / kTile;
   L.n_tiles = L.grid_w * L.grid_h;
-  // key = tile << depth_bits | top depth_bits of the fp32-orderable depth:
-  // the depth part fills the last 8-bit digit (>= 24 bits), so a 1080p frame
-  // sorts 40 bits in 5 passes; K5 re-orders runs of equal keys by the
-  // float64 depth, which makes the truncation invisible in the final order.
+  // One 64-bit word per (tile, splat) entry:
+  //   (tile << depth_bits | top depth_bits of the fp32-orderable depth) << id_bits | id
+  // The sort key (tile | depth) fills whole 8-bit digits (depth >= 24 bits
+  // when the word allows), so a 1080p frame sorts 40 bits in 5 passes that
+  // move 8 B per entry; the id rides along in the low bits (stable LSD keeps
+  // Gaussian order inside equal keys = the rank tie-break).  K5 re-orders
+  // runs of equal keys by the float64 depth, which makes the truncation
+  // invisible in the final order.
   {
     const int tb = tile_bits(L.n_tiles);
-    L.sort_bits = ((tb + 24 + 7) / 8) * 8;
-    L.depth_bits = L.sort_bits - tb;
-    if (L.depth_bits > 32) {
-      L.depth_bits = 32;
-      L.sort_bits = tb + 32;
-    }
+    int ib = 1;
+    while (ib < 31 && (int64_t)1 << ib < n) ++ib;
+    L.id_bits = ib;
+    int kb = ((tb + 24 + 7) / 8) * 8;
+    if (kb > 64 - ib) kb = 64 - ib;
+    if (kb - tb > 32) kb = tb + 32;
+    L.sort_bits = kb;
+    L.depth_bits = kb - tb;
   }
   L.sort_passes = (L.sort_bits + 7) / 8;
   L.entry_capacity = ecap;
@@ -61,19 +67,18 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.lookback = o;     o = align_up(o + (size_t)L.sort_passes * L.partitions * 256 * 8);
   L.keys0 = o;        o = align_up(o + (size_t)ecap * 8);
   L.keys1 = o;        o = align_up(o + (size_t)ecap * 8);
-  L.vals0 = o;        o = align_up(o + (size_t)ecap * 4);
-  L.vals1 = o;        o = align_up(o + (size_t)ecap * 4);
+  L.vals = o;         o = align_up(o + (size_t)ecap * 4);
   L.total = o;
 }
 
 int64_t max_capacity(int64_t n, int32_t W, int32_t H, size_t ws_bytes) {
-  // per-entry bytes: 2 x (8 + 4) + lookback (passes * 256 * 8 / 4096)
+  // per-entry bytes: 2 x 8 (keys) + 4 (ids) + lookback (passes * 256 * 8 / 4096)
   StpLayout L0;
   plan(n, W, H, 0, L0);
   if (ws_bytes < L0.total) return -1;
   // largest e with plan(e).total <= ws_bytes (monotone in e): binary search
   // from the per-entry estimate, so stp_workspace_bytes(.., e) round-trips
-  const double per = 24.0 + (double)L0.sort_passes * 256 * 8 / kSortTile;
+  const double per = 20.0 + (double)L0.sort_passes * 256 * 8 / kSortTile;
   int64_t hi = (int64_t)((double)(ws_bytes - L0.total) / per) + kSortTile + 1;
   int64_t lo = 0;
   StpLayout L;
@@ -130,8 +135,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.offsets = reinterpret_cast<uint32_t*>(b + L.offsets);
   f.keys[0] = reinterpret_cast<uint64_t*>(b + L.keys0);
   f.keys[1] = reinterpret_cast<uint64_t*>(b + L.keys1);
-  f.vals[0] = reinterpret_cast<uint32_t*>(b + L.vals0);
-  f.vals[1] = reinterpret_cast<uint32_t*>(b + L.vals1);
+  f.vals = reinterpret_cast<uint32_t*>(b + L.vals);
   f.ranges = reinterpret_cast<uint2*>(b + L.ranges);
   f.counters = reinterpret_cast<unsigned long long*>(b + L.counters);
   f.hist = reinterpret_cast<uint32_t*>(b + L.hist);
@@ -144,6 +148,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.n_tiles = L.n_tiles;
   f.passes = L.sort_passes;
   f.depth_bits = L.depth_bits;
+  f.id_bits = L.id_bits;
   f.partitions = L.partitions;
   memcpy(f.cam.R, cam->R, sizeof(f.cam.R));
   memcpy(f.cam.pos, cam->pos, sizeof(f.cam.pos));

@@ -315,8 +315,8 @@ struct Frame {
   uint8_t* state;
   uint32_t* counts;
   uint32_t* offsets;
-  uint64_t* keys[2];
-  uint32_t* vals[2];
+  uint64_t* keys[2];      // packed entry words (ping-pong)
+  uint32_t* vals;         // sorted Gaussian ids (written by K5)
   uint2* ranges;
   unsigned long long* counters;
   uint32_t* hist;         // [passes][256]
@@ -326,7 +326,8 @@ struct Frame {
   int64_t ecap;
   int gw, gh, n_tiles;
   int passes, partitions;
-  int depth_bits;         // sort key = tile << depth_bits | truncated depth key
+  int depth_bits;         // entry word = (tile << depth_bits | truncated depth key) << id_bits | id
+  int id_bits;
   int exact_only;         // no STP_FLAG_FAST32: every item through the fp64 kernel
   int fb_test;            // STP_FLAG_FB_TEST
   DevCam cam;

@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec* __restrict__ recs, const uint64_t* __restrict__ masks,
     const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
-    int depth_bits, int64_t ecap, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    int depth_bits, int id_bits, int64_t ecap, uint64_t* __restrict__ keys) {
   __shared__ uint32_t s_pos[kPreThreads];
   __shared__ unsigned long long s_m[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
@@ -765,9 +765,9 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
       const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
-        keys[pos] = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
-                    (depth_key(depth) >> (32 - depth_bits));
-        vals[pos] = (uint32_t)(blockIdx.x * kPreThreads + wbase + owner);
+        const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
+                             (depth_key(depth) >> (32 - depth_bits));
+        keys[pos] = (key << id_bits) | (uint64_t)(blockIdx.x * kPreThreads + wbase + owner);
       }
     }
     if (v && lane == __ffs(peers) - 1 && kb) s_pos[wbase + owner] = base + __popc(kb);
@@ -818,8 +818,8 @@ void launch_duplicate(const Frame& f, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
                                                      f.cam,
-                                                     f.cfg, f.gw, f.depth_bits, f.ecap, f.keys[0],
-                                                     f.vals[0]);
+                                                     f.cfg, f.gw, f.depth_bits, f.id_bits, f.ecap,
+                                                     f.keys[0]);
 }
 
 }  // namespace stp

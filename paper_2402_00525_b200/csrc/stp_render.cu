@@ -771,7 +771,7 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   RenderArgs A;
   A.list = f.exact_only ? nullptr : f.fb_items;
   A.recs = f.recs;
-  A.vals = f.vals[buf];
+  A.vals = f.vals;
   A.ranges = f.ranges;
   A.cam = f.cam;
   A.cfg = f.cfg;

@@ -805,7 +805,7 @@ void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStre
   FastArgs A;
   A.recs = f.recs;
   A.r32 = f.recs32;
-  A.vals = f.vals[buf];
+  A.vals = f.vals;
   A.ranges = f.ranges;
   A.camp = f.camp;
   A.cam = f.cam;

@@ -1,6 +1,7 @@
 // K4: hand-written onesweep LSD radix sort (Adinets & Merrill 2022 scheme)
-//     over the 64-bit (tile << depth_bits | truncated depth key) keys with uint32 Gaussian-id
-//     values; replaces np.lexsort((rank, key, tile_id)) (rasterizer.py:353-357).
+//     over 64-bit entry words ((tile | truncated depth key) << id_bits | id):
+//     the passes cover the key bits only and the Gaussian id rides in the
+//     low bits; replaces np.lexsort((rank, key, tile_id)) (rasterizer.py:353-357).
 //     8-bit digits, ceil((32 + tile_bits) / 8) passes, one global-histogram
 //     pass up front, per-partition decoupled look-back with epoch-tagged
 //     status words (no per-frame clearing).  Stable: partitions are ranked in
@@ -32,7 +33,7 @@ __device__ __forceinline__ int64_t n_entries(const unsigned long long* counters,
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ keys,
                                                             const unsigned long long* counters,
-                                                            int64_t ecap, int passes,
+                                                            int64_t ecap, int passes, int shift0,
                                                             uint32_t* __restrict__ hist) {
   __shared__ uint32_t s_hist[8][kRadix];
   for (int i = threadIdx.x; i < 8 * kRadix; i += kSortThreads) (&s_hist[0][0])[i] = 0;
@@ -41,7 +42,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
   for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * kSortThreads) {
     const uint64_t k = keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (8 * p)) & 0xff], 1u);
+    for (int p = 0; p < passes; ++p)
+      atomicAdd(&s_hist[p][(k >> (shift0 + 8 * p)) & 0xff], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += kSortThreads) {
@@ -57,12 +59,10 @@ struct SortSmem {
   uint32_t scan_tmp[kRadix];
   uint32_t part;
   uint64_t keys[kSortTile];
-  uint32_t vals[kSortTile];
 };
 
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
-    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+    const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const unsigned long long* counters, int64_t ecap, int shift,
     const uint32_t* __restrict__ hist, unsigned long long* lookback,
     unsigned long long* part_counter) {
@@ -81,7 +81,6 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 
   // warp-striped load: warp w owns [base + w*512, +512), item k of lane l at k*32 + l
   uint64_t key[kSortItems];
-  uint32_t val[kSortItems];
   uint32_t dig[kSortItems];
   uint32_t rank[kSortItems];
 #pragma unroll
@@ -89,11 +88,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const int li = w * (kSortItems * 32) + k * 32 + lane;
     if (li < n_valid) {
       key[k] = kin[base + li];
-      val[k] = vin[base + li];
       dig[k] = (uint32_t)(key[k] >> shift) & 0xff;
     } else {
       key[k] = ~0ull;
-      val[k] = 0;
       dig[k] = 0xff;
     }
   }
@@ -169,10 +166,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 #pragma unroll
   for (int k = 0; k < kSortItems; ++k) {
     const uint32_t pos = sm.local_off[dig[k]] + sm.warp_hist[w][dig[k]] + rank[k];
-    if (pos < (uint32_t)kSortTile) {
-      sm.keys[pos] = key[k];
-      sm.vals[pos] = val[k];
-    }
+    if (pos < (uint32_t)kSortTile) sm.keys[pos] = key[k];
   }
   __syncthreads();
   for (int i = tid; i < n_valid; i += kSortThreads) {
@@ -180,7 +174,6 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint32_t d = (uint32_t)(k >> shift) & 0xff;
     const uint32_t o = sm.global_off[d] + (uint32_t)i - sm.local_off[d];
     kout[o] = k;
-    vout[o] = sm.vals[i];
   }
 }
 
@@ -221,20 +214,24 @@ __device__ __forceinline__ int block_sum(int v) {
 // registers / shared memory and added with one atomic per block (a per-entry
 // or per-warp atomic on one counter serialises tens of thousands of updates).
 __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys,
-                                                const uint32_t* __restrict__ vals,
+                                                uint32_t* __restrict__ vals,
                                                 unsigned long long* counters, int64_t ecap,
                                                 uint2* __restrict__ ranges,
                                                 const SplatRec* __restrict__ recs, DevCam cam,
-                                                int gw, int depth_bits,
+                                                int gw, int depth_bits, int id_bits,
                                                 double* __restrict__ d64) {
   const int64_t E = n_entries(counters, ecap);
+  const uint64_t id_mask = (1ull << id_bits) - 1ull;
   int heads = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
+    const uint64_t w = keys[i];
+    const uint64_t k = w >> id_bits;                      // tile | truncated depth
     const uint32_t tile = (uint32_t)(k >> depth_bits);
-    const uint64_t kp = (i > 0) ? keys[i - 1] : ~k;
-    const uint64_t kn = (i + 1 < E) ? keys[i + 1] : ~k;
+    const uint64_t kp = (i > 0) ? keys[i - 1] >> id_bits : ~k;
+    const uint64_t kn = (i + 1 < E) ? keys[i + 1] >> id_bits : ~k;
+    const uint32_t id = (uint32_t)(w & id_mask);
+    vals[i] = id;
     if (i == 0 || (uint32_t)(kp >> depth_bits) != tile) {
       ranges[tile].x = (uint32_t)i;
       ++heads;
@@ -243,8 +240,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
     // members of a run of equal keys (same tile, same truncated depth key):
     // their float64 depths, computed in parallel, go to the free ping-pong
     // buffer for k_ties
-    if (kn == k || (i > 0 && kp == k))
-      d64[i] = entry_depth64(recs, cam, vals[i], (int)tile, gw);
+    if (kn == k || (i > 0 && kp == k)) d64[i] = entry_depth64(recs, cam, id, (int)tile, gw);
   }
   const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
   if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
@@ -255,16 +251,19 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
 __global__ void __launch_bounds__(256) k_ties(const uint64_t* __restrict__ keys,
                                               uint32_t* __restrict__ vals,
                                               double* __restrict__ d64,
-                                              unsigned long long* counters, int64_t ecap) {
+                                              unsigned long long* counters, int64_t ecap,
+                                              int id_bits) {
   const int64_t E = n_entries(counters, ecap);
   int runs = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    if (!((i + 1 < E && keys[i + 1] == k) && (i == 0 || keys[i - 1] != k))) continue;
+    const uint64_t k = keys[i] >> id_bits;
+    if (!((i + 1 < E && (keys[i + 1] >> id_bits) == k) &&
+          (i == 0 || (keys[i - 1] >> id_bits) != k)))
+      continue;
     ++runs;
     int64_t L = 2;
-    while (i + L < E && keys[i + L] == k) ++L;
+    while (i + L < E && (keys[i + L] >> id_bits) == k) ++L;
     if (L <= kTieLocal) {
       double d[kTieLocal];
       uint32_t id[kTieLocal];
@@ -320,11 +319,11 @@ int launch_sort(const Frame& f, cudaStream_t s) {
   }
   const int hist_blocks = 148 * 4;
   k_sort_hist<<<hist_blocks, kSortThreads, 0, s>>>(f.keys[0], f.counters, f.ecap, f.passes,
-                                                    f.hist);
+                                                    f.id_bits, f.hist);
   int cur = 0;
   for (int p = 0; p < f.passes; ++p) {
     k_onesweep<<<f.partitions, kSortThreads, sizeof(SortSmem), s>>>(
-        f.keys[cur], f.vals[cur], f.keys[cur ^ 1], f.vals[cur ^ 1], f.counters, f.ecap, 8 * p,
+        f.keys[cur], f.keys[cur ^ 1], f.counters, f.ecap, f.id_bits + 8 * p,
         f.hist + p * kRadix, f.lookback + (size_t)p * f.partitions * kRadix,
         f.counters + C_PART + p);
     cur ^= 1;
@@ -337,9 +336,10 @@ void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
   const int64_t blocks = min((int64_t)148 * 8, (f.ecap + 255) / 256);
   // the other ping-pong key buffer (E x 8 B) is free: float64 depths of tie runs
   double* d64 = reinterpret_cast<double*>(f.keys[buf ^ 1]);
-  k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], f.counters, f.ecap,
-                                            f.ranges, f.recs, f.cam, f.gw, f.depth_bits, d64);
-  k_ties<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals[buf], d64, f.counters, f.ecap);
+  k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, f.counters, f.ecap, f.ranges,
+                                            f.recs, f.cam, f.gw, f.depth_bits, f.id_bits, d64);
+  k_ties<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, d64, f.counters, f.ecap,
+                                          f.id_bits);
 }
 
 }  // namespace stp

@@ -385,12 +385,13 @@ class Renderer:
             _raise(rc, "stp_read_stats")
         E = int(st.bin_entries)
         ko = L.keys1 if L.final_buffer else L.keys0
-        vo = L.vals1 if L.final_buffer else L.vals0
+        vo = L.vals
         keys = self.ws.buf[ko: ko + 8 * E].view(torch.int64).cpu().numpy().view(np.uint64)
         vals = self.ws.buf[vo: vo + 4 * E].view(torch.int32).cpu().numpy()
-        db = np.uint64(L.depth_bits)
-        return (keys >> db).astype(np.int64), vals.astype(np.int64), \
-            ((keys & ((np.uint64(1) << db) - np.uint64(1))) << (np.uint64(32) - db)).astype(np.uint32)
+        db, ib = np.uint64(L.depth_bits), np.uint64(L.id_bits)
+        key = keys >> ib
+        return (key >> db).astype(np.int64), vals.astype(np.int64), \
+            ((key & ((np.uint64(1) << db) - np.uint64(1))) << (np.uint64(32) - db)).astype(np.uint32)
 
     @staticmethod
     def _records(outs, src, cam):

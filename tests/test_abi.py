@@ -122,11 +122,11 @@ def test_workspace_layout(lib):
     assert lib.stp_workspace_layout(n, W, H, b1, ctypes.byref(L)) == _lib.STP_OK
     assert L.entry_capacity >= 100_000 and L.total <= b1
     assert (L.grid_w, L.grid_h, L.n_tiles) == (120, 68, 8160)
-    # 13 tile bits + 27 depth bits: 5 eight-bit passes
-    assert (L.sort_bits, L.depth_bits, L.sort_passes) == (40, 27, 5)
+    # 13 tile bits + 27 depth bits: 5 eight-bit passes; ids in the low 10 bits
+    assert (L.sort_bits, L.depth_bits, L.sort_passes, L.id_bits) == (40, 27, 5, 10)
     regions = sorted((getattr(L, k), k) for k in ("recs", "recs32", "fb_items", "camera", "masks",
                                                     "state", "counts", "offsets", "keys0",
-                                                    "keys1", "vals0", "vals1", "ranges",
+                                                    "keys1", "vals", "ranges",
                                                     "counters", "hist", "lookback",
                                                     "scan_scratch"))
     offs = [o for o, _ in regions]
@@ -137,6 +137,14 @@ def test_workspace_layout(lib):
     b = lib.stp_workspace_bytes(n, 3840, 2160, 1000)
     assert lib.stp_workspace_layout(n, 3840, 2160, b, ctypes.byref(L)) == _lib.STP_OK
     assert L.n_tiles == 32400 and (L.sort_bits, L.depth_bits) == (40, 25)
+    # 6M Gaussians at 4K: 23 id bits, 15 tile + 25 depth bits = 63
+    b = lib.stp_workspace_bytes(6_000_000, 3840, 2160, 1000)
+    assert lib.stp_workspace_layout(6_000_000, 3840, 2160, b, ctypes.byref(L)) == _lib.STP_OK
+    assert (L.id_bits, L.sort_bits, L.sort_passes) == (23, 40, 5)
+    # 100M Gaussians: the word keeps 64 - 27 = 37 key bits (22 depth bits)
+    b = lib.stp_workspace_bytes(100_000_000, 3840, 2160, 1000)
+    assert lib.stp_workspace_layout(100_000_000, 3840, 2160, b, ctypes.byref(L)) == _lib.STP_OK
+    assert (L.id_bits, L.sort_bits, L.depth_bits) == (27, 37, 22)
 
 
 def test_host_mode_validation_mirrors_reference():
