@@ -334,15 +334,23 @@ __device__ __forceinline__ int count_below_f(const Key* ad, const uint32_t* ai, 
 }
 
 // ---------------------------------------------------------------------------
-// shared-memory queues of one sub-tile (4-byte keys and ids):
-// keys [tail0 qt | tail1 qt | batch 32 | mid 4*qm | scratch 4*(qm+4) | groups 64]
-// ids  [same layout | ring 4*R]
-__host__ __device__ inline int fsub_nk(int qt, int qm) {
-  return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64;
-}
+// shared-memory queues of one sub-tile (4-byte keys and ids), addressed
+// arithmetically:
+//   keys [tail0 qt | tail1 qt | batch 32 | mid 4 x qm | scratch 4 x (qm+5) |
+//         pad | groups 4 x 17]   ids [same | rings 4 x (R+1)]
+// Bank-conflict-free for the 4 quads read by one instruction (mid merge,
+// pixel rings): group base 4 banks past the mids, odd strides.
 __host__ __device__ inline int fring_size(int qm) { return qm <= 16 ? 64 : 128; }
+__host__ __device__ inline int fq_mid0(int qt) { return 2 * qt + 32; }
+__host__ __device__ inline int fq_scr0(int qt, int qm) { return fq_mid0(qt) + 4 * qm; }
+__host__ __device__ inline int fq_grp0(int qt, int qm) {
+  const int b = fq_scr0(qt, qm) + 4 * (qm + 5);
+  return b + ((fq_mid0(qt) + 4 - b) & 31);
+}
+__host__ __device__ inline int fq_ring0(int qt, int qm) { return fq_grp0(qt, qm) + 4 * 17; }
+__host__ __device__ inline int fsub_nk(int qt, int qm) { return fq_ring0(qt, qm); }
 __host__ __device__ inline size_t fwarp_smem_bytes(int qt, int qm) {
-  return (size_t)2 * (2 * fsub_nk(qt, qm) + 4 * fring_size(qm)) * 4;
+  return (size_t)2 * (2 * fsub_nk(qt, qm) + 4 * (fring_size(qm) + 1)) * 4;
 }
 
 struct SubQF {
@@ -353,13 +361,11 @@ struct SubQF {
   __device__ __forceinline__ uint32_t* ti(int c) const { return i + c * qt; }
   __device__ __forceinline__ Key* bd() const { return d + 2 * qt; }
   __device__ __forceinline__ uint32_t* bi() const { return i + 2 * qt; }
-  __device__ __forceinline__ int o_mid(int q) const { return 2 * qt + 32 + q * qm; }
-  __device__ __forceinline__ int o_scr(int q) const { return 2 * qt + 32 + 4 * qm + q * (qm + 4); }
-  __device__ __forceinline__ int o_grp(int q) const {
-    return 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 16 * q;
-  }
+  __device__ __forceinline__ int o_mid(int q) const { return fq_mid0(qt) + q * qm; }
+  __device__ __forceinline__ int o_scr(int q) const { return fq_scr0(qt, qm) + q * (qm + 5); }
+  __device__ __forceinline__ int o_grp(int q) const { return fq_grp0(qt, qm) + 17 * q; }
   __device__ __forceinline__ uint32_t* ring(int q, int R) const {
-    return i + 2 * qt + 32 + 4 * qm + 4 * (qm + 4) + 64 + q * R;
+    return i + fq_ring0(qt, qm) + q * (R + 1);
   }
 };
 
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(kFThreads, STP_FAST_MINB) k_render_fast(FastAr
   const int R = fring_size(qm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* wbase = smem_raw + warp * fwarp_smem_bytes(qt, qm);
-  const int nk = fsub_nk(qt, qm), ni = fsub_nk(qt, qm) + 4 * R;
+  const int nk = fsub_nk(qt, qm), ni = fsub_nk(qt, qm) + 4 * (R + 1);
   auto subq = [&](int s) {
     SubQF q;
     q.d = reinterpret_cast<Key*>(wbase) + s * nk;
