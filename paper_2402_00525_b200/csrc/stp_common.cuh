@@ -133,8 +133,8 @@ __device__ __forceinline__ void max_point(double mx, double my, double a, double
                                           double inv_a, double inv_c, double xmin, double ymin,
                                           double w, double iw, double& ox, double& oy) {
   const double xmax = xmin + w, ymax = ymin + w;
-  const bool inside_x = (mx >= xmin) && (mx <= xmax);
-  const bool inside_y = (my >= ymin) && (my <= ymax);
+  const bool inside_x = (mx >= xmin) & (mx <= xmax);
+  const bool inside_y = (my >= ymin) & (my <= ymax);
   if (inside_x && inside_y) {
     ox = mx;
     oy = my;

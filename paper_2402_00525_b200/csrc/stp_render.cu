@@ -235,14 +235,14 @@ __device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1,
       const double od1 = shfl_xor_d(d1, j);
       const uint32_t oi1 = __shfl_xor_sync(kFull, i1, j);
       const bool want_min = (((lane & j) == 0) == ((lane & k) == 0));
-      if (want_min ? lt(od0, oi0, d0, i0) : lt(d0, i0, od0, oi0)) {
-        d0 = od0;
-        i0 = oi0;
-      }
-      if (want_min ? lt(od1, oi1, d1, i1) : lt(d1, i1, od1, oi1)) {
-        d1 = od1;
-        i1 = oi1;
-      }
+      // elements are distinct (ids unique) except empty slots, whose swap is
+      // a no-op: "partner < me" decides both directions with one compare
+      const bool take0 = want_min == lt(od0, oi0, d0, i0);
+      const bool take1 = want_min == lt(od1, oi1, d1, i1);
+      d0 = take0 ? od0 : d0;
+      i0 = take0 ? oi0 : i0;
+      d1 = take1 ? od1 : d1;
+      i1 = take1 ? oi1 : i1;
     }
   }
 }
