@@ -27,11 +27,12 @@ struct __align__(16) SplatRec {
   double mx, my;        // mean2d (pixels)                                   0
   double ca, cb, cc;    // conic (a, b, c)                                   16
   double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr  40
-  double m[6];          // packed inverse covariance (m00,m11,m22,m01,m02,m12) 48
-  double q0, q1;        // inv_cov3 (mean - camera origin), x and y          96
+  double m[6];          // camera-space M' = R inv_cov3 R^T as                48
+                        // (m00, m11, m22, 2 m01, 2 m02, 2 m12)
+  double q0, q1;        // q' = M' p_view (= R inv_cov3 (mean - origin)), x y 96
   float op;             // opacity                                           112
   float c0, c1, c2;     // SH colour (lower-clamped at 0)
-  double q2;            // inv_cov3 (mean - camera origin), z                128
+  double q2;            // q', z                                             128
   int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)
   double inv_a, inv_c;  // 1/a, 1/c for the Alg. 1 edge searches            144
 };
@@ -257,6 +258,32 @@ __device__ __forceinline__ double key_cam(const SplatRec32* __restrict__ r, doub
   const double N = fma(u, qa.y, fma(w, qb.x, qb.y));
   const double D = fma(u, fma(ma.x, u, fma(mb.y, w, mc.x)), fma(w, fma(ma.y, w, mc.y), mb.x));
   return vn * fdiv(N, D);
+}
+
+// the same from a SplatRec (camera-space M', q')
+__device__ __forceinline__ double key_rec(const double* m, double q0, double q1, double q2,
+                                          double u, double w, double vn) {
+  const double N = fma(u, q0, fma(w, q1, q2));
+  const double D = fma(u, fma(m[0], u, fma(m[3], w, m[4])), fma(w, fma(m[1], w, m[5]), m[2]));
+  return vn * fdiv(N, D);
+}
+
+// camera ray (u, w, 1) through a float64 image point and its length
+__device__ __forceinline__ void cam_ray(const DevCam& cam, double x, double y, double& u,
+                                        double& w, double& vn) {
+  u = (x - cam.cx) * cam.inv_fx;
+  w = (y - cam.cy) * cam.inv_fy;
+  const double vv = fma(u, u, fma(w, w, 1.0));
+  vn = vv * frsqrt(vv);
+}
+
+// t_opt of a SplatRec along the ray through a float64 image point
+// (tile_culling.py:161-195 in the camera-space form)
+__device__ __forceinline__ double key_rec_at(const DevCam& cam, const SplatRec& r, double x,
+                                             double y) {
+  double u, w, vn;
+  cam_ray(cam, x, y, u, w, vn);
+  return key_rec(r.m, r.q0, r.q1, r.q2, u, w, vn);
 }
 
 // camera ray of a float64 image point and the key along it

@@ -412,15 +412,30 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
               for (int bb = 0; bb < 3; ++bb) acc += rot[aa * 3 + bb] * is[bb] * rot[cc * 3 + bb];
               inv3[aa * 3 + cc] = acc;
             }
-          r.m[0] = inv3[0];
-          r.m[1] = inv3[4];
-          r.m[2] = inv3[8];
-          r.m[3] = inv3[1];
-          r.m[4] = inv3[2];
-          r.m[5] = inv3[5];
-          r.q0 = inv3[0] * rel0 + inv3[1] * rel1 + inv3[2] * rel2;
-          r.q1 = inv3[3] * rel0 + inv3[4] * rel1 + inv3[5] * rel2;
-          r.q2 = inv3[6] * rel0 + inv3[7] * rel1 + inv3[8] * rel2;
+          // camera space: M' = W inv3 W^T, q' = M' p_view (SplatRec comment)
+          double WI[9];  // W inv3
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+              WI[aa * 3 + cc] = W[aa * 3 + 0] * inv3[0 * 3 + cc] + W[aa * 3 + 1] * inv3[1 * 3 + cc] +
+                                W[aa * 3 + 2] * inv3[2 * 3 + cc];
+          double Mc[9];
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+              Mc[aa * 3 + cc] = WI[aa * 3 + 0] * W[cc * 3 + 0] + WI[aa * 3 + 1] * W[cc * 3 + 1] +
+                                WI[aa * 3 + 2] * W[cc * 3 + 2];
+          r.m[0] = Mc[0];
+          r.m[1] = Mc[4];
+          r.m[2] = Mc[8];
+          r.m[3] = Mc[1] + Mc[3];
+          r.m[4] = Mc[2] + Mc[6];
+          r.m[5] = Mc[5] + Mc[7];
+          r.q0 = Mc[0] * pv0 + Mc[1] * pv1 + Mc[2] * z;
+          r.q1 = Mc[3] * pv0 + Mc[4] * pv1 + Mc[5] * z;
+          r.q2 = Mc[6] * pv0 + Mc[7] * pv1 + Mc[8] * z;
 #if STP_SPLIT_SH
           // SH colour: K1b (k_shade), for the splats that reach a tile
           r.c0 = r.c1 = r.c2 = 0.f;
@@ -450,29 +465,15 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
             f.ca = r.ca;
             f.cb = r.cb;
             f.cc = r.cc;
-            double WI[9];  // W inv3
-#pragma unroll
-            for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-              for (int cc = 0; cc < 3; ++cc)
-                WI[aa * 3 + cc] = W[aa * 3 + 0] * inv3[0 * 3 + cc] + W[aa * 3 + 1] * inv3[1 * 3 + cc] +
-                                  W[aa * 3 + 2] * inv3[2 * 3 + cc];
-            double Mc[9];  // (W inv3) W^T
-#pragma unroll
-            for (int aa = 0; aa < 3; ++aa)
-#pragma unroll
-              for (int cc = 0; cc < 3; ++cc)
-                Mc[aa * 3 + cc] = WI[aa * 3 + 0] * W[cc * 3 + 0] + WI[aa * 3 + 1] * W[cc * 3 + 1] +
-                                  WI[aa * 3 + 2] * W[cc * 3 + 2];
-            f.m00 = Mc[0];
-            f.m11 = Mc[4];
-            f.m22 = Mc[8];
-            f.m01x2 = Mc[1] + Mc[3];
-            f.m02x2 = Mc[2] + Mc[6];
-            f.m12x2 = Mc[5] + Mc[7];
-            f.q0 = Mc[0] * pv0 + Mc[1] * pv1 + Mc[2] * z;
-            f.q1 = Mc[3] * pv0 + Mc[4] * pv1 + Mc[5] * z;
-            f.q2 = Mc[6] * pv0 + Mc[7] * pv1 + Mc[8] * z;
+            f.m00 = r.m[0];
+            f.m11 = r.m[1];
+            f.m22 = r.m[2];
+            f.m01x2 = r.m[3];
+            f.m02x2 = r.m[4];
+            f.m12x2 = r.m[5];
+            f.q0 = r.q0;
+            f.q1 = r.q1;
+            f.q2 = r.q2;
             f.op = opf;
             f.c0 = col[0];
             f.c1 = col[1];
@@ -558,10 +559,30 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     const double op = b.opacity[i];
     r.thr = (op > 0.0) ? log(op / cfg.eps) : -INFINITY;
     r.op = (float)op;
-    for (int k = 0; k < 6; ++k) r.m[k] = b.inv_cov3[6 * i + k];
-    r.q0 = b.inv_cov_center[3 * i];
-    r.q1 = b.inv_cov_center[3 * i + 1];
-    r.q2 = b.inv_cov_center[3 * i + 2];
+    {
+      // world inverse covariance / centre -> camera space (SplatRec comment)
+      const double* W = cam.R;
+      const double* m6 = b.inv_cov3 + 6 * i;
+      const double M[9] = {m6[0], m6[3], m6[4], m6[3], m6[1], m6[5], m6[4], m6[5], m6[2]};
+      double WM[9], Mc[9];
+      for (int aa = 0; aa < 3; ++aa)
+        for (int cc = 0; cc < 3; ++cc)
+          WM[aa * 3 + cc] = W[aa * 3] * M[cc] + W[aa * 3 + 1] * M[3 + cc] + W[aa * 3 + 2] * M[6 + cc];
+      for (int aa = 0; aa < 3; ++aa)
+        for (int cc = 0; cc < 3; ++cc)
+          Mc[aa * 3 + cc] =
+              WM[aa * 3] * W[cc * 3] + WM[aa * 3 + 1] * W[cc * 3 + 1] + WM[aa * 3 + 2] * W[cc * 3 + 2];
+      r.m[0] = Mc[0];
+      r.m[1] = Mc[4];
+      r.m[2] = Mc[8];
+      r.m[3] = Mc[1] + Mc[3];
+      r.m[4] = Mc[2] + Mc[6];
+      r.m[5] = Mc[5] + Mc[7];
+      const double* q = b.inv_cov_center + 3 * i;
+      r.q0 = W[0] * q[0] + W[1] * q[1] + W[2] * q[2];
+      r.q1 = W[3] * q[0] + W[4] * q[1] + W[5] * q[2];
+      r.q2 = W[6] * q[0] + W[7] * q[1] + W[8] * q[2];
+    }
     r.c0 = (float)b.color[3 * i];
     r.c1 = (float)b.color[3 * i + 1];
     r.c2 = (float)b.color[3 * i + 2];
@@ -573,32 +594,21 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     r.ry1 = (int16_t)y1;
     recs[i] = r;
     if (recs32) {
-      // camera space: M' = R M R^T, q' = R q
-      const double* W = cam.R;
-      const double M[9] = {r.m[0], r.m[3], r.m[4], r.m[3], r.m[1], r.m[5], r.m[4], r.m[5], r.m[2]};
-      double WM[9], Mc[9];
-      for (int aa = 0; aa < 3; ++aa)
-        for (int cc = 0; cc < 3; ++cc)
-          WM[aa * 3 + cc] = W[aa * 3] * M[cc] + W[aa * 3 + 1] * M[3 + cc] + W[aa * 3 + 2] * M[6 + cc];
-      for (int aa = 0; aa < 3; ++aa)
-        for (int cc = 0; cc < 3; ++cc)
-          Mc[aa * 3 + cc] =
-              WM[aa * 3] * W[cc * 3] + WM[aa * 3 + 1] * W[cc * 3 + 1] + WM[aa * 3 + 2] * W[cc * 3 + 2];
       SplatRec32 f;
       f.mx = r.mx;
       f.my = r.my;
       f.ca = r.ca;
       f.cb = r.cb;
       f.cc = r.cc;
-      f.m00 = Mc[0];
-      f.m11 = Mc[4];
-      f.m22 = Mc[8];
-      f.m01x2 = Mc[1] + Mc[3];
-      f.m02x2 = Mc[2] + Mc[6];
-      f.m12x2 = Mc[5] + Mc[7];
-      f.q0 = W[0] * r.q0 + W[1] * r.q1 + W[2] * r.q2;
-      f.q1 = W[3] * r.q0 + W[4] * r.q1 + W[5] * r.q2;
-      f.q2 = W[6] * r.q0 + W[7] * r.q1 + W[8] * r.q2;
+      f.m00 = r.m[0];
+      f.m11 = r.m[1];
+      f.m22 = r.m[2];
+      f.m01x2 = r.m[3];
+      f.m02x2 = r.m[4];
+      f.m12x2 = r.m[5];
+      f.q0 = r.q0;
+      f.q1 = r.q1;
+      f.q2 = r.q2;
       f.op = r.op;
       f.c0 = r.c0;
       f.c1 = r.c1;
@@ -760,9 +770,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const uint32_t base = v ? s_pos[wbase + owner] : 0;
     __syncwarp();
     if (keep) {
-      double d0, d1, d2;
-      ray_dir(cam, ptx, pty, d0, d1, d2);  // rasterizer.py:349-350
-      const double depth = blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+      const double depth = key_rec_at(cam, r, ptx, pty);  // rasterizer.py:346-350
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
         const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |

@@ -79,7 +79,8 @@ struct Head {
 
 struct Pixel {
   double px, py;
-  double d0, d1, d2;  // unit pixel ray (rasterizer.py:405)
+  double u, w, vn;    // camera ray (u, w, 1) of the pixel centre, |(u, w, 1)|
+                      // (rasterizer.py:405 in the camera-space form)
   double T;           // transmittance (float64: the termination test)
   float C0, C1, C2, D;
   int rc;             // blend records written
@@ -141,14 +142,12 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
   const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
   const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
   const double q2 = __ldg(&r->q2);
-  // t_opt = (d.q) / (f(d).m6), ray_features (rasterizer.py:406) folded in.
+  // t_opt on the pixel ray (camera-space form of rasterizer.py:405-406).
   // Evaluated before the alpha test: the exp chain and this chain are
   // independent, so the two float64 dependency chains overlap (alpha < eps
   // after the early-out above is rare).
-  const double num = P.d0 * q01.x + P.d1 * q01.y + P.d2 * q2;
-  const double den = P.d0 * (P.d0 * m01.x + 2.0 * (P.d1 * m23.y + P.d2 * m45.x)) +
-                     P.d1 * (P.d1 * m01.y + 2.0 * P.d2 * m45.y) + P.d2 * P.d2 * m23.x;
-  t = fdiv(num, den);
+  const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
+  t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
   al = (double)op * exp_neg(pw, tab);
   if (al < A.cfg.eps) return false;
   if (al > A.cfg.cap) al = A.cfg.cap;
@@ -383,7 +382,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
       P.px = (double)gx + 0.5;
       P.py = (double)gy + 0.5;
-      ray_dir(A.cam, P.px, P.py, P.d0, P.d1, P.d2);
+      cam_ray(A.cam, P.px, P.py, P.u, P.w, P.vn);
       P.T = in_img ? 1.0 : 0.0;
       P.C0 = P.C1 = P.C2 = P.D = 0.f;
       P.rc = 0;
@@ -439,9 +438,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
             const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
             max_point(mxy.x, mxy.y, ab.x, ab.y, cc, inv.x, inv.y, r2x, r2y, 2.0, 0.5, ptx, pty);
           }
-          double d0, d1, d2;
-          ray_dir(A.cam, ptx, pty, d0, d1, d2);
-          const double dv = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+          const double dv = key_rec_at(A.cam, *r, ptx, pty);
           if (u) {
             gd[1] = dv;
             gi[1] = sid;
@@ -634,9 +631,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
                       pty);
             if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
                            A.cfg.eps)) {
-              double d0, d1, d2;
-              ray_dir(A.cam, ptx, pty, d0, d1, d2);
-              const double dv = blend_depth(r->m, r->q0, r->q1, r->q2, d0, d1, d2);
+              const double dv = key_rec_at(A.cam, *r, ptx, pty);
               if (s) {
                 dB = dv;
                 iB = sid;

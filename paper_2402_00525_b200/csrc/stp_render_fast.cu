@@ -116,9 +116,7 @@ __device__ __noinline__ double exact_key(const SplatRec* __restrict__ recs,
   if (kind == 0)
     max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, x, y, (double)w, 1.0 / (double)w,
               px, py);
-  double d0, d1, d2;
-  ray_dir(*cam, px, py, d0, d1, d2);
-  return blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+  return key_rec_at(*cam, r, px, py);
 }
 
 // (d, rank) order of the reference with float64 keys; empty slots last

@@ -187,9 +187,7 @@ __device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ rec
   double ptx, pty;
   max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
             (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
-  double d0, d1, d2;
-  ray_dir(cam, ptx, pty, d0, d1, d2);
-  return blend_depth(r.m, r.q0, r.q1, r.q2, d0, d1, d2);
+  return key_rec_at(cam, r, ptx, pty);
 }
 
 constexpr int kTieLocal = 32;
