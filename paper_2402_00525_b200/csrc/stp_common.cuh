@@ -208,6 +208,24 @@ __device__ __forceinline__ double exp_neg(double p, const double* tab) {
 }
 
 
+// exp_neg without the p > 700 branch (the caller clamps p)
+__device__ __forceinline__ double exp_neg_nb(double p, const double* tab) {
+  const double kd = rint(p * c_exp_k[0]);
+  const int k = (int)kd;
+  double r = fma(-kd, c_exp_k[1], p);
+  r = fma(-kd, c_exp_k[2], r);
+  double e = c_exp_k[3];
+  e = fma(e, -r, c_exp_k[4]);
+  e = fma(e, -r, c_exp_k[5]);
+  e = fma(e, -r, c_exp_k[6]);
+  e = fma(e, -r, c_exp_k[7]);
+  e = fma(e, -r, 1.0);
+  e = fma(e, -r, 1.0);
+  const int j = k & 63, ex = k >> 6;
+  const double scale = __hiloint2double((1023 - ex) << 20, 0);
+  return tab[j] * e * scale;
+}
+
 // exponent of gauss2d (tile_culling.py:96)
 __device__ __forceinline__ double gpower(double a, double b, double c, double dx, double dy) {
   return 0.5 * (a * dx * dx + c * dy * dy) + b * dx * dy;

@@ -50,14 +50,19 @@ constexpr unsigned kNoId = 0xffffffffu;
     if (lane == 0) atomicAdd(A.counters + C_PROF + (slot), (unsigned long long)(_pn - _pt)); \
     _pt = _pn;                                                                      \
   } while (0)
+#else
+#define PROF_T0() (void)0
+#define PROF_ADD(slot) (void)0
+#endif
+// Optional work counters (-DSTP_WORK_STATS), separate from the phase timer
+// because their ballots and atomics perturb the timing.
+#ifdef STP_WORK_STATS
 #define STAT_ADD(slot, pred)                                                        \
   do {                                                                              \
     const unsigned _b = __ballot_sync(kFull, (pred));                               \
     if (lane == 0 && _b) atomicAdd(A.counters + C_STAT + (slot), (unsigned long long)__popc(_b)); \
   } while (0)
 #else
-#define PROF_T0() (void)0
-#define PROF_ADD(slot) (void)0
 #define STAT_ADD(slot, pred) (void)0
 #endif
 
@@ -152,6 +157,32 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
   if (al < A.cfg.eps) return false;
   if (al > A.cfg.cap) al = A.cfg.cap;
   return true;
+}
+
+// Branch-free variant: everything computed, the decision returned, so two
+// evaluations placed side by side form one basic block whose float64 chains
+// the scheduler interleaves.
+__device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A, uint32_t id,
+                                             const double* tab, double& t, double& al) {
+  const SplatRec* r = A.recs + id;
+  const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
+  const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
+  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+  const float op = __ldg(&r->op);
+  const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
+  const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
+  const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
+  const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
+  const double q2 = __ldg(&r->q2);
+  const double dx = P.px - mxy.x, dy = P.py - mxy.y;
+  const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
+  const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
+  t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
+  const double pc = fmin(pw, 700.0);
+  al = (double)op * exp_neg_nb(pc, tab);
+  const bool pass = (pw <= ct.y + 1e-9) & (al >= A.cfg.eps);
+  al = fmin(al, A.cfg.cap);
+  return pass;
 }
 
 // insort into the pixel queue; on overflow blend the minimum
@@ -570,17 +601,26 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           const int pend = ps ? pb : pa;
           const int base = ps ? rh1 : rh0;
           const uint32_t* ring = subq(ps).ring(pq, R);
-          for (int e = 0; e < rounds; ++e) {
+          // two emitted entries per step: their evaluations are independent
+          // (one basic block, interleaved chains); the head insertions stay
+          // in order.  Terminated pixels skip the insertion (their blends are
+          // no-ops, hierarchy.py:82-84).
+          for (int e = 0; e < rounds; e += 2) {
+            const bool v0 = e < pend && P.T >= term;
+            const bool v1 = e + 1 < min(pend, rounds) && P.T >= term;
             STAT_ADD(4, e < pend);
-            STAT_ADD(5, e < pend && P.T >= term);
-            bool pass = false;
-            if (e < pend && P.T >= term) {
-              const uint32_t id = ring[(base + e) & (R - 1)];
-              double t, al;
-              pass = emit_eval(P, A, id, s_tab, t, al);
-              if (pass) head_push<QH, EXACT>(P, H, A, qh_rt, t, al, id);
+            STAT_ADD(5, v0);
+            const uint32_t id0 = ring[(base + e) & (R - 1)];
+            const uint32_t id1 = ring[(base + e + 1) & (R - 1)];
+            double t0 = 0.0, a0 = 0.0, t1 = 0.0, a1 = 0.0;
+            bool p0 = false, p1 = false;
+            if (v0 | v1) {
+              p0 = emit_eval_bf(P, A, v0 ? id0 : id1, s_tab, t0, a0) & v0;
+              p1 = emit_eval_bf(P, A, v1 ? id1 : id0, s_tab, t1, a1) & v1;
             }
-            STAT_ADD(6, pass);
+            if (p0) head_push<QH, EXACT>(P, H, A, qh_rt, t0, a0, id0);
+            if (p1 && P.T >= term) head_push<QH, EXACT>(P, H, A, qh_rt, t1, a1, id1);
+            STAT_ADD(6, p0);
           }
         }
         rh0 += min(rounds, pa);
