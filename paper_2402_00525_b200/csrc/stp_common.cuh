@@ -21,20 +21,22 @@ constexpr int kTile = 16;
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 
-// Projected splat, one per kept Gaussian, indexed by Gaussian id.  160 B =
-// 10 x 16 B: everything K3 (duplicate) and K6 (render) gather per entry.
+// Projected splat, one per kept Gaussian, indexed by Gaussian id; 160 B.
+// The first 128-B line holds everything the pixel stage reads for one
+// emitted entry (alpha, t_opt, colour), so each evaluation touches one line;
+// the second holds the culling-only fields.
 struct __align__(16) SplatRec {
   double mx, my;        // mean2d (pixels)                                   0
-  double ca, cb, cc;    // conic (a, b, c)                                   16
-  double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr  40
-  double m[6];          // camera-space M' = R inv_cov3 R^T as                48
+  double ca, cb;        // conic a, b                                        16
+  double cc, q2;        // conic c; q'_z                                     32
+  double m[6];          // camera-space M' = R inv_cov3 R^T as               48
                         // (m00, m11, m22, 2 m01, 2 m02, 2 m12)
   double q0, q1;        // q' = M' p_view (= R inv_cov3 (mean - origin)), x y 96
   float op;             // opacity                                           112
   float c0, c1, c2;     // SH colour (lower-clamped at 0)
-  double q2;            // q', z                                             128
-  int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)
-  double inv_a, inv_c;  // 1/a, 1/c for the Alg. 1 edge searches            144
+  double inv_a, inv_c;  // 1/a, 1/c for the Alg. 1 edge searches            128
+  double thr;           // log(opacity / eps): alpha >= eps <=> power <= thr  144
+  int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)  152
 };
 static_assert(sizeof(SplatRec) == 160, "SplatRec must be 160 B");
 

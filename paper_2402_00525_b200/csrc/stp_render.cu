@@ -99,6 +99,7 @@ struct RenderArgs {
   DevCam cam;
   DevCfg cfg;
   int gw, n_items;
+  float log_eps;
   StpOutputs out;
   unsigned long long* counters;
   const uint32_t* list;   // list mode: (tile*8 + pair) items handed over by the fast path
@@ -137,16 +138,19 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
   const SplatRec* r = A.recs + id;
   const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
   const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));  // cc q2
   const double dx = P.px - mxy.x, dy = P.py - mxy.y;
   const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
-  if (pw > ct.y + 1e-9) return false;  // alpha < eps, away from the boundary
   const float op = __ldg(&r->op);
+  // early out when alpha < eps beyond doubt (MUFU log; the decision is the
+  // float64 test below)
+  const float thr = __logf(op) - A.log_eps;
+  if ((float)pw > thr + fmaf(1e-5f, fabsf(thr), 1e-5f)) return false;
   const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
   const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
   const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
   const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
-  const double q2 = __ldg(&r->q2);
+  const double q2 = ct.y;
   // t_opt on the pixel ray (camera-space form of rasterizer.py:405-406).
   // Evaluated before the alpha test: the exp chain and this chain are
   // independent, so the two float64 dependency chains overlap (alpha < eps
@@ -167,20 +171,20 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
   const SplatRec* r = A.recs + id;
   const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
   const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));  // cc q2
   const float op = __ldg(&r->op);
   const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
   const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
   const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
   const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
-  const double q2 = __ldg(&r->q2);
+  const double q2 = ct.y;
   const double dx = P.px - mxy.x, dy = P.py - mxy.y;
   const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
   const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
   t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
   const double pc = fmin(pw, 700.0);
   al = (double)op * exp_neg_nb(pc, tab);
-  const bool pass = (pw <= ct.y + 1e-9) & (al >= A.cfg.eps);
+  const bool pass = al >= A.cfg.eps;  // hierarchy.py:99-101
   al = fmin(al, A.cfg.cap);
   return pass;
 }
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           const SplatRec* r = A.recs + sid;
           const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
           const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-          const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+          const double2 ct = make_double2(__ldg(&r->cc), __ldg(&r->thr));
           const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
           const float op = __ldg(&r->op);
 #pragma unroll
@@ -810,6 +814,7 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   RenderArgs A;
   A.list = f.exact_only ? nullptr : f.fb_items;
   A.recs = f.recs;
+  A.log_eps = (float)log(f.cfg.eps);
   A.vals = f.vals;
   A.ranges = f.ranges;
   A.cam = f.cam;

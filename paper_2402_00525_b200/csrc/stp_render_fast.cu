@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kFThreads, STP_FAST_MINB) k_render_fast(FastAr
           const SplatRec* r = A.recs + sid;
           const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
           const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-          const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));
+          const double2 ct = make_double2(__ldg(&r->cc), __ldg(&r->thr));
           const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
           const float op = __ldg(&r->op);
 #pragma unroll 1
