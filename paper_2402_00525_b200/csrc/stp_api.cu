@@ -10,7 +10,7 @@ size_t render_smem_bytes(int qt, int qm);
 
 namespace {
 
-constexpr int kSortTile = 4096;
+constexpr int kSortTile = kSortPartition;
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }

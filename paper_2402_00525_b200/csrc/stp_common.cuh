@@ -18,6 +18,10 @@
 namespace stp {
 
 constexpr int kTile = 16;
+#ifndef STP_SORT_ITEMS
+#define STP_SORT_ITEMS 12
+#endif
+constexpr int kSortPartition = 256 * STP_SORT_ITEMS;  // K4 entries per partition (256 threads)
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 

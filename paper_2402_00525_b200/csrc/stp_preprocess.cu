@@ -261,32 +261,20 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
     if (cnt) masks[i] = s_mask[threadIdx.x];
     if (state) state[i] = (uint8_t)reason;
   }
-  // projection stats: warp ballots into shared counters, one barrier
-  __shared__ int s_st[4];
-  if (threadIdx.x < 4) s_st[threadIdx.x] = 0;
-  __syncthreads();
+  // projection stats: per-warp ballots added to per-SM slots (no block
+  // barrier: warps leave the load-balanced count loop at different times)
   {
     const unsigned b1 = __ballot_sync(kFull, reason == 1), b2 = __ballot_sync(kFull, reason == 2);
     const unsigned b3 = __ballot_sync(kFull, reason == 3), b0 = __ballot_sync(kFull, reason == 0);
     if (lane == 0) {
-      if (b1) atomicAdd(&s_st[0], __popc(b1));
-      if (b2) atomicAdd(&s_st[1], __popc(b2));
-      if (b3) atomicAdd(&s_st[2], __popc(b3));
-      if (b0) atomicAdd(&s_st[3], __popc(b0));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* ps = counters + C_PSTAT + (smid & 255) * 4;
+      if (b1) atomicAdd(ps + 0, (unsigned long long)__popc(b1));
+      if (b2) atomicAdd(ps + 1, (unsigned long long)__popc(b2));
+      if (b3) atomicAdd(ps + 2, (unsigned long long)__popc(b3));
+      if (b0) atomicAdd(ps + 3, (unsigned long long)__popc(b0));
     }
-  }
-  __syncthreads();
-  const int n_behind = s_st[0], n_guard = s_st[1], n_degen = s_st[2], n_kept = s_st[3];
-  if (threadIdx.x == 0) {
-    // per-SM slots: one global counter per stat would take ~12k serialised
-    // atomics per frame
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    unsigned long long* ps = counters + C_PSTAT + (smid & 255) * 4;
-    if (n_behind) atomicAdd(ps + 0, (unsigned long long)n_behind);
-    if (n_guard) atomicAdd(ps + 1, (unsigned long long)n_guard);
-    if (n_degen) atomicAdd(ps + 2, (unsigned long long)n_degen);
-    if (n_kept) atomicAdd(ps + 3, (unsigned long long)n_kept);
   }
 }
 
@@ -326,6 +314,15 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
       if (!in_guard) {
         reason = 2;  // :370-373
       } else {
+#if !STP_SPLIT_SH
+        // the SH row (192 B at degree 3) is only needed at the end: start
+        // pulling it into L2 now, under the covariance math
+        {
+          const char* shp = reinterpret_cast<const char*>(sc.sh + i * sc.sh_coeffs * 3);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(shp));
+          if (sc.sh_coeffs > 5) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + 128));
+        }
+#endif
         // _quats_to_matrices (gaussian_math.py:102-115)
         const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
         const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;

@@ -17,8 +17,8 @@ namespace stp {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 items per partition
+constexpr int kSortItems = STP_SORT_ITEMS;
+constexpr int kSortTile = kSortPartition;  // kSortThreads * kSortItems items per partition
 constexpr int kRadix = 256;
 
 // look-back word: [epoch:32 | flag:2 | count:30]
