@@ -177,12 +177,13 @@ __device__ __forceinline__ void coarse_rect(double px, double py, double radius,
                                             int& x0, int& x1, int& y0, int& y1) {
   const double ts = (double)kTile;
   const double lo = -2.0;
-  const double fx0 = fmin(fmax(floor((px - radius) / ts), lo), (double)gw + 1);
-  const double fy0 = fmin(fmax(floor((py - radius) / ts), lo), (double)gh + 1);
+  const double its = 1.0 / ts;  // exact (power of two): x / ts == x * its
+  const double fx0 = fmin(fmax(floor((px - radius) * its), lo), (double)gw + 1);
+  const double fy0 = fmin(fmax(floor((py - radius) * its), lo), (double)gh + 1);
   const double fx1 =
-      fmin(fmax(fmax(ceil((px + radius) / ts) - 1.0, floor(px / ts)), lo), (double)gw + 1);
+      fmin(fmax(fmax(ceil((px + radius) * its) - 1.0, floor(px * its)), lo), (double)gw + 1);
   const double fy1 =
-      fmin(fmax(fmax(ceil((py + radius) / ts) - 1.0, floor(py / ts)), lo), (double)gh + 1);
+      fmin(fmax(fmax(ceil((py + radius) * its) - 1.0, floor(py * its)), lo), (double)gh + 1);
   x0 = max((int)fx0, 0);
   y0 = max((int)fy0, 0);
   x1 = min((int)fx1, gw - 1);
@@ -307,8 +308,10 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     if (!(z > cfg.near_plane)) {
       reason = 1;  // :364
     } else {
-      const double px = cam.fx * pv0 / z + cam.cx;  // :368-369
-      const double py = cam.fy * pv1 / z + cam.cy;
+      // divisions below: fdiv (MUFU + Newton, <= 1 ulp) in the reference's
+      // operation order, instead of the long IEEE division sequence
+      const double px = fdiv(cam.fx * pv0, z) + cam.cx;  // :368-369
+      const double py = fdiv(cam.fy * pv1, z) + cam.cy;
       const bool in_guard = (fabs(px - cam.cx) <= cfg.guard * cam.W / 2.0) &&
                             (fabs(py - cam.cy) <= cfg.guard * cam.H / 2.0);
       if (!in_guard) {
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
         const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
         const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;
         const double qn = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
-        const double w = qw0 / qn, x = qx0 / qn, y = qy0 / qn, zq = qz0 / qn;
+        const double w = fdiv(qw0, qn), x = fdiv(qx0, qn), y = fdiv(qy0, qn), zq = fdiv(qz0, qn);
         double rot[9] = {1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y),
                          2 * (x * y + w * zq),      1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x),
                          2 * (x * zq - w * y),      2 * (y * zq + w * x),  1 - 2 * (x * x + y * y)};
@@ -346,8 +349,9 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
             cov3[aa * 3 + cc] = acc;
           }
         // J and M = J W (gaussian_math.py:378-383)
-        const double J[6] = {cam.fx / z, 0.0, -cam.fx * pv0 / (z * z),
-                             0.0, cam.fy / z, -cam.fy * pv1 / (z * z)};
+        const double zz = z * z;
+        const double J[6] = {fdiv(cam.fx, z), 0.0, -fdiv(cam.fx * pv0, zz),
+                             0.0, fdiv(cam.fy, z), -fdiv(cam.fy * pv1, zz)};
         double M[6];
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -377,25 +381,26 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           SplatRec r;
           r.mx = px;
           r.my = py;
-          r.ca = c / det;  // conic (:397)
-          r.cb = -b / det;
-          r.cc = a / det;
-          r.inv_a = 1.0 / r.ca;
-          r.inv_c = 1.0 / r.cc;
+          r.ca = fdiv(c, det);  // conic (:397)
+          r.cb = -fdiv(b, det);
+          r.cc = fdiv(a, det);
+          r.inv_a = fdiv(1.0, r.ca);
+          r.inv_c = fdiv(1.0, r.cc);
           // opacity-aware radius (:399-404)
           const float opf = __ldg(sc.opacity + i);
           const double op = opf;
           const double mid = 0.5 * (a + c);
           const double lam_max = mid + sqrt(fmax(mid * mid - a * c + b * b, 0.0));
-          const double cutoff = (op > cfg.eps) ? sqrt(2.0 * log(op / cfg.eps)) : 0.0;
+          const double lg = log(op / cfg.eps);
+          const double cutoff = (op > cfg.eps) ? sqrt(2.0 * lg) : 0.0;
           const double radius = cutoff * sqrt(lam_max);
-          r.thr = (op > 0.0) ? log(op / cfg.eps) : -INFINITY;
+          r.thr = (op > 0.0) ? lg : -INFINITY;
           r.op = opf;
           // packed clamped inverse covariance (:406-412) and its centre (:413)
           double is[3];
-          is[0] = fmin(1.0 / s0, cfg.clamp);
-          is[1] = fmin(1.0 / s1, cfg.clamp);
-          is[2] = fmin(1.0 / s2, cfg.clamp);
+          is[0] = fmin(fdiv(1.0, s0), cfg.clamp);
+          is[1] = fmin(fdiv(1.0, s1), cfg.clamp);
+          is[2] = fmin(fdiv(1.0, s2), cfg.clamp);
           is[0] *= is[0];
           is[1] *= is[1];
           is[2] *= is[2];
