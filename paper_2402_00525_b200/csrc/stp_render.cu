@@ -605,26 +605,32 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           const int pend = ps ? pb : pa;
           const int base = ps ? rh1 : rh0;
           const uint32_t* ring = subq(ps).ring(pq, R);
-          // two emitted entries per step: their evaluations are independent
-          // (one basic block, interleaved chains); the head insertions stay
-          // in order.  Terminated pixels skip the insertion (their blends are
+          // STP_PIX_UNROLL emitted entries per step: their evaluations are
+          // independent (one basic block, interleaved chains); the head
+          // insertions stay in order.  Terminated pixels skip the insertion (their blends are
           // no-ops, hierarchy.py:82-84).
-          for (int e = 0; e < rounds; e += 2) {
-            const bool v0 = e < pend && P.T >= term;
-            const bool v1 = e + 1 < min(pend, rounds) && P.T >= term;
+#ifndef STP_PIX_UNROLL
+#define STP_PIX_UNROLL 2
+#endif
+          for (int e = 0; e < rounds; e += STP_PIX_UNROLL) {
+            const int lim = min(pend, rounds);
+            const bool live = P.T >= term;
+            uint32_t ids[STP_PIX_UNROLL];
+            double ts[STP_PIX_UNROLL], as[STP_PIX_UNROLL];
+            bool ps[STP_PIX_UNROLL];
             STAT_ADD(4, e < pend);
-            STAT_ADD(5, v0);
-            const uint32_t id0 = ring[(base + e) & (R - 1)];
-            const uint32_t id1 = ring[(base + e + 1) & (R - 1)];
-            double t0 = 0.0, a0 = 0.0, t1 = 0.0, a1 = 0.0;
-            bool p0 = false, p1 = false;
-            if (v0 | v1) {
-              p0 = emit_eval_bf(P, A, v0 ? id0 : id1, s_tab, t0, a0) & v0;
-              p1 = emit_eval_bf(P, A, v1 ? id1 : id0, s_tab, t1, a1) & v1;
+            STAT_ADD(5, e < pend && live);
+            if (e < lim && live) {
+#pragma unroll
+              for (int k = 0; k < STP_PIX_UNROLL; ++k) {
+                const bool vk = e + k < lim;
+                ids[k] = ring[(base + e + (vk ? k : 0)) & (R - 1)];
+                ps[k] = emit_eval_bf(P, A, ids[k], s_tab, ts[k], as[k]) & vk;
+              }
+#pragma unroll
+              for (int k = 0; k < STP_PIX_UNROLL; ++k)
+                if (ps[k] && P.T >= term) head_push<QH, EXACT>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
             }
-            if (p0) head_push<QH, EXACT>(P, H, A, qh_rt, t0, a0, id0);
-            if (p1 && P.T >= term) head_push<QH, EXACT>(P, H, A, qh_rt, t1, a1, id1);
-            STAT_ADD(6, p0);
           }
         }
         rh0 += min(rounds, pa);
