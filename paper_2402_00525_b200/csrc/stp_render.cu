@@ -281,6 +281,37 @@ __device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1,
   }
 }
 
+// Bitonic sort of (d, id) within each 16-lane half of the warp (L = lane &
+// 15; both halves sorted ascending at once).
+__device__ __forceinline__ void half_sort16(double& d, uint32_t& id, int L) {
+#pragma unroll 1
+  for (int k = 2; k <= 16; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double od = shfl_xor_d(d, j);
+      const uint32_t oi = __shfl_xor_sync(kFull, id, j);
+      const bool want_min = (((L & j) == 0) == ((L & k) == 0));
+      const bool take = want_min == lt(od, oi, d, id);
+      d = take ? od : d;
+      id = take ? oi : id;
+    }
+  }
+}
+
+// position of the k-th (0-based) set bit of m (k < popc(m))
+__device__ __forceinline__ int select_bit32(unsigned m, int k) {
+  int pos = 0;
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    const int c = __popc(m & ((1u << s) - 1u));
+    const bool up = k >= c;
+    k -= up ? c : 0;
+    m = up ? (m >> s) : m;
+    pos += up ? s : 0;
+  }
+  return pos;
+}
+
 // number of (d,id) in sorted a[0..n) strictly below (x, xi)
 __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai, int n, double x,
                                            uint32_t xi) {
@@ -703,27 +734,69 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
         STAT_ADD(2, lane == 0);
         STAT_ADD(3, lane == 0 && nkA + nkB > 0);
         if (nkA + nkB == 0) continue;
-        warp_sort2(dA, iA, dB, iB, lane);
+        // Sort the kept candidates by (d4, rank).  Common case (<= 16 kept per
+        // sub-tile): compact each sub-tile's kept entries into one half-warp
+        // and run ONE 16-wide bitonic network over both halves at once (10
+        // stages, one array) instead of two 32-wide networks (15 stages, two
+        // arrays).  Lane h*16+L then holds element L of sub-tile h.
+        double dS0, dS1;
+        uint32_t iS0, iS1;
+        int xS0, xS1;
+        bool vS0, vS1;
+        if (nkA <= 16 && nkB <= 16) {
+          const unsigned bA = __ballot_sync(kFull, iA != kNoId);
+          const unsigned bB = __ballot_sync(kFull, iB != kNoId);
+          const int h = lane >> 4, L = lane & 15;
+          const int nk = h ? nkB : nkA;
+          const int src = select_bit32(h ? bB : bA, L < nk ? L : 0);
+          const double sdA = shfl_d(dA, src), sdB = shfl_d(dB, src);
+          const uint32_t siA = __shfl_sync(kFull, iA, src), siB = __shfl_sync(kFull, iB, src);
+          double d = h ? sdB : sdA;
+          uint32_t id = h ? siB : siA;
+          if (L >= nk) {
+            d = INFINITY;
+            id = kNoId;
+          }
+          half_sort16(d, id, L);
+          dS0 = dS1 = d;
+          iS0 = iS1 = id;
+          xS0 = xS1 = L;
+          vS0 = (h == 0) && L < nkA;
+          vS1 = (h == 1) && L < nkB;
+        } else {
+          warp_sort2(dA, iA, dB, iB, lane);
+          dS0 = dA;
+          dS1 = dB;
+          iS0 = iA;
+          iS1 = iB;
+          xS0 = xS1 = lane;
+          vS0 = lane < nkA;
+          vS1 = lane < nkB;
+        }
         // ---- merge each sorted batch into its tail (heap_merge, :201)
 #pragma unroll 1
         for (int s = 0; s < 2; ++s) {
           const int nks = s ? nkB : nkA;
           if (nks == 0) continue;
-          const double ds = s ? dB : dA;
-          const uint32_t is = s ? iB : iA;
+          const double ds = s ? dS1 : dS0;
+          const uint32_t is = s ? iS1 : iS0;
+          const int xs = s ? xS1 : xS0;
+          const bool vs = s ? vS1 : vS0;
           const SubQ Q = subq(s);
           const int cur = s ? cur1 : cur0, th = s ? th1 : th0, nt = s ? nt1 : nt0;
-          Q.bd()[lane] = ds;
-          Q.bi()[lane] = is;
+          if (vs) {
+            Q.bd()[xs] = ds;
+            Q.bi()[xs] = is;
+          }
           __syncwarp();
           const double* td = Q.td(cur) + th;
           const uint32_t* ti = Q.ti(cur) + th;
           double* od = Q.td(cur ^ 1);
           uint32_t* oi = Q.ti(cur ^ 1);
-          if (lane < nks) {
+          if (vs) {
             const int rk = count_below(td, ti, nt, ds, is);
-            od[lane + rk] = ds;
-            oi[lane + rk] = is;
+            od[xs + rk] = ds;
+            oi[xs + rk] = is;
           }
           for (int t = lane; t < nt; t += 32) {
             const int rk = count_below(Q.bd(), Q.bi(), nks, td[t], ti[t]);
