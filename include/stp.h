@@ -138,7 +138,7 @@ typedef struct {
 
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
-  size_t recs, recs32, fb_items, camera, masks, tile_cnt, tile_cur, state, counts, offsets, keys0, keys1, vals, ranges,
+  size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
       counters, hist, lookback, scan_scratch, total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;

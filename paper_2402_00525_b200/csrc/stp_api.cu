@@ -49,7 +49,7 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.entry_capacity = ecap;
   L.partitions = (int32_t)((ecap + kSortTile - 1) / kSortTile);
   L.splat_record_bytes = (int32_t)sizeof(SplatRec);
-  L.final_buffer = 0;  // K4 sorts the tile buckets in place
+  L.final_buffer = L.sort_passes & 1;
   const int64_t nb = (n + kSortTile - 1) / kSortTile;
   size_t o = 0;
   L.counters = o;     o = align_up(o + C_COUNT * 8);
@@ -61,8 +61,6 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.fb_items = o;     o = align_up(o + (size_t)L.n_tiles * 8 * 4);
   L.camera = o;       o = align_up(o + sizeof(DevCam));
   L.masks = o;        o = align_up(o + (size_t)n * 8);
-  L.tile_cnt = o;     o = align_up(o + (size_t)L.n_tiles * 4);
-  L.tile_cur = o;     o = align_up(o + (size_t)L.n_tiles * 4);
   L.state = o;        o = align_up(o + (size_t)n);
   L.counts = o;       o = align_up(o + (size_t)n * 4);
   L.offsets = o;      o = align_up(o + (size_t)n * 4);
@@ -130,8 +128,6 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.fb_items = reinterpret_cast<uint32_t*>(b + L.fb_items);
   f.camp = reinterpret_cast<DevCam*>(b + L.camera);
   f.masks = reinterpret_cast<uint64_t*>(b + L.masks);
-  f.tile_cnt = reinterpret_cast<uint32_t*>(b + L.tile_cnt);
-  f.tile_cur = reinterpret_cast<uint32_t*>(b + L.tile_cur);
   f.exact_only = (cfg->flags & STP_FLAG_FAST32) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
@@ -205,10 +201,10 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   if (batch) launch_ingest(f, *batch, s);
   else launch_preprocess(f, *sc, s);
   if (ev) cudaEventRecord(ev[1], s);
-  launch_tile_scan(f, s);
+  launch_scan(f, s);
   launch_duplicate(f, s);
   if (ev) cudaEventRecord(ev[2], s);
-  const int buf = launch_tile_sort(f, s);
+  const int buf = launch_sort(f, s);
   launch_ranges(f, buf, s);
   if (ev) cudaEventRecord(ev[3], s);
   launch_render(f, buf, o, s);

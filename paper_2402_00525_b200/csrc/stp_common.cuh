@@ -96,7 +96,6 @@ enum Counter {
   C_FB = 41,        // render: items handed to the exact (fp64) pass
   C_FBWORK = 42,    // render: exact-pass work counter
   C_RESOLVE = 43,   // (unused: per-SM slots at C_RES)
-  C_TSORT = 45,     // K4: tile-sort work counter
   C_STAT = 48,      // 8 work counters (STP_PHASE_PROF builds)
   C_SM = 64,        // render: per-SM sub-tile counters [256]
   C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
@@ -362,8 +361,6 @@ struct Frame {
   SplatRec* recs;
   SplatRec32* recs32;
   uint64_t* masks;        // per Gaussian: surviving tiles of a <= 64-tile coarse rect
-  uint32_t* tile_cnt;     // per tile: surviving entries (K1), then
-  uint32_t* tile_cur;     //   bucket cursors (K2 -> K3)
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;
@@ -392,8 +389,6 @@ void launch_init(const Frame& f, cudaStream_t s);
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s);
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s);
 void launch_scan(const Frame& f, cudaStream_t s);
-void launch_tile_scan(const Frame& f, cudaStream_t s);
-int launch_tile_sort(const Frame& f, cudaStream_t s);
 void launch_duplicate(const Frame& f, cudaStream_t s);
 int launch_sort(const Frame& f, cudaStream_t s);  // returns the buffer holding the result
 void launch_ranges(const Frame& f, int buf, cudaStream_t s);

@@ -35,7 +35,7 @@ __constant__ double c_SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.457
 // K0: zero the per-frame counters / histograms / tile ranges, bump the epoch
 // that tags the sort's look-back words (so they never need clearing).
 __global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n, uint2* ranges,
-                       int n_tiles, DevCam cam, DevCam* camp, uint32_t* tile_cnt) {
+                       int n_tiles, DevCam cam, DevCam* camp) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
   if (tid == 0) {
@@ -45,10 +45,7 @@ __global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n,
   for (int i = tid; i < C_COUNT; i += stride)
     if (i != C_EPOCH) counters[i] = 0;
   for (int i = tid; i < hist_n; i += stride) hist[i] = 0;
-  for (int i = tid; i < n_tiles; i += stride) {
-    ranges[i] = make_uint2(0, 0);
-    tile_cnt[i] = 0;
-  }
+  for (int i = tid; i < n_tiles; i += stride) ranges[i] = make_uint2(0, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -208,9 +205,7 @@ __device__ __forceinline__ void coarse_rect(double px, double py, double radius,
 // (masks, for K3) and the projection stats.  Called by K1 and the SplatBatch
 // ingest kernel with reason 0 (kept) .. 4 (out of range).
 __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64_t i, bool valid,
-                                            const DevCfg& cfg, int gw,
-                                            uint32_t* __restrict__ tile_cnt,
-                                            uint64_t* __restrict__ masks,
+                                            const DevCfg& cfg, uint64_t* __restrict__ masks,
                                             uint32_t* __restrict__ counts,
                                             uint8_t* __restrict__ state,
                                             unsigned long long* __restrict__ counters) {
@@ -241,19 +236,12 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
   const int wbase = threadIdx.x & ~31;
   warp_expand(area, lane, [&](bool v, int owner, int local) {
     bool keep = false;
-    int tile = 0;
     if (v) {
       const StagedGeo& o = s_geo[wbase + owner];
       const int tx = o.rx0 + local % o.wx, ty = o.ry0 + local / o.wx;
       double px, py;
       keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
                                           cfg.eps, tx, ty, px, py);
-      tile = ty * gw + tx;
-    }
-    // per-tile entry counts (the K4 buckets), aggregated over the round
-    {
-      const unsigned tp = __match_any_sync(kFull, keep ? tile : -1 - lane);
-      if (keep && lane == __ffs(tp) - 1) atomicAdd(tile_cnt + tile, (unsigned)__popc(tp));
     }
     const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
     const unsigned kb = __ballot_sync(kFull, keep);
@@ -294,8 +282,8 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
 __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ tile_cnt, uint32_t* __restrict__ counts,
-    uint8_t* __restrict__ state, unsigned long long* __restrict__ counters) {
+    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool valid = i < sc.n;
@@ -512,7 +500,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     }
   }
 
-  count_tiles(reason, g, i, valid, cfg, gw, tile_cnt, masks, counts, state, counters);
+  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -549,8 +537,8 @@ __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
 __global__ void __launch_bounds__(kPreThreads) k_ingest(
     StpSplatBatch b, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ tile_cnt, uint32_t* __restrict__ counts,
-    uint8_t* __restrict__ state, unsigned long long* __restrict__ counters) {
+    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const bool valid = i < b.n;
   int reason = valid ? 0 : 4;
@@ -643,7 +631,7 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     g.ry0 = y0;
     g.ry1 = y1;
   }
-  count_tiles(reason, g, i, valid, cfg, gw, tile_cnt, masks, counts, state, counters);
+  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -730,15 +718,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
 }
 
 // ---------------------------------------------------------------------------
-// K3 duplicate: every surviving (splat, tile) pair writes its entry word
-// ((tile | truncated depth key) << id_bits | id) straight into its tile's
-// bucket (slot from a per-tile cursor; K4 sorts each bucket).
+// K3 duplicate.
 
 __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec* __restrict__ recs, const uint64_t* __restrict__ masks,
-    const uint32_t* __restrict__ counts, int64_t n, DevCam cam, DevCfg cfg, int gw,
-    int depth_bits, int id_bits, int64_t ecap, uint32_t* __restrict__ tile_cur,
-    uint64_t* __restrict__ keys) {
+    const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
+    int depth_bits, int id_bits, int64_t ecap, uint64_t* __restrict__ keys) {
+  __shared__ uint32_t s_pos[kPreThreads];
   __shared__ unsigned long long s_m[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -751,6 +738,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     // only surviving pairs are enumerated (no second cull)
     if (area <= 64) area = (int)cnt;
     s_m[threadIdx.x] = masks[i];
+    s_pos[threadIdx.x] = offsets[i];
   }
   __syncwarp();
   const int wbase = threadIdx.x & ~31;
@@ -778,22 +766,22 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
         if (!cfg.exact) keep = true;
       }
     }
-    // bucket slot: one cursor atomic per (round, tile), ranks among peers
-    const int tile = ty * gw + tx;
-    const unsigned tp = __match_any_sync(kFull, keep ? tile : -1 - lane);
+    // deterministic slot: rank among this round's survivors of the same splat
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned kb = __ballot_sync(kFull, keep) & peers;
+    const uint32_t base = v ? s_pos[wbase + owner] : 0;
+    __syncwarp();
     if (keep) {
-      const int leader = __ffs(tp) - 1;
-      uint32_t b = 0;
-      if (lane == leader) b = atomicAdd(tile_cur + tile, (unsigned)__popc(tp));
-      b = __shfl_sync(tp, b, leader);
-      const uint32_t pos = b + __popc(tp & lt_mask);
       const double depth = key_rec_at(cam, r, ptx, pty);  // rasterizer.py:346-350
+      const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
-        const uint64_t key = ((uint64_t)(uint32_t)tile << depth_bits) |
+        const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
                              (depth_key(depth) >> (32 - depth_bits));
         keys[pos] = (key << id_bits) | (uint64_t)(blockIdx.x * kPreThreads + wbase + owner);
       }
     }
+    if (v && lane == __ffs(peers) - 1 && kb) s_pos[wbase + owner] = base + __popc(kb);
+    __syncwarp();
   });
 }
 
@@ -804,8 +792,7 @@ void launch_init(const Frame& f, cudaStream_t s) {
   const int hist_n = f.passes * 256;
   const int work = max(max(hist_n, f.n_tiles), (int)C_COUNT);
   const int blocks = min((work + 255) / 256, 1024);
-  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp,
-                                f.tile_cnt);
+  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp);
 }
 
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
@@ -813,7 +800,7 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                       f.exact_only ? nullptr : f.recs32, f.masks,
-                                                      f.tile_cnt, f.counts, f.state, f.counters);
+                                                      f.counts, f.state, f.counters);
 #if STP_SPLIT_SH
   k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs,
                                            f.exact_only ? nullptr : f.recs32);
@@ -825,46 +812,7 @@ void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_ingest<<<(unsigned)blocks, kPreThreads, 0, s>>>(b, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                   f.exact_only ? nullptr : f.recs32, f.masks,
-                                                  f.tile_cnt, f.counts, f.state, f.counters);
-}
-
-// K2: exclusive scan of the per-tile entry counts -> bucket ranges, cursors,
-// total entries and non-empty tile count (one block).
-__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ tile_cnt,
-                                                    int n_tiles, int64_t ecap,
-                                                    uint2* __restrict__ ranges,
-                                                    uint32_t* __restrict__ tile_cur,
-                                                    unsigned long long* counters) {
-  __shared__ uint32_t s_warp[32];
-  unsigned long long carry = 0;
-  int nonempty = 0;
-  for (int base = 0; base < n_tiles; base += 1024) {
-    const int t = base + threadIdx.x;
-    const uint32_t v = (t < n_tiles) ? tile_cnt[t] : 0;
-    uint32_t total;
-    const uint32_t ex = block_excl_scan(v, s_warp, total);
-    if (t < n_tiles) {
-      // ranges clamped to the workspace: an overflowing frame (the host
-      // retries it with a larger workspace) never reads past the buffers
-      const unsigned long long off = carry + ex;
-      ranges[t] = make_uint2((uint32_t)min(off, (unsigned long long)ecap),
-                             (uint32_t)min(off + v, (unsigned long long)ecap));
-      tile_cur[t] = (uint32_t)off;
-    }
-    nonempty += v > 0;
-    carry += total;
-  }
-  uint32_t tot_ne;
-  block_excl_scan((uint32_t)nonempty, s_warp, tot_ne);
-  if (threadIdx.x == 0) {
-    counters[C_ENTRIES] = carry;
-    counters[C_TILES] = tot_ne;
-  }
-}
-
-void launch_tile_scan(const Frame& f, cudaStream_t s) {
-  k_tile_scan<<<1, 1024, 0, s>>>(f.tile_cnt, f.n_tiles, f.ecap, f.ranges, f.tile_cur,
-                                 f.counters);
+                                                  f.counts, f.state, f.counters);
 }
 
 void launch_scan(const Frame& f, cudaStream_t s) {
@@ -878,9 +826,10 @@ void launch_scan(const Frame& f, cudaStream_t s) {
 void launch_duplicate(const Frame& f, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
-  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.n, f.cam,
+  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
+                                                     f.cam,
                                                      f.cfg, f.gw, f.depth_bits, f.id_bits, f.ecap,
-                                                     f.tile_cur, f.keys[0]);
+                                                     f.keys[0]);
 }
 
 }  // namespace stp

@@ -178,159 +178,6 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 }
 
 // ---------------------------------------------------------------------------
-// K4 (tile buckets): each tile's bucket -- filled by K3 in arbitrary order --
-// is sorted by its truncated depth key with a CTA-wide stable LSD radix sort
-// (9-bit digits, 3 passes at 27 depth bits) in shared memory; buckets larger
-// than the shared-memory capacity run the same passes through global memory
-// (the free ping-pong buffer).  Order inside equal keys is left to K5, which
-// re-sorts those runs by (float64 depth, rank).
-
-constexpr int kTsThreads = 256;
-constexpr int kTsWarps = kTsThreads / 32;
-constexpr int kTsCap = 4096;  // entries sorted in shared memory
-constexpr int kTsBits = 9;
-constexpr int kTsBins = 1 << kTsBits;
-
-struct TileSortSmem {
-  unsigned long long buf[2][kTsCap];
-  uint32_t off[kTsWarps][kTsBins];  // per-warp digit counts, then write offsets
-  uint32_t part[kTsWarps];
-  int tile;
-};
-
-// exclusive scan over a 256-thread block
-__device__ __forceinline__ uint32_t block_scan256(uint32_t v, uint32_t* part) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) part[w] = x;
-  __syncthreads();
-  uint32_t pre = 0;
-  for (int k = 0; k < w; ++k) pre += part[k];
-  __syncthreads();
-  return pre + x - v;
-}
-
-// one stable LSD pass (digit = bits [shift, shift+bits)) over n words, src -> dst
-__device__ void cta_radix_pass(const unsigned long long* src, unsigned long long* dst, int n,
-                               int shift, int bits, TileSortSmem& sm) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const unsigned lt_mask = (1u << lane) - 1;
-  const uint32_t mask = (1u << bits) - 1u;
-  for (int k = tid; k < kTsWarps * kTsBins; k += kTsThreads) (&sm.off[0][0])[k] = 0;
-  __syncthreads();
-  // warp w owns the contiguous slice [lo, hi): stable across warps
-  const int chunk = (n + kTsWarps - 1) / kTsWarps;
-  const int lo = min(n, w * chunk), hi = min(n, lo + chunk);
-  for (int b = lo; b < hi; b += 32) {
-    const int k = b + lane;
-    const bool v = k < hi;
-    const uint32_t d = v ? (uint32_t)(src[k] >> shift) & mask : 0xffffffffu;
-    const unsigned peers = __match_any_sync(kFull, d);
-    if (v && lane == __ffs(peers) - 1) sm.off[w][d] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  // offsets, digit-major then warp: each thread owns kTsBins / 256 digits
-  constexpr int kPer = kTsBins / kTsThreads;
-  uint32_t tot[kPer], sum = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int d = tid * kPer + j;
-    uint32_t t = 0;
-    for (int ww = 0; ww < kTsWarps; ++ww) t += sm.off[ww][d];
-    tot[j] = t;
-    sum += t;
-  }
-  uint32_t base = block_scan256(sum, sm.part);
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int d = tid * kPer + j;
-    for (int ww = 0; ww < kTsWarps; ++ww) {
-      const uint32_t c = sm.off[ww][d];
-      sm.off[ww][d] = base;
-      base += c;
-    }
-  }
-  __syncthreads();
-  for (int b = lo; b < hi; b += 32) {
-    const int k = b + lane;
-    const bool v = k < hi;
-    const unsigned long long x = v ? src[k] : 0ull;
-    const uint32_t d = v ? (uint32_t)(x >> shift) & mask : 0xffffffffu;
-    const unsigned peers = __match_any_sync(kFull, d);
-    if (v) dst[sm.off[w][d] + __popc(peers & lt_mask)] = x;
-    __syncwarp();
-    if (v && lane == __ffs(peers) - 1) sm.off[w][d] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kTsThreads, 2) k_tile_sort(unsigned long long* keys,
-                                                             unsigned long long* tmp,
-                                                             const uint2* __restrict__ ranges,
-                                                             int n_tiles, int shift0, int dbits,
-                                                             unsigned long long* counters) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSortSmem& sm = *reinterpret_cast<TileSortSmem*>(smem_raw);
-  const int passes = (dbits + kTsBits - 1) / kTsBits;
-  for (;;) {
-    if (threadIdx.x == 0) sm.tile = (int)atomicAdd(counters + C_TSORT, 1ull);
-    __syncthreads();
-    const int t = sm.tile;
-    __syncthreads();
-    if (t >= n_tiles) break;
-    const uint2 rg = ranges[t];
-    const int n = (int)(rg.y - rg.x);
-    if (n <= 1) continue;
-    if (n <= kTsCap) {
-      for (int k = threadIdx.x; k < n; k += kTsThreads) sm.buf[0][k] = keys[rg.x + k];
-      __syncthreads();
-      for (int p = 0; p < passes; ++p)
-        cta_radix_pass(sm.buf[p & 1], sm.buf[(p & 1) ^ 1], n, shift0 + kTsBits * p,
-                       min(kTsBits, dbits - kTsBits * p), sm);
-      for (int k = threadIdx.x; k < n; k += kTsThreads) keys[rg.x + k] = sm.buf[passes & 1][k];
-    } else {
-      unsigned long long* a = keys + rg.x;
-      unsigned long long* b = tmp + rg.x;
-      for (int p = 0; p < passes; ++p) {
-        cta_radix_pass(a, b, n, shift0 + kTsBits * p, min(kTsBits, dbits - kTsBits * p), sm);
-        unsigned long long* c = a;
-        a = b;
-        b = c;
-      }
-      if (a != keys + rg.x)
-        for (int k = threadIdx.x; k < n; k += kTsThreads) keys[rg.x + k] = a[k];
-    }
-    __syncthreads();
-  }
-}
-
-int launch_tile_sort(const Frame& f, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(TileSortSmem));
-    attr_set = true;
-  }
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = min(f.n_tiles, 2 * n_sm);
-  if (grid > 0)
-    k_tile_sort<<<grid, kTsThreads, sizeof(TileSortSmem), s>>>(
-        reinterpret_cast<unsigned long long*>(f.keys[0]),
-        reinterpret_cast<unsigned long long*>(f.keys[1]), f.ranges, f.n_tiles, f.id_bits,
-        f.depth_bits, f.counters);
-  return 0;
-}
-
-// ---------------------------------------------------------------------------
 // K5 tile ranges + float64 tie fix-up.
 
 __device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ recs, const DevCam& cam,
@@ -393,7 +240,8 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
     // buffer for k_ties
     if (kn == k || (i > 0 && kp == k)) d64[i] = entry_depth64(recs, cam, id, (int)tile, gw);
   }
-  (void)heads;  // non-empty tiles are counted by k_tile_scan
+  const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
+  if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
 }
 
 // K5b: each run of equal keys is re-ordered by (float64 depth, rank); the

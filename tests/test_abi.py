@@ -125,7 +125,6 @@ def test_workspace_layout(lib):
     # 13 tile bits + 27 depth bits: 5 eight-bit passes; ids in the low 10 bits
     assert (L.sort_bits, L.depth_bits, L.sort_passes, L.id_bits) == (40, 27, 5, 10)
     regions = sorted((getattr(L, k), k) for k in ("recs", "recs32", "fb_items", "camera", "masks",
-                                                    "tile_cnt", "tile_cur",
                                                     "state", "counts", "offsets", "keys0",
                                                     "keys1", "vals", "ranges",
                                                     "counters", "hist", "lookback",
