@@ -215,3 +215,17 @@ def test_splatbatch_input_oracle_scaled():
     np.testing.assert_allclose(out.color, ref["color"], atol=TOL, rtol=0)
     np.testing.assert_allclose(out.transmittance, ref["transmittance"], atol=TOL, rtol=0)
     np.testing.assert_allclose(out.depth, ref["depth"], atol=TOL, rtol=1e-5)
+
+
+def test_oracle_parity_c4_law_4k():
+    """C4 law (dense depth stack, 2% long elongated splats) on a full 3840x2160
+    frame: 32,400 tiles (15 tile bits, 25 depth bits in the sort word) at
+    120k Gaussians, against the oracle."""
+    from paper_2402_00525_b200 import Camera, Hierarchical, RenderConfig, scenes
+    arrs = scenes.to_f32_scene(scenes.frustum_cloud(120_000, 4, 3840, 2160, 2200.0, z_lo=2.0,
+                                                    z_hi=6.0, elongated_frac=0.02))
+    cam = Camera(rotation=np.eye(3), position=np.zeros(3), fx=2200.0, fy=2200.0, width=3840,
+                 height=2160)
+    out, ref = _oracle_compare(arrs, cam, RenderConfig(with_depth=True), Hierarchical(),
+                               records=False)
+    assert out.stats["tiles"] > 8192
