@@ -33,7 +33,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("frames/sec at 1080p, 3M Gaussians (1 GPU); views/sec at 1/2/4/8 B200; HBM GB/s")
 UNIT = "views/s"
-WORKLOAD = "C3: synthetic 3M-Gaussian garden-scale scene (SH3), 256-view 1920x1080 orbit"
+WORKLOADS = {
+    "C1": "C1: synthetic 10k random Gaussians (SH0), single 256x256 view",
+    "C2": "C2: synthetic 1M Gaussians (SH3), single 1920x1080 view",
+    "C3": "C3: synthetic 3M-Gaussian garden-scale scene (SH3), 256-view 1920x1080 orbit",
+    "C4": "C4: synthetic 6M Gaussians (SH3) at 3840x2160, culling / queue stress",
+    "C5": "C5: synthetic 1.5M half-density scene (SH3), 1080p rotation sweep",
+}
 
 
 def parse():
@@ -161,11 +167,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
         "steps": done, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "gaussians": len(scene["opacity"]),
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.config.upper()], "gaussians": len(scene["opacity"]),
                                         "width": cams[0].width, "height": cams[0].height,
                                         "views": len(cams), "mode": "hierarchical:64/8/4"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{done} full C3 views (project + bin_and_sort + "
+                         "sample": f"{done} full {args.config.upper()} views (project + bin_and_sort + "
                                    f"hierarchical render of all tiles) by oracle/stp_oracle.cpp, "
                                    f"the float64 C++ restatement of the reference pinned to its "
                                    f"golden outputs; requested steps={args.steps}, timed within "
@@ -394,7 +400,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 geometry/decisions + f32 blend",
         "data": "synthetic (seeded scene generator, paper_2402_00525_b200/scenes.py)",
-        "config": {"workload": WORKLOAD, "gaussians": gs.n, "sh_degree": 3, "width": W,
+        "config": {"workload": WORKLOADS[args.config.upper()], "gaussians": gs.n, "sh_degree": int(round(gs.sh_coeffs ** 0.5)) - 1, "width": W,
                    "height": H, "views": n_views, "views_per_step_per_gpu": 1,
                    "parallelism": f"views sharded over {world} GPU(s), no hot-path collective; "
                                   f"{n_str} views in flight per GPU (streams)",
@@ -428,7 +434,7 @@ def run_ours(args):
         host = {k: dev_t[k].cpu().numpy() for k in keys}
         rate, done, times = cpu_view_rate(host, cams, [my_views[warm]] * 3, 30.0, threads)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"{done} full C3 view(s) (view {my_views[warm]}): "
+                                "sample": f"{done} full {args.config.upper()} view(s) (view {my_views[warm]}): "
                                           "project + bin_and_sort + hierarchical render of "
                                           "all tiles by the float64 C++ restatement "
                                           "(oracle/stp_oracle.cpp)"}
