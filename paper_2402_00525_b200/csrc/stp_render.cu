@@ -33,6 +33,9 @@
 
 namespace stp {
 
+#ifndef STP_QT_SPECIALIZE
+#define STP_QT_SPECIALIZE 1
+#endif
 #ifndef STP_EXACT_MINB
 #define STP_EXACT_MINB 4
 #endif
@@ -366,11 +369,15 @@ struct SubQ {
 };
 
 // QMX = 8: mid queues of at most 8 (loops statically bounded); 0: generic.
-template <int QH, bool EXACT, int QMX>
+// QT > 0: the queue sizes are compile-time (tail QT, mid QMX), so every
+// shared-memory offset is an immediate (the default 64/8/4 configuration;
+// otherwise the compiler re-derives the offsets inside the hot loops).
+template <int QH, bool EXACT, int QMX, int QT>
 __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
-  const int qt = A.cfg.q_tail, qm = A.cfg.q_mid, qh_rt = A.cfg.q_head;
+  const int qt = QT ? QT : A.cfg.q_tail, qm = (QT && QMX) ? QMX : A.cfg.q_mid;
+  const int qh_rt = A.cfg.q_head;
   const int R = ring_size(qm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 64; i += kRenderThreads) s_tab[i] = kExp2Tab[i];
@@ -632,6 +639,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       if (pa > ring_full || pb > ring_full || (ready && pa + pb > 0)) {
         // ================= consume: pixels take emits from their quad rings
         const int rounds = (pa > 0 && pb > 0) ? min(pa, pb) : max(pa, pb);
+        STAT_ADD(9, lane == 0);
         {
           const int pend = ps ? pb : pa;
           const int base = ps ? rh1 : rh0;
@@ -649,19 +657,42 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
             uint32_t ids[STP_PIX_UNROLL];
             double ts[STP_PIX_UNROLL], as[STP_PIX_UNROLL];
             bool ps[STP_PIX_UNROLL];
-            STAT_ADD(4, e < pend);
-            STAT_ADD(5, e < pend && live);
+#ifdef STP_WORK_STATS
+            bool evk[STP_PIX_UNROLL], fk[STP_PIX_UNROLL];
+#pragma unroll
+            for (int k = 0; k < STP_PIX_UNROLL; ++k) evk[k] = fk[k] = false;
+#endif
             if (e < lim && live) {
 #pragma unroll
               for (int k = 0; k < STP_PIX_UNROLL; ++k) {
                 const bool vk = e + k < lim;
                 ids[k] = ring[(base + e + (vk ? k : 0)) & (R - 1)];
                 ps[k] = emit_eval_bf(P, A, ids[k], s_tab, ts[k], as[k]) & vk;
+#ifdef STP_WORK_STATS
+                evk[k] = vk;
+                fk[k] = vk && !ps[k];
+#endif
               }
 #pragma unroll
               for (int k = 0; k < STP_PIX_UNROLL; ++k)
                 if (ps[k] && P.T >= term) head_push<QH, EXACT>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
             }
+#ifdef STP_WORK_STATS
+            STAT_ADD(8, lane == 0);
+#pragma unroll
+            for (int k = 0; k < STP_PIX_UNROLL; ++k) {
+              STAT_ADD(4, e + k < pend);
+              STAT_ADD(5, evk[k]);
+              STAT_ADD(6, evk[k] && !fk[k]);
+              // quad lanes: base b, b+1, b+4, b+5; all slots of live quad
+              // lanes failed (terminated lanes count as failed)
+              const unsigned bf = __ballot_sync(kFull, fk[k] || (e + k < pend && !evk[k]));
+              const unsigned bv = __ballot_sync(kFull, e + k < pend);
+              const int qb = (lane & 16) + (pq >> 1) * 8 + (pq & 1) * 2;
+              const unsigned qmask = 0x33u << qb;
+              STAT_ADD(7, evk[k] && (bf & qmask) == qmask && (bv & qmask) == qmask);
+            }
+#endif
           }
         }
         rh0 += min(rounds, pa);
@@ -863,15 +894,15 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
 
 size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
 
-template <int QH, bool EXACT, int QMX>
+template <int QH, bool EXACT, int QMX, int QT = 0>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
   static int blocks_per_sm = 0, n_sm = 0;
   if (smem != attr || blocks_per_sm == 0) {
-    cudaFuncSetAttribute(k_render<QH, EXACT, QMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_render<QH, EXACT, QMX, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT>,
                                                   kRenderThreads, smem);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -880,7 +911,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   }
   const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = min(want, n_sm * blocks_per_sm);
-  if (grid > 0) k_render<QH, EXACT, QMX><<<grid, kRenderThreads, smem, s>>>(A);
+  if (grid > 0) k_render<QH, EXACT, QMX, QT><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
 void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
@@ -910,7 +941,11 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   switch (f.cfg.q_head) {
     case 1: launch_render_t<1, true, 8>(A, smem, s); break;
     case 2: launch_render_t<2, true, 8>(A, smem, s); break;
-    case 4: launch_render_t<4, true, 8>(A, smem, s); break;
+    case 4:
+      if (STP_QT_SPECIALIZE && f.cfg.q_tail == 64 && f.cfg.q_mid == 8)
+        launch_render_t<4, true, 8, 64>(A, smem, s);
+      else launch_render_t<4, true, 8>(A, smem, s);
+      break;
     case 8: launch_render_t<8, true, 8>(A, smem, s); break;
     case 16: launch_render_t<16, true, 8>(A, smem, s); break;
     default: launch_render_t<16, false, 8>(A, smem, s); break;
