@@ -134,6 +134,20 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.T = P.T * (1.0 - al);
 }
 
+// blend of a live pixel (P.T >= term checked by the caller)
+__device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double t, double al,
+                                           uint32_t id) {
+  const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
+  const double w = al * P.T;
+  const float wf = (float)w;
+  P.C0 += oc.y * wf;
+  P.C1 += oc.z * wf;
+  P.C2 += oc.w * wf;
+  P.D += (float)(t * w);
+  if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
+  P.T = P.T * (1.0 - al);
+}
+
 // alpha / eps test / cap / pixel-ray t_opt of one emitted entry
 // (hierarchy.py:94-105).  Returns false when the entry is dropped.
 __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, uint32_t id,
@@ -202,6 +216,26 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
                                           double t, double al, uint32_t id) {
   const int qh = EXACT ? QH : qh_rt;
   const bool full = H.n >= qh;
+  if (EXACT && full) {
+    // c[i] = e < H[i] is monotone in i (H sorted).  The blended entry is
+    // min(e, H[0]); the new queue is R[i] = c[i] ? H[i] : (c[i+1] ? e :
+    // H[i+1]), R[QH-1] = c[QH-1] ? H[QH-1] : e (unchanged when c[0]).  All
+    // compares issue in parallel, no branch.  The caller checked P.T >= term.
+    bool c[QH];
+#pragma unroll
+    for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
+    blend_live(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
+#pragma unroll
+    for (int i = 0; i < QH; ++i) {
+      const bool nx = i + 1 < QH;
+      const int j = nx ? i + 1 : i;
+      const bool cn = nx ? c[j] : false;
+      H.t[i] = c[i] ? H.t[i] : (cn ? t : (nx ? H.t[j] : t));
+      H.a[i] = c[i] ? H.a[i] : (cn ? al : (nx ? H.a[j] : al));
+      H.id[i] = c[i] ? H.id[i] : (cn ? id : (nx ? H.id[j] : id));
+    }
+    return;
+  }
   if (full) {
     const bool e_min = lt(t, id, H.t[0], H.id[0]);
     blend(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
