@@ -214,10 +214,23 @@ __device__ __forceinline__ double exp_neg(double p, const double* tab) {
 }
 
 
-// exp_neg without the p > 700 branch (the caller clamps p)
+// a <= b ? a : b (= fmin for a non-NaN b; a NaN gives b) as one compare and
+// one select: the compiler would canonicalise the ternary to fmin and expand
+// it to a 5-instruction min/NaN sequence.
+__device__ __forceinline__ double min_le(double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+      : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+
+// exp_neg without the p > 700 branch (the caller clamps p).  k = round(p *
+// 64/ln2) via the 1.5*2^52 shifter (no FRND/F2I), and 2^-(k>>6) folded into
+// the table entry's exponent field (exact: no underflow for p <= 700).
 __device__ __forceinline__ double exp_neg_nb(double p, const double* tab) {
-  const double kd = rint(p * c_exp_k[0]);
-  const int k = (int)kd;
+  const double sh = fma(p, c_exp_k[0], 0x1.8p52);
+  const int k = __double2loint(sh);
+  const double kd = sh - 0x1.8p52;
   double r = fma(-kd, c_exp_k[1], p);
   r = fma(-kd, c_exp_k[2], r);
   double e = c_exp_k[3];
@@ -227,9 +240,9 @@ __device__ __forceinline__ double exp_neg_nb(double p, const double* tab) {
   e = fma(e, -r, c_exp_k[7]);
   e = fma(e, -r, 1.0);
   e = fma(e, -r, 1.0);
-  const int j = k & 63, ex = k >> 6;
-  const double scale = __hiloint2double((1023 - ex) << 20, 0);
-  return tab[j] * e * scale;
+  const double tj = tab[k & 63];
+  const double ts = __hiloint2double(__double2hiint(tj) - ((k >> 6) << 20), __double2loint(tj));
+  return ts * e;
 }
 
 // exponent of gauss2d (tile_culling.py:96)

@@ -199,10 +199,10 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
   const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
   const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
   t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
-  const double pc = fmin(pw, 700.0);
+  const double pc = min_le(pw, 700.0);
   al = (double)op * exp_neg_nb(pc, tab);
   const bool pass = al >= A.cfg.eps;  // hierarchy.py:99-101
-  al = fmin(al, A.cfg.cap);
+  al = min_le(al, A.cfg.cap);
   return pass;
 }
 
