@@ -139,7 +139,9 @@ typedef struct {
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
   size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
-      counters, hist, lookback, scan_scratch, total;
+      counters, hist, lookback, scan_scratch,
+      rowlist, /* ids of kept Gaussians whose coarse rect exceeds 64 tiles */
+      total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;
   int32_t splat_record_bytes;

@@ -79,7 +79,7 @@ class StpStats(ctypes.Structure):
 class StpLayout(ctypes.Structure):
     _fields_ = [(n, ctypes.c_size_t) for n in (
         "recs", "recs32", "fb_items", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals", "ranges",
-        "counters", "hist", "lookback", "scan_scratch", "total")] + [
+        "counters", "hist", "lookback", "scan_scratch", "rowlist", "total")] + [
         ("entry_capacity", ctypes.c_int64), ("n_tiles", ctypes.c_int32),
         ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32),
         ("sort_passes", ctypes.c_int32), ("sort_bits", ctypes.c_int32),

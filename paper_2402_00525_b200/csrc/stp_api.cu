@@ -64,6 +64,7 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.state = o;        o = align_up(o + (size_t)n);
   L.counts = o;       o = align_up(o + (size_t)n * 4);
   L.offsets = o;      o = align_up(o + (size_t)n * 4);
+  L.rowlist = o;      o = align_up(o + (size_t)n * 4);
   L.lookback = o;     o = align_up(o + (size_t)L.sort_passes * L.partitions * 256 * 8);
   L.keys0 = o;        o = align_up(o + (size_t)ecap * 8);
   L.keys1 = o;        o = align_up(o + (size_t)ecap * 8);
@@ -128,6 +129,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.fb_items = reinterpret_cast<uint32_t*>(b + L.fb_items);
   f.camp = reinterpret_cast<DevCam*>(b + L.camera);
   f.masks = reinterpret_cast<uint64_t*>(b + L.masks);
+  f.rowlist = reinterpret_cast<uint32_t*>(b + L.rowlist);
   f.exact_only = (cfg->flags & STP_FLAG_FAST32) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;

@@ -89,6 +89,7 @@ enum Counter {
   C_TILES = 6,
   C_NONFINITE = 7,
   C_TIES = 8,
+  C_ROWS = 9,       // K1: Gaussians appended to the row-culling list
   C_PART = 16,      // 8 per-pass partition counters
   C_WORK = 24,      // render work counter
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
@@ -306,12 +307,16 @@ __device__ __forceinline__ double key_rec(const double* m, double q0, double q1,
 }
 
 // camera ray (u, w, 1) through a float64 image point and its length
-__device__ __forceinline__ void cam_ray(const DevCam& cam, double x, double y, double& u,
-                                        double& w, double& vn) {
-  u = (x - cam.cx) * cam.inv_fx;
-  w = (y - cam.cy) * cam.inv_fy;
+__device__ __forceinline__ void cam_ray_i(double cx, double cy, double ifx, double ify, double x,
+                                          double y, double& u, double& w, double& vn) {
+  u = (x - cx) * ifx;
+  w = (y - cy) * ify;
   const double vv = fma(u, u, fma(w, w, 1.0));
   vn = vv * frsqrt(vv);
+}
+__device__ __forceinline__ void cam_ray(const DevCam& cam, double x, double y, double& u,
+                                        double& w, double& vn) {
+  cam_ray_i(cam.cx, cam.cy, cam.inv_fx, cam.inv_fy, x, y, u, w, vn);
 }
 
 // t_opt of a SplatRec along the ray through a float64 image point
@@ -365,6 +370,78 @@ __device__ __forceinline__ bool tile_survives(double mx, double my, double a, do
   return alpha_keep(gpower(a, b, c, ptx - mx, pty - my), thr, op, eps);
 }
 
+// Rects over 64 tiles whose ellipse covers well under half of them (long thin
+// or faint splats) are culled row by row (row_span, k_rows_*); the others
+// (large round splats fill their rect) stay on K1/K3's per-tile path, where
+// their pairs share the warp's load-balanced rounds.  A heuristic (fp32, only
+// K1 evaluates it and lists the Gaussian): est = ellipse area + perimeter in
+// tiles.
+#ifndef STP_ROWS
+#define STP_ROWS 1
+#endif
+__device__ __forceinline__ bool use_rows(double a, double b, double c, double thr, int area) {
+  if (!STP_ROWS || area <= 64) return false;
+  const float fa = (float)a, fb = (float)b, fc = (float)c;
+  const float D = fmaf(fa, fc, -fb * fb);
+  const float T = fmaxf((float)thr, 0.f) + 1e-6f;
+  if (!(D > 0.f)) return true;
+  const float iD = __frcp_rn(D);
+  const float hx = sqrtf(2.f * T * fc * iD), hy = sqrtf(2.f * T * fa * iD);
+  const float est = 3.14159265f * 2.f * T * rsqrtf(D) * (1.f / 256.f) + (hx + hy) * 0.125f + 1.f;
+  return (float)area > 2.f * est;
+}
+
+// Superset of the tile columns of tile row ty (within [rx0, rx1]) that
+// tile_survives can keep, for rects too large to test tile by tile.  A kept
+// tile holds its Alg. 1 point, where power <= thr + 1e-9 (alpha_keep), so it
+// meets the ellipse E = {d : d^T Q d <= 2T}, Q = [[a, b], [b, c]], T = thr
+// + margin.  E's x-extent over the row's band: the right boundary
+// R(dy) = (-b dy + sqrt(2Ta - D dy^2)) / a (D = ac - b^2) is concave with its
+// maximum at the rightmost point of E, dy = -b sqrt(2T / (cD)); L mirrors it.
+// Returns lo > hi when the row cannot hold a kept tile; degenerate or
+// non-finite input returns the whole row.
+__device__ __forceinline__ void row_span(double mx, double my, double a, double b, double c,
+                                         double thr, int ty, int rx0, int rx1, int& lo,
+                                         int& hi) {
+  lo = rx0;
+  hi = rx1;
+  const double T = thr + 1e-6 + 1e-6 * fabs(thr);
+  const double D = a * c - b * b;
+  if (!(D > 0.0 && a > 0.0 && c > 0.0 && T < 1e300 && mx == mx && my == my)) return;
+  if (!(T > 0.0)) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  const double iD = 1.0 / D;
+  const double ye = sqrt(2.0 * T * a * iD) * (1.0 + 1e-9) + 1e-9;  // |dy| on E
+  double y0 = (double)(ty * kTile) - my, y1 = y0 + (double)kTile;
+  y0 = fmax(y0, -ye);
+  y1 = fmin(y1, ye);
+  if (y0 > y1) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  const double ys = b * sqrt(2.0 * T / (c * D));  // dy of the leftmost point of E
+  const double yr = fmin(fmax(-ys, y0), y1), yl = fmin(fmax(ys, y0), y1);
+  const double ia = 1.0 / a;
+  const double xr = (-b * yr + sqrt(fmax(2.0 * T * a - D * yr * yr, 0.0))) * ia;
+  const double xl = (-b * yl - sqrt(fmax(2.0 * T * a - D * yl * yl, 0.0))) * ia;
+  const double del = 1e-3 + 1e-7 * (fabs(mx) + fabs(xl) + fabs(xr));
+  const double XL = mx + xl - del, XR = mx + xr + del;
+  // tiles [16 tx, 16 tx + 16] meeting [XL, XR]
+  const double flo = fmax(ceil(XL * (1.0 / kTile)) - 1.0, (double)rx0);
+  const double fhi = fmin(floor(XR * (1.0 / kTile)), (double)rx1);
+  if (!(flo <= fhi)) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  lo = (int)flo;
+  hi = (int)fhi;
+}
+
 }  // namespace stp
 
 // Host-side launchers (defined in the .cu files, called by stp_api.cu).
@@ -374,6 +451,7 @@ struct Frame {
   SplatRec* recs;
   SplatRec32* recs32;
   uint64_t* masks;        // per Gaussian: surviving tiles of a <= 64-tile coarse rect
+  uint32_t* rowlist;      // ids of kept Gaussians with a > 64-tile rect (C_ROWS of them)
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;

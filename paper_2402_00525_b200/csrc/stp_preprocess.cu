@@ -16,6 +16,9 @@
 namespace stp {
 
 constexpr int kPreThreads = 256;
+constexpr int kMaskTiles = 64;  // rects up to this many tiles carry a survivor mask (K1 -> K3)
+// masks[] value of a Gaussian K1 listed for the row kernels (rect > 64 tiles)
+constexpr unsigned long long kRowsListed = ~0ull;
 #ifndef STP_K1_MINB
 #define STP_K1_MINB 3
 #endif
@@ -206,6 +209,7 @@ __device__ __forceinline__ void coarse_rect(double px, double py, double radius,
 // ingest kernel with reason 0 (kept) .. 4 (out of range).
 __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64_t i, bool valid,
                                             const DevCfg& cfg, uint64_t* __restrict__ masks,
+                                            uint32_t* __restrict__ rowlist,
                                             uint32_t* __restrict__ counts,
                                             uint8_t* __restrict__ state,
                                             unsigned long long* __restrict__ counters) {
@@ -214,7 +218,10 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
   __shared__ uint32_t s_cnt[kPreThreads];
   __shared__ unsigned long long s_mask[kPreThreads];
   const int wx = g.rx1 - g.rx0 + 1, wy = g.ry1 - g.ry0 + 1;
-  const int area = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
+  const int full = (reason == 0 && wx > 0 && wy > 0) ? wx * wy : 0;
+  // sparse rects over 64 tiles (exact culling) go to the row kernels
+  const bool rows = cfg.exact && full > kMaskTiles && use_rows(g.a, g.b, g.c, g.thr, full);
+  const int area = rows ? 0 : full;
   {
     StagedGeo& sg = s_geo[threadIdx.x];
     sg.mx = g.mx;
@@ -234,6 +241,16 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
   }
   __syncwarp();
   const int wbase = threadIdx.x & ~31;
+#ifdef STP_WORK_STATS
+  {
+    const unsigned tot = __reduce_add_sync(kFull, (unsigned)full);
+    const unsigned big = __reduce_add_sync(kFull, full > 64 ? (unsigned)full : 0u);
+    if (lane == 0) {
+      atomicAdd(counters + C_STAT + 10, (unsigned long long)tot);
+      atomicAdd(counters + C_STAT + 11, (unsigned long long)big);
+    }
+  }
+#endif
   warp_expand(area, lane, [&](bool v, int owner, int local) {
     bool keep = false;
     if (v) {
@@ -256,10 +273,22 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
     }
     __syncwarp();
   });
+  // large rects: appended to the row list; k_rows_count counts them
+  {
+    const unsigned rb = __ballot_sync(kFull, rows);
+    if (rb) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(counters + C_ROWS, (unsigned long long)__popc(rb));
+      base = __shfl_sync(kFull, base, 0);
+      if (rows) rowlist[base + __popc(rb & ((1u << lane) - 1))] = (uint32_t)i;
+    }
+  }
   const uint32_t cnt = s_cnt[threadIdx.x];
   if (valid) {
     counts[i] = cnt;
-    if (cnt) masks[i] = s_mask[threadIdx.x];
+    // (rects over 64 tiles keep no survivor mask: 0, or the listed marker)
+    if (cnt) masks[i] = full <= kMaskTiles ? s_mask[threadIdx.x] : 0ull;
+    else if (rows) masks[i] = kRowsListed;  // K3 leaves it to k_rows_dup
     if (state) state[i] = (uint8_t)reason;
   }
   // projection stats: per-warp ballots added to per-SM slots (no block
@@ -282,7 +311,7 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
 __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    uint32_t* __restrict__ rowlist, uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -500,7 +529,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     }
   }
 
-  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
+  count_tiles(reason, g, i, valid, cfg, masks, rowlist, counts, state, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -537,7 +566,7 @@ __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
 __global__ void __launch_bounds__(kPreThreads) k_ingest(
     StpSplatBatch b, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    uint32_t* __restrict__ rowlist, uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const bool valid = i < b.n;
@@ -631,7 +660,7 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     g.ry0 = y0;
     g.ry1 = y1;
   }
-  count_tiles(reason, g, i, valid, cfg, masks, counts, state, counters);
+  count_tiles(reason, g, i, valid, cfg, masks, rowlist, counts, state, counters);
 }
 
 // ---------------------------------------------------------------------------
@@ -735,9 +764,11 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const short4 rc = *reinterpret_cast<const short4*>(&recs[i].rx0);
     area = (rc.y - rc.x + 1) * (rc.w - rc.z + 1);
     // rects of <= 64 tiles: K1 left the survivors' positions in a mask, so
-    // only surviving pairs are enumerated (no second cull)
-    if (area <= 64) area = (int)cnt;
+    // only surviving pairs are enumerated (no second cull); larger ones go
+    // row by row below (exact culling)
     s_m[threadIdx.x] = masks[i];
+    if (area <= kMaskTiles) area = (int)cnt;
+    else if (s_m[threadIdx.x] == kRowsListed) area = 0;  // k_rows_dup
     s_pos[threadIdx.x] = offsets[i];
   }
   __syncwarp();
@@ -786,6 +817,107 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
 }
 
 // ---------------------------------------------------------------------------
+// Sparse large rects (K1b count, K3b duplicate).  A Gaussian whose coarse
+// rect exceeds kMaskTiles tiles and is mostly empty (use_rows: long thin or
+// faint splats; up to thousands of tiles at 4K, most far from the ellipse)
+// is listed by K1 and handled here instead of tile by tile: one warp per
+// (Gaussian, 32-row chunk) unit, the chunk's rows one per lane, each row's
+// candidate columns from row_span, and only those candidates take the exact
+// test (tile_survives), spread over the lanes by warp_expand.  Same survivors
+// as testing every tile.
+
+template <class F>
+__device__ __forceinline__ void for_row_tiles(const SplatRec& o, int r0, int nrows, double eps,
+                                              F&& fn) {
+  const int lane = threadIdx.x & 31;
+  int lo = 1, hi = 0;
+  const int ty = o.ry0 + r0 + lane;
+  const bool v = lane < nrows;
+  if (v) row_span(o.mx, o.my, o.ca, o.cb, o.cc, o.thr, ty, o.rx0, o.rx1, lo, hi);
+  warp_expand(v && hi >= lo ? hi - lo + 1 : 0, lane, [&](bool v2, int u, int col) {
+    const int tyu = __shfl_sync(kFull, ty, u);
+    const int tx = __shfl_sync(kFull, lo, u) + col;
+    bool keep = false;
+    double ptx = 0.0, pty = 0.0;
+    if (v2)
+      keep = tile_survives(o.mx, o.my, o.ca, o.cb, o.cc, o.inv_a, o.inv_c, o.thr, o.op, eps, tx,
+                           tyu, ptx, pty);
+    fn(keep, tx, tyu, ptx, pty);
+  });
+}
+
+// unit w -> (listed Gaussian, rows [r0, r0 + nr)); cpg = 32-row chunks per
+// Gaussian (ceil(grid_h / 32)), the surplus chunks of shorter rects are empty
+__device__ __forceinline__ const SplatRec& row_unit(const SplatRec* __restrict__ recs,
+                                                    const uint32_t* __restrict__ rowlist,
+                                                    int64_t w, int cpg, uint32_t& id, int& r0,
+                                                    int& nr) {
+  id = rowlist[w / cpg];
+  const SplatRec& o = recs[id];
+  r0 = (int)(w % cpg) * 32;
+  nr = max(0, min(o.ry1 - o.ry0 + 1 - r0, 32));
+  return o;
+}
+
+__global__ void __launch_bounds__(256) k_rows_count(const SplatRec* __restrict__ recs,
+                                                    const uint32_t* __restrict__ rowlist,
+                                                    const unsigned long long* counters,
+                                                    DevCfg cfg, int cpg,
+                                                    uint32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t units = (int64_t)counters[C_ROWS] * cpg;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < units;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t id;
+    int r0, nr;
+    const SplatRec& o = row_unit(recs, rowlist, w, cpg, id, r0, nr);
+    if (nr == 0) continue;
+    unsigned cnt = 0;
+    for_row_tiles(o, r0, nr, cfg.eps, [&](bool keep, int, int, double, double) {
+      cnt += __popc(__ballot_sync(kFull, keep));
+    });
+    // counts[id] is 0 from K1; the chunks of one Gaussian add up
+    if (lane == 0 && cnt) atomicAdd(counts + id, cnt);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rows_dup(const SplatRec* __restrict__ recs,
+                                                  const uint32_t* __restrict__ rowlist,
+                                                  const unsigned long long* counters,
+                                                  uint32_t* __restrict__ offsets, DevCam cam,
+                                                  DevCfg cfg, int cpg, int gw, int depth_bits,
+                                                  int id_bits, int64_t ecap,
+                                                  uint64_t* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1;
+  const int64_t units = (int64_t)counters[C_ROWS] * cpg;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < units;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t id;
+    int r0, nr;
+    const SplatRec& o = row_unit(recs, rowlist, w, cpg, id, r0, nr);
+    if (nr == 0) continue;
+    for_row_tiles(o, r0, nr, cfg.eps, [&](bool keep, int tx, int ty, double ptx, double pty) {
+      // slots: the Gaussian's offset is its write cursor (its entries are
+      // distinct sort words, so their order in the unsorted array is free)
+      const unsigned kb = __ballot_sync(kFull, keep);
+      uint32_t base = 0;
+      if (lane == 0 && kb) base = atomicAdd(offsets + id, (uint32_t)__popc(kb));
+      base = __shfl_sync(kFull, base, 0);
+      if (keep) {
+        const double depth = key_rec_at(cam, o, ptx, pty);  // rasterizer.py:346-350
+        const uint32_t p = base + __popc(kb & lt_mask);
+        if ((int64_t)p < ecap) {
+          const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
+                               (depth_key(depth) >> (32 - depth_bits));
+          keys[p] = (key << id_bits) | (uint64_t)id;
+        }
+      }
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 
 void launch_init(const Frame& f, cudaStream_t s) {
@@ -795,16 +927,30 @@ void launch_init(const Frame& f, cudaStream_t s) {
   k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp);
 }
 
+// grid of the row-culling kernels: the list length is on the device, so a
+// fixed grid of warps strides over it (idle warps exit at once)
+static unsigned rows_blocks(const Frame& f) {
+  const int64_t b = (f.n + 255) / 256;
+  return (unsigned)(b < 148 * 8 ? b : 148 * 8);
+}
+
+static void launch_rows_count(const Frame& f, cudaStream_t s) {
+  if (f.cfg.exact)
+    k_rows_count<<<rows_blocks(f), 256, 0, s>>>(f.recs, f.rowlist, f.counters, f.cfg,
+                                                (f.gh + 31) / 32, f.counts);
+}
+
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                       f.exact_only ? nullptr : f.recs32, f.masks,
-                                                      f.counts, f.state, f.counters);
+                                                      f.rowlist, f.counts, f.state, f.counters);
 #if STP_SPLIT_SH
   k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs,
                                            f.exact_only ? nullptr : f.recs32);
 #endif
+  launch_rows_count(f, s);
 }
 
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
@@ -812,7 +958,8 @@ void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_ingest<<<(unsigned)blocks, kPreThreads, 0, s>>>(b, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                   f.exact_only ? nullptr : f.recs32, f.masks,
-                                                  f.counts, f.state, f.counters);
+                                                  f.rowlist, f.counts, f.state, f.counters);
+  launch_rows_count(f, s);
 }
 
 void launch_scan(const Frame& f, cudaStream_t s) {
@@ -830,6 +977,10 @@ void launch_duplicate(const Frame& f, cudaStream_t s) {
                                                      f.cam,
                                                      f.cfg, f.gw, f.depth_bits, f.id_bits, f.ecap,
                                                      f.keys[0]);
+  if (f.cfg.exact)
+    k_rows_dup<<<rows_blocks(f), 256, 0, s>>>(f.recs, f.rowlist, f.counters, f.offsets, f.cam,
+                                              f.cfg, (f.gh + 31) / 32, f.gw, f.depth_bits, f.id_bits, f.ecap,
+                                              f.keys[0]);
 }
 
 }  // namespace stp

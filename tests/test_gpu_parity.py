@@ -229,3 +229,17 @@ def test_oracle_parity_c4_law_4k():
     out, ref = _oracle_compare(arrs, cam, RenderConfig(with_depth=True), Hierarchical(),
                                records=False)
     assert out.stats["tiles"] > 8192
+
+
+def test_oracle_parity_elongated_rows():
+    """30% long thin splats at random orientations (rects far over 64 tiles):
+    K1/K3 cull those rects row by row (row_span superset, then the exact
+    per-tile test); tile lists and order must still equal the oracle's."""
+    from paper_2402_00525_b200 import Camera, Hierarchical, RenderConfig, scenes
+    arrs = scenes.to_f32_scene(scenes.frustum_cloud(20_000, 11, 1280, 720, 900.0, z_lo=1.5,
+                                                    z_hi=5.0, elongated_frac=0.3))
+    cam = Camera(rotation=np.eye(3), position=np.zeros(3), fx=900.0, fy=900.0, width=1280,
+                 height=720)
+    out, ref = _oracle_compare(arrs, cam, RenderConfig(with_depth=True), Hierarchical(),
+                               records=False)
+    assert out.stats["bin_entries"] > 100_000
