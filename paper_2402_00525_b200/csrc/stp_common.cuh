@@ -29,7 +29,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // The first 128-B line holds everything the pixel stage reads for one
 // emitted entry (alpha, t_opt, colour), so each evaluation touches one line;
 // the second holds the culling-only fields.
-struct __align__(16) SplatRec {
+struct __align__(32) SplatRec {
   double mx, my;        // mean2d (pixels)                                   0
   double ca, cb;        // conic a, b                                        16
   double cc, q2;        // conic c; q'_z                                     32
@@ -43,6 +43,13 @@ struct __align__(16) SplatRec {
   int16_t rx0, rx1, ry0, ry1;  // coarse tile rect, inclusive (rasterizer.py:307-321)  152
 };
 static_assert(sizeof(SplatRec) == 160, "SplatRec must be 160 B");
+
+// 256-bit read-only load (sm_100: LDG.E.256), 32-B aligned
+__device__ __forceinline__ void ld256(const void* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p));
+}
 
 // Camera-space record of the K6 fast path (128 B, one cache line), written
 // by K1 next to SplatRec.  With the camera ray v = ((x-cx)/fx, (y-cy)/fy, 1),

@@ -314,7 +314,6 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     uint32_t* __restrict__ rowlist, uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
-  const int lane = threadIdx.x & 31;
   const bool valid = i < sc.n;
   int reason = 4;  // 0 kept, 1 behind, 2 guard, 3 degenerate, 4 out of range
   SplatGeo g;

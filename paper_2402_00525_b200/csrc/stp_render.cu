@@ -186,19 +186,17 @@ __device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, u
 __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A, uint32_t id,
                                              const double* tab, double& t, double& al) {
   const SplatRec* r = A.recs + id;
-  const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
-  const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));  // cc q2
-  const float op = __ldg(&r->op);
-  const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
-  const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
-  const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
-  const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
-  const double q2 = ct.y;
-  const double dx = P.px - mxy.x, dy = P.py - mxy.y;
-  const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
-  const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
-  t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
+  // the record's first 128-B line in four 256-bit loads
+  double mx, my, a, b, c, q2, m0, m1, m2, m3, m4, m5, q0, q1, opc, c12;
+  ld256(&r->mx, mx, my, a, b);
+  ld256(&r->cc, c, q2, m0, m1);
+  ld256(&r->m[2], m2, m3, m4, m5);
+  ld256(&r->q0, q0, q1, opc, c12);
+  const float op = __int_as_float(__double2loint(opc));
+  const double dx = P.px - mx, dy = P.py - my;
+  const double pw = gpower(a, b, c, dx, dy);
+  const double mm[6] = {m0, m1, m2, m3, m4, m5};
+  t = key_rec(mm, q0, q1, q2, P.u, P.w, P.vn);
   const double pc = min_le(pw, 700.0);
   al = (double)op * exp_neg_nb(pc, tab);
   const bool pass = al >= A.cfg.eps;  // hierarchy.py:99-101
@@ -534,18 +532,23 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
         if (e < c) {
           const uint32_t sid = tip[e];
           const SplatRec* r = A.recs + sid;
+          // the record in 256-bit loads: everything but colour
+          double mx, my, a, b, c, q2, m[6], q0, q1, x0, x1, ia, ic, x2, x3;
+          ld256(&r->mx, mx, my, a, b);
+          ld256(&r->cc, c, q2, m[0], m[1]);
+          ld256(&r->m[2], m[2], m[3], m[4], m[5]);
+          ld256(&r->q0, q0, q1, x0, x1);
           double ptx, pty;
           if (A.cfg.mid_center) {
             ptx = r2x + 1.0;
             pty = r2y + 1.0;
           } else {
-            const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
-            const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-            const double cc = __ldg(&r->cc);
-            const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
-            max_point(mxy.x, mxy.y, ab.x, ab.y, cc, inv.x, inv.y, r2x, r2y, 2.0, 0.5, ptx, pty);
+            ld256(&r->inv_a, ia, ic, x2, x3);
+            max_point(mx, my, a, b, c, ia, ic, r2x, r2y, 2.0, 0.5, ptx, pty);
           }
-          const double dv = key_rec_at(A.cam, *r, ptx, pty);
+          double cu, cw, cv;
+          cam_ray(A.cam, ptx, pty, cu, cw, cv);
+          const double dv = key_rec(m, q0, q1, q2, cu, cw, cv);
           if (u) {
             gd[1] = dv;
             gi[1] = sid;
