@@ -766,10 +766,13 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
         if (j < k_total) {
           const uint32_t sid = A.vals[start + j];
           const SplatRec* r = A.recs + sid;
-          const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
-          const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-          const double2 ct = make_double2(__ldg(&r->cc), __ldg(&r->thr));
-          const double2 inv = __ldg(reinterpret_cast<const double2*>(&r->inv_a));
+          double mx, my, a, b, ia, ic, thr, rect;
+          ld256(&r->mx, mx, my, a, b);
+          ld256(&r->inv_a, ia, ic, thr, rect);
+          const double2 mxy = make_double2(mx, my);
+          const double2 ab = make_double2(a, b);
+          const double2 ct = make_double2(__ldg(&r->cc), thr);
+          const double2 inv = make_double2(ia, ic);
           const float op = __ldg(&r->op);
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
