@@ -69,14 +69,17 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t E = n_entries(counters, ecap);
+  const uint32_t epoch = (uint32_t)counters[C_EPOCH];
+  // persistent: partitions are claimed in increasing order (so the look-back
+  // predecessor is always held by a running block) until the entries run out
+  for (;;) {
   if (tid == 0) sm.part = (uint32_t)atomicAdd(part_counter, 1ull);
   for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
   __syncthreads();
   const uint32_t part = sm.part;
-  const int64_t E = n_entries(counters, ecap);
   const int64_t base = (int64_t)part * kSortTile;
   if (base >= E) return;
-  const uint32_t epoch = (uint32_t)counters[C_EPOCH];
   const int n_valid = (int)min((int64_t)kSortTile, E - base);
 
   // warp-striped load: warp w owns [base + w*512, +512), item k of lane l at k*32 + l
@@ -174,6 +177,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint32_t d = (uint32_t)(k >> shift) & 0xff;
     const uint32_t o = sm.global_off[d] + (uint32_t)i - sm.local_off[d];
     kout[o] = k;
+  }
+  __syncthreads();
   }
 }
 
@@ -310,17 +315,27 @@ __global__ void __launch_bounds__(256) k_ties(const uint64_t* __restrict__ keys,
 
 int launch_sort(const Frame& f, cudaStream_t s) {
   static bool attr_set = false;
+  static int sweep_grid = 0;
   if (!attr_set) {
     cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(SortSmem));
+    int per_sm = 0, dev = 0, n_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep, kSortThreads,
+                                                  sizeof(SortSmem));
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    sweep_grid = max(1, per_sm) * n_sm;
     attr_set = true;
   }
+  // one resident wave of persistent blocks (the entry count is only known
+  // on the device; a grid sized by the capacity would launch mostly idle blocks)
+  const int sweep_blocks = min(f.partitions, sweep_grid);
   const int hist_blocks = 148 * 4;
   k_sort_hist<<<hist_blocks, kSortThreads, 0, s>>>(f.keys[0], f.counters, f.ecap, f.passes,
                                                     f.id_bits, f.hist);
   int cur = 0;
   for (int p = 0; p < f.passes; ++p) {
-    k_onesweep<<<f.partitions, kSortThreads, sizeof(SortSmem), s>>>(
+    k_onesweep<<<sweep_blocks, kSortThreads, sizeof(SortSmem), s>>>(
         f.keys[cur], f.keys[cur ^ 1], f.counters, f.ecap, f.id_bits + 8 * p,
         f.hist + p * kRadix, f.lookback + (size_t)p * f.partitions * kRadix,
         f.counters + C_PART + p);
