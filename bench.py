@@ -392,8 +392,8 @@ def run_ours(args):
     e2e_value = world * e2e_steps / (float(e2e_ms.item()) / 1e3)
 
     # K0, K1 + row count, 3 x K2, K3 + row duplicate, K4 histogram + passes,
-    # K5 (ranges + ties), K6 (fast + list pass)
-    launches_per_view = (1 + 2 + 3 + 2 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 2 +
+    # K5 (ranges with the tie fix-up), K6 (fast + list pass)
+    launches_per_view = (1 + 2 + 3 + 2 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 1 +
                          (2 if args.fast32 else 1))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,

@@ -9,8 +9,7 @@
 // K5: tile ranges (rasterizer.py:358-372) and the float64 tie fix-up: runs of
 //     equal (truncated) keys inside a tile are re-ordered by the float64 depth
 //     and then rank, so the final order equals the reference's float64
-//     lexsort (k_ranges computes the run members' depths in parallel, k_ties
-//     sorts each run).
+//     lexsort (one kernel: a run's first entry sorts the run).
 #include "stp_common.cuh"
 
 namespace stp {
@@ -216,6 +215,13 @@ __device__ __forceinline__ int block_sum(int v) {
 // Grid-stride over the sorted entries; per-block counts are reduced in
 // registers / shared memory and added with one atomic per block (a per-entry
 // or per-warp atomic on one counter serialises tens of thousands of updates).
+// Each entry writes its Gaussian id and the tile bounds it starts / ends.  A
+// run of equal sort keys (same tile, same truncated depth) is re-ordered by
+// (float64 depth, rank) -- np.lexsort's order -- by the thread of its first
+// member: it computes the members' depths, insertion-sorts them (runs are
+// short; the stable LSD sort delivered them in rank order) and writes their
+// ids; the other members write nothing.  Runs over kTieLocal go through the
+// free ping-pong buffer d64.
 __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys,
                                                 uint32_t* __restrict__ vals,
                                                 unsigned long long* counters, int64_t ecap,
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
                                                 double* __restrict__ d64) {
   const int64_t E = n_entries(counters, ecap);
   const uint64_t id_mask = (1ull << id_bits) - 1ull;
-  int heads = 0;
+  int heads = 0, runs = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t w = keys[i];
@@ -234,71 +240,47 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
     const uint64_t kp = (i > 0) ? keys[i - 1] >> id_bits : ~k;
     const uint64_t kn = (i + 1 < E) ? keys[i + 1] >> id_bits : ~k;
     const uint32_t id = (uint32_t)(w & id_mask);
-    vals[i] = id;
     if (i == 0 || (uint32_t)(kp >> depth_bits) != tile) {
       ranges[tile].x = (uint32_t)i;
       ++heads;
     }
     if (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile) ranges[tile].y = (uint32_t)(i + 1);
-    // members of a run of equal keys (same tile, same truncated depth key):
-    // their float64 depths, computed in parallel, go to the free ping-pong
-    // buffer for k_ties
-    if (kn == k || (i > 0 && kp == k)) d64[i] = entry_depth64(recs, cam, id, (int)tile, gw);
-  }
-  const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
-  if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
-}
-
-// K5b: each run of equal keys is re-ordered by (float64 depth, rank); the
-// depths were computed by k_ranges.
-__global__ void __launch_bounds__(256) k_ties(const uint64_t* __restrict__ keys,
-                                              uint32_t* __restrict__ vals,
-                                              double* __restrict__ d64,
-                                              unsigned long long* counters, int64_t ecap,
-                                              int id_bits) {
-  const int64_t E = n_entries(counters, ecap);
-  int runs = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i] >> id_bits;
-    if (!((i + 1 < E && (keys[i + 1] >> id_bits) == k) &&
-          (i == 0 || (keys[i - 1] >> id_bits) != k)))
+    const bool first = i == 0 || kp != k;
+    if (kn != k) {
+      if (first) vals[i] = id;  // not in a run
       continue;
+    }
+    if (!first) continue;       // run member: written by the run's first entry
     ++runs;
     int64_t L = 2;
     while (i + L < E && (keys[i + L] >> id_bits) == k) ++L;
     if (L <= kTieLocal) {
       double d[kTieLocal];
-      uint32_t id[kTieLocal];
+      uint32_t ids[kTieLocal];
       for (int m = 0; m < L; ++m) {
-        id[m] = vals[i + m];
-        d[m] = d64[i + m];
-      }
-      // insertion sort by (depth, rank); members arrive in rank order
-      for (int m = 1; m < L; ++m) {
-        const double dv = d[m];
-        const uint32_t iv = id[m];
+        const uint32_t im = (uint32_t)(keys[i + m] & id_mask);
+        const double dv = entry_depth64(recs, cam, im, (int)tile, gw);
+        // insertion by (depth, rank); members arrive in rank order
         int p = m - 1;
-        while (p >= 0 && (d[p] > dv || (d[p] == dv && id[p] > iv))) {
+        while (p >= 0 && d[p] > dv) {
           d[p + 1] = d[p];
-          id[p + 1] = id[p];
+          ids[p + 1] = ids[p];
           --p;
         }
         d[p + 1] = dv;
-        id[p + 1] = iv;
+        ids[p + 1] = im;
       }
-      for (int m = 0; m < L; ++m) vals[i + m] = id[m];
+      for (int m = 0; m < L; ++m) vals[i + m] = ids[m];
     } else {
-      // long runs (coincident splats): in-place insertion sort through memory
-      for (int64_t m = 1; m < L; ++m) {
-        const uint32_t iv = vals[i + m];
-        const double dv = d64[i + m];
+      // long runs (coincident splats): insertion sort through memory
+      for (int64_t m = 0; m < L; ++m) {
+        const uint32_t iv = (uint32_t)(keys[i + m] & id_mask);
+        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw);
         int64_t p = m - 1;
         while (p >= 0) {
-          const uint32_t ip = vals[i + p];
           const double dp = d64[i + p];
-          if (!(dp > dv || (dp == dv && ip > iv))) break;
-          vals[i + p + 1] = ip;
+          if (!(dp > dv)) break;
+          vals[i + p + 1] = vals[i + p];
           d64[i + p + 1] = dp;
           --p;
         }
@@ -307,6 +289,8 @@ __global__ void __launch_bounds__(256) k_ties(const uint64_t* __restrict__ keys,
       }
     }
   }
+  const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
+  if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
   const int nr = __syncthreads_count(runs > 0) ? block_sum(runs) : 0;
   if (threadIdx.x == 0 && nr) atomicAdd(counters + C_TIES, (unsigned long long)nr);
 }
@@ -351,8 +335,6 @@ void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
   double* d64 = reinterpret_cast<double*>(f.keys[buf ^ 1]);
   k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, f.counters, f.ecap, f.ranges,
                                             f.recs, f.cam, f.gw, f.depth_bits, f.id_bits, d64);
-  k_ties<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, d64, f.counters, f.ecap,
-                                          f.id_bits);
 }
 
 }  // namespace stp
