@@ -844,45 +844,66 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           vS0 = lane < nkA;
           vS1 = lane < nkB;
         }
-        // ---- merge each sorted batch into its tail (heap_merge, :201)
-#pragma unroll 1
-        for (int s = 0; s < 2; ++s) {
-          const int nks = s ? nkB : nkA;
-          if (nks == 0) continue;
-          const double ds = s ? dS1 : dS0;
-          const uint32_t is = s ? iS1 : iS0;
-          const int xs = s ? xS1 : xS0;
-          const bool vs = s ? vS1 : vS0;
-          const SubQ Q = subq(s);
-          const int cur = s ? cur1 : cur0, th = s ? th1 : th0, nt = s ? nt1 : nt0;
-          if (vs) {
-            Q.bd()[xs] = ds;
-            Q.bi()[xs] = is;
+        // ---- merge each sorted batch into its tail (heap_merge, :201), both
+        // sub-tiles in the same instructions: every lane ranks its new
+        // element(s) in its sub-tile's tail and the tails' elements in their
+        // batches (lane-selected queues; sub-tiles without kept entries keep
+        // their buffers).
+        {
+          const bool cpt = nkA <= 16 && nkB <= 16;
+          // pass 1: element (s1, d1) of this lane -- the compact path's half
+          // h, else sub-tile 0; pass 2 (non-compact only): sub-tile 1
+          const int s1 = cpt ? (lane >> 4) : 0;
+          const bool v1 = s1 ? vS1 : vS0;
+          const double d1 = s1 ? dS1 : dS0;
+          const uint32_t i1 = s1 ? iS1 : iS0;
+          const int x1 = s1 ? xS1 : xS0;
+          const SubQ Q1 = subq(s1);
+          if (v1) {
+            Q1.bd()[x1] = d1;
+            Q1.bi()[x1] = i1;
+          }
+          if (!cpt && vS1) {
+            const SubQ Q = subq(1);
+            Q.bd()[xS1] = dS1;
+            Q.bi()[xS1] = iS1;
           }
           __syncwarp();
-          const double* td = Q.td(cur) + th;
-          const uint32_t* ti = Q.ti(cur) + th;
-          double* od = Q.td(cur ^ 1);
-          uint32_t* oi = Q.ti(cur ^ 1);
-          if (vs) {
-            const int rk = count_below(td, ti, nt, ds, is);
-            od[xs + rk] = ds;
-            oi[xs + rk] = is;
+          if (v1) {
+            const int cur = s1 ? cur1 : cur0, th = s1 ? th1 : th0, nt = s1 ? nt1 : nt0;
+            const int rk = count_below(Q1.td(cur) + th, Q1.ti(cur) + th, nt, d1, i1);
+            Q1.td(cur ^ 1)[x1 + rk] = d1;
+            Q1.ti(cur ^ 1)[x1 + rk] = i1;
           }
-          for (int t = lane; t < nt; t += 32) {
-            const int rk = count_below(Q.bd(), Q.bi(), nks, td[t], ti[t]);
-            od[t + rk] = td[t];
-            oi[t + rk] = ti[t];
+          if (!cpt && vS1) {
+            const SubQ Q = subq(1);
+            const int rk = count_below(Q.td(cur1) + th1, Q.ti(cur1) + th1, nt1, dS1, iS1);
+            Q.td(cur1 ^ 1)[xS1 + rk] = dS1;
+            Q.ti(cur1 ^ 1)[xS1 + rk] = iS1;
+          }
+          // the tails' elements, both sub-tiles in one index space
+          const int n0 = nkA ? nt0 : 0, n1 = nkB ? nt1 : 0;
+          for (int u = lane; u < n0 + n1; u += 32) {
+            const int st = u >= n0;
+            const int t = u - (st ? n0 : 0);
+            const SubQ Q = subq(st);
+            const int cur = st ? cur1 : cur0, th = st ? th1 : th0;
+            const double tv = Q.td(cur)[th + t];
+            const uint32_t tiv = Q.ti(cur)[th + t];
+            const int rk = count_below(Q.bd(), Q.bi(), st ? nkB : nkA, tv, tiv);
+            Q.td(cur ^ 1)[t + rk] = tv;
+            Q.ti(cur ^ 1)[t + rk] = tiv;
           }
           __syncwarp();
-          if (s) {
-            cur1 ^= 1;
-            th1 = 0;
-            nt1 += nks;
-          } else {
+          if (nkA) {
             cur0 ^= 1;
             th0 = 0;
-            nt0 += nks;
+            nt0 += nkA;
+          }
+          if (nkB) {
+            cur1 ^= 1;
+            th1 = 0;
+            nt1 += nkB;
           }
         }
         PROF_ADD(1);
