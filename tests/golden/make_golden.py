@@ -77,10 +77,13 @@ def save(name, arrs, cam, mode, cfg, sh_coeffs=16, rec_pixels=None, store_batch=
                  guard_band=cfg.guard_band, dilation=cfg.dilation,
                  inv_scale_clamp=cfg.inv_scale_clamp, with_depth=cfg.with_depth,
                  exact_tile_culling=cfg.exact_tile_culling)
-    mode_d = dict(queue_tail=mode.queue_tail, queue_mid=mode.queue_mid,
-                  queue_head=mode.queue_head, batch_load=mode.batch_load,
-                  batch_mid=mode.batch_mid, batch_head=mode.batch_head,
-                  mid_depth_at_center=mode.mid_depth_at_center)
+    if isinstance(mode, S.GlobalZ):
+        mode_d = dict(mode="globalz")
+    else:
+        mode_d = dict(queue_tail=mode.queue_tail, queue_mid=mode.queue_mid,
+                      queue_head=mode.queue_head, batch_load=mode.batch_load,
+                      batch_mid=mode.batch_mid, batch_head=mode.batch_head,
+                      mid_depth_at_center=mode.mid_depth_at_center)
     cfg_rec = S.RenderConfig(**{**cfg_d, "capture_records": True})
     t0 = time.time()
     frame = S.render(gs, cam, mode, cfg_rec)
@@ -215,6 +218,24 @@ def main(only=None):
         save("c1", sc, cams[0], H, S.RenderConfig(with_depth=True), sh_coeffs=1,
              rec_pixels=pix, store_batch=False)
     jobs["c1"] = c1
+
+    # 9. GlobalZ (the 3DGS baseline order: one view-z key per splat, coarse
+    #    bins by default) on the same scenes, plus GlobalZ with exact culling
+    def globalz():
+        G = S.GlobalZ()
+        gs, cams, _ = random_cloud(300, seed=5)
+        save("gz_cloud300", from_gaussians(gs), cams[0], G,
+             S.RenderConfig(with_depth=True, background=np.array([0.1, 0.2, 0.3])))
+        arrs = scenes.frustum_cloud(1500, 21, 203, 117, 150.0, z_lo=1.0, z_hi=5.0)
+        arrs["scales"] = arrs["scales"] * 4.0
+        pos = np.array([0.1, -0.05, -0.2])
+        R = scenes.look_at(pos, np.array([0.15, 0.0, 3.0]))
+        cam = axis_cam(203, 117, f=150.0, R=R, pos=pos, cx=97.3, cy=61.9)
+        save("gz_sh3_border", scenes.to_f32_scene(arrs), cam, G, S.RenderConfig(with_depth=True))
+        gs, cams, _ = random_cloud(200, seed=11)
+        save("gz_exact", from_gaussians(gs), cams[0], G,
+             S.RenderConfig(with_depth=True, exact_tile_culling=True))
+    jobs["globalz"] = globalz
 
     for name, fn in jobs.items():
         if only and name not in only:

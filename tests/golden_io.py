@@ -9,7 +9,7 @@ import os
 
 import numpy as np
 
-from paper_2402_00525_b200.types import Camera, Hierarchical, RenderConfig
+from paper_2402_00525_b200.types import Camera, GlobalZ, Hierarchical, RenderConfig
 
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -27,7 +27,8 @@ def load(name):
                  cx=cx, cy=cy)
     cfg_d = json.loads(str(d["cfg_json"]))
     cfg = RenderConfig(**cfg_d)
-    mode = Hierarchical(**json.loads(str(d["mode_json"])))
+    md = json.loads(str(d["mode_json"]))
+    mode = GlobalZ() if md.get("mode") == "globalz" else Hierarchical(**md)
     scene = {k: d[k] for k in ("means", "quats", "scales", "opacity", "sh")}
     return scene, cam, cfg, mode, d
 
