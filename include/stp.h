@@ -66,6 +66,8 @@ typedef struct {
   const double* inv_cov3;        /* [n,6] packed m00, m11, m22, m01, m02, m12  */
   const double* inv_cov_center;  /* [n,3]                                      */
   int64_t n;
+  const double* global_depth;    /* [n] view z (GlobalZ keys) or NULL           */
+  const double* center_dist;     /* [n] |mean - origin| (GlobalZ depth) or NULL */
 } StpSplatBatch;
 
 /* Pinhole camera (scene_io.py:84-129): world->view rotation, row-major. */
@@ -94,7 +96,15 @@ typedef struct {
   int32_t exact_culling;    /* exact 16x16 tile culling (default 1)        */
   int32_t record_cap;       /* per-pixel blend-record capacity, 0 = off    */
   int32_t flags;            /* STP_FLAG_*                                  */
+  int32_t sort_mode;        /* STP_MODE_* (rasterizer.py:89 SortMode)      */
 } StpConfig;
+
+/* Sort modes.  HIERARCHICAL: per-tile t_opt keys + the 3-level resort
+ * (hierarchy.py); GLOBALZ: one view-space z key per splat and the bin's
+ * order for every pixel (rasterizer.py:472-485, the 3DGS baseline; queue
+ * fields are ignored). */
+#define STP_MODE_HIERARCHICAL 0
+#define STP_MODE_GLOBALZ 1
 
 #define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
 #define STP_FLAG_FAST32 2   /* K6 through the fp32-state certified kernel
@@ -141,6 +151,7 @@ typedef struct {
   size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
       counters, hist, lookback, scan_scratch,
       rowlist, /* ids of kept Gaussians whose coarse rect exceeds 64 tiles */
+      aux,     /* [n] (view z, |mean - origin|) float64 pairs (GlobalZ)     */
       total;
   int64_t entry_capacity;
   int32_t n_tiles, grid_w, grid_h, sort_passes, sort_bits, partitions;

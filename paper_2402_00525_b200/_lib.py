@@ -16,6 +16,8 @@ STP_OK, STP_ERR_CONFIG, STP_ERR_DATA, STP_ERR_WORKSPACE_TOO_SMALL, STP_ERR_CUDA 
 STP_FLAG_TIMINGS = 1
 STP_FLAG_FAST32 = 2
 STP_FLAG_FB_TEST = 4
+STP_MODE_HIERARCHICAL = 0
+STP_MODE_GLOBALZ = 1
 
 EXPORTS = ("stp_abi_version", "stp_error_string", "stp_validate_config", "stp_workspace_bytes",
            "stp_workspace_layout", "stp_render", "stp_render_batch", "stp_render_views",
@@ -35,7 +37,8 @@ class StpSplatBatch(ctypes.Structure):
     _fields_ = [("mean2d", ctypes.c_void_p), ("conic", ctypes.c_void_p),
                 ("color", ctypes.c_void_p), ("opacity", ctypes.c_void_p),
                 ("radius", ctypes.c_void_p), ("inv_cov3", ctypes.c_void_p),
-                ("inv_cov_center", ctypes.c_void_p), ("n", ctypes.c_int64)]
+                ("inv_cov_center", ctypes.c_void_p), ("n", ctypes.c_int64),
+                ("global_depth", ctypes.c_void_p), ("center_dist", ctypes.c_void_p)]
 
 
 class StpCamera(ctypes.Structure):
@@ -54,7 +57,8 @@ class StpConfig(ctypes.Structure):
                 ("b_load", ctypes.c_int32), ("b_mid", ctypes.c_int32),
                 ("b_head", ctypes.c_int32), ("mid_depth_at_center", ctypes.c_int32),
                 ("with_depth", ctypes.c_int32), ("exact_culling", ctypes.c_int32),
-                ("record_cap", ctypes.c_int32), ("flags", ctypes.c_int32)]
+                ("record_cap", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("sort_mode", ctypes.c_int32)]
 
 
 class StpOutputs(ctypes.Structure):
@@ -79,7 +83,7 @@ class StpStats(ctypes.Structure):
 class StpLayout(ctypes.Structure):
     _fields_ = [(n, ctypes.c_size_t) for n in (
         "recs", "recs32", "fb_items", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals", "ranges",
-        "counters", "hist", "lookback", "scan_scratch", "rowlist", "total")] + [
+        "counters", "hist", "lookback", "scan_scratch", "rowlist", "aux", "total")] + [
         ("entry_capacity", ctypes.c_int64), ("n_tiles", ctypes.c_int32),
         ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32),
         ("sort_passes", ctypes.c_int32), ("sort_bits", ctypes.c_int32),

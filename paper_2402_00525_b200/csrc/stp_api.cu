@@ -65,6 +65,7 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.counts = o;       o = align_up(o + (size_t)n * 4);
   L.offsets = o;      o = align_up(o + (size_t)n * 4);
   L.rowlist = o;      o = align_up(o + (size_t)n * 4);
+  L.aux = o;          o = align_up(o + (size_t)n * 16);
   L.lookback = o;     o = align_up(o + (size_t)L.sort_passes * L.partitions * 256 * 8);
   L.keys0 = o;        o = align_up(o + (size_t)ecap * 8);
   L.keys1 = o;        o = align_up(o + (size_t)ecap * 8);
@@ -102,6 +103,11 @@ const char* kErrors[] = {"ok", "invalid configuration", "data error",
 int cfg_check(const StpConfig* c) {
   if (!c) return STP_ERR_CONFIG;
   if (c->tile_size != 16) return STP_ERR_CONFIG;
+  if (c->sort_mode != STP_MODE_HIERARCHICAL && c->sort_mode != STP_MODE_GLOBALZ)
+    return STP_ERR_CONFIG;
+  if (!(c->alpha_cap > 0.0 && c->alpha_cap < 1.0)) return STP_ERR_CONFIG;
+  if (c->record_cap < 0) return STP_ERR_CONFIG;
+  if (c->sort_mode == STP_MODE_GLOBALZ) return STP_OK;  // no queues
   // validate_mode (rasterizer.py:98-115)
   if (c->q_tail < 64 || c->q_tail % 32 != 0) return STP_ERR_CONFIG;
   if (c->q_mid < 4 || c->q_mid % 4 != 0) return STP_ERR_CONFIG;
@@ -130,7 +136,9 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.camp = reinterpret_cast<DevCam*>(b + L.camera);
   f.masks = reinterpret_cast<uint64_t*>(b + L.masks);
   f.rowlist = reinterpret_cast<uint32_t*>(b + L.rowlist);
-  f.exact_only = (cfg->flags & STP_FLAG_FAST32) ? 0 : 1;
+  f.aux = reinterpret_cast<double2*>(b + L.aux);
+  f.globalz = cfg->sort_mode == STP_MODE_GLOBALZ ? 1 : 0;
+  f.exact_only = ((cfg->flags & STP_FLAG_FAST32) && !f.globalz) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);
@@ -190,7 +198,8 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   StpLayout L;
   if (!carve_frame(batch ? batch->n : sc->n, cam, cfg, ws, ws_bytes, f, L))
     return STP_ERR_WORKSPACE_TOO_SMALL;
-  if ((size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024) return STP_ERR_CONFIG;
+  if (!f.globalz && (size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024)
+    return STP_ERR_CONFIG;
   cudaEvent_t own[5];
   if (ms && !ev) {
     for (int i = 0; i < 5; ++i) cudaEventCreate(&own[i]);

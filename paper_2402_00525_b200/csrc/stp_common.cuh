@@ -459,6 +459,8 @@ struct Frame {
   SplatRec32* recs32;
   uint64_t* masks;        // per Gaussian: surviving tiles of a <= 64-tile coarse rect
   uint32_t* rowlist;      // ids of kept Gaussians with a > 64-tile rect (C_ROWS of them)
+  double2* aux;           // per Gaussian (view z, |mean - origin|), GlobalZ only
+  int globalz;            // sort mode GlobalZ (view-z keys, ordered blend)
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;

@@ -311,7 +311,8 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
 __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ rowlist, uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    uint32_t* __restrict__ rowlist, double2* __restrict__ aux, uint32_t* __restrict__ counts,
+    uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const bool valid = i < sc.n;
@@ -487,6 +488,8 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           r.ry0 = (int16_t)y0;
           r.ry1 = (int16_t)y1;
           recs[i] = r;
+          // GlobalZ: view z and |mean - origin| (gaussian_math.py:421-430)
+          if (aux) aux[i] = make_double2(z, sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2));
           if (recs32) {
             // camera-space record (see SplatRec32): M' = W inv3 W^T, q' = M' p_view
             SplatRec32 f;
@@ -565,7 +568,8 @@ __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
 __global__ void __launch_bounds__(kPreThreads) k_ingest(
     StpSplatBatch b, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
     SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
-    uint32_t* __restrict__ rowlist, uint32_t* __restrict__ counts, uint8_t* __restrict__ state,
+    uint32_t* __restrict__ rowlist, double2* __restrict__ aux, uint32_t* __restrict__ counts,
+    uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   const bool valid = i < b.n;
@@ -623,6 +627,9 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     r.ry0 = (int16_t)y0;
     r.ry1 = (int16_t)y1;
     recs[i] = r;
+    if (aux)
+      aux[i] = make_double2(b.global_depth ? b.global_depth[i] : 0.0,
+                            b.center_dist ? b.center_dist[i] : 0.0);
     if (recs32) {
       SplatRec32 f;
       f.mx = r.mx;
@@ -752,7 +759,8 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec* __restrict__ recs, const uint64_t* __restrict__ masks,
     const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, int64_t n, DevCam cam, DevCfg cfg, int gw,
-    int depth_bits, int id_bits, int64_t ecap, uint64_t* __restrict__ keys) {
+    int depth_bits, int id_bits, int64_t ecap, const double2* __restrict__ aux,
+    uint64_t* __restrict__ keys) {
   __shared__ uint32_t s_pos[kPreThreads];
   __shared__ unsigned long long s_m[kPreThreads];
   const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
@@ -785,8 +793,9 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
         const int b = select_bit64(s_m[wbase + owner], local);
         tx = r.rx0 + b % w;
         ty = r.ry0 + b / w;
-        max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
-                  (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
+        if (!aux)  // the peak only feeds the t_opt key
+          max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
+                    (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
         keep = true;
       } else {
         tx = r.rx0 + local % w;
@@ -802,7 +811,9 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const uint32_t base = v ? s_pos[wbase + owner] : 0;
     __syncwarp();
     if (keep) {
-      const double depth = key_rec_at(cam, r, ptx, pty);  // rasterizer.py:346-350
+      // rasterizer.py:343-350: view z (GlobalZ) or t_opt at the 16x16 peak
+      const double depth = aux ? aux[(int64_t)blockIdx.x * kPreThreads + wbase + owner].x
+                               : key_rec_at(cam, r, ptx, pty);
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
         const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
@@ -886,6 +897,7 @@ __global__ void __launch_bounds__(256) k_rows_dup(const SplatRec* __restrict__ r
                                                   uint32_t* __restrict__ offsets, DevCam cam,
                                                   DevCfg cfg, int cpg, int gw, int depth_bits,
                                                   int id_bits, int64_t ecap,
+                                                  const double2* __restrict__ aux,
                                                   uint64_t* __restrict__ keys) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1;
@@ -904,7 +916,7 @@ __global__ void __launch_bounds__(256) k_rows_dup(const SplatRec* __restrict__ r
       if (lane == 0 && kb) base = atomicAdd(offsets + id, (uint32_t)__popc(kb));
       base = __shfl_sync(kFull, base, 0);
       if (keep) {
-        const double depth = key_rec_at(cam, o, ptx, pty);  // rasterizer.py:346-350
+        const double depth = aux ? aux[id].x : key_rec_at(cam, o, ptx, pty);  // :343-350
         const uint32_t p = base + __popc(kb & lt_mask);
         if ((int64_t)p < ecap) {
           const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
@@ -944,7 +956,8 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                       f.exact_only ? nullptr : f.recs32, f.masks,
-                                                      f.rowlist, f.counts, f.state, f.counters);
+                                                      f.rowlist, f.globalz ? f.aux : nullptr,
+                                                      f.counts, f.state, f.counters);
 #if STP_SPLIT_SH
   k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs,
                                            f.exact_only ? nullptr : f.recs32);
@@ -957,7 +970,8 @@ void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_ingest<<<(unsigned)blocks, kPreThreads, 0, s>>>(b, f.cam, f.cfg, f.gw, f.gh, f.recs,
                                                   f.exact_only ? nullptr : f.recs32, f.masks,
-                                                  f.rowlist, f.counts, f.state, f.counters);
+                                                  f.rowlist, f.globalz ? f.aux : nullptr,
+                                                  f.counts, f.state, f.counters);
   launch_rows_count(f, s);
 }
 
@@ -975,11 +989,11 @@ void launch_duplicate(const Frame& f, cudaStream_t s) {
   k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
                                                      f.cam,
                                                      f.cfg, f.gw, f.depth_bits, f.id_bits, f.ecap,
-                                                     f.keys[0]);
+                                                     f.globalz ? f.aux : nullptr, f.keys[0]);
   if (f.cfg.exact)
     k_rows_dup<<<rows_blocks(f), 256, 0, s>>>(f.recs, f.rowlist, f.counters, f.offsets, f.cam,
                                               f.cfg, (f.gh + 31) / 32, f.gw, f.depth_bits, f.id_bits, f.ecap,
-                                              f.keys[0]);
+                                              f.globalz ? f.aux : nullptr, f.keys[0]);
 }
 
 }  // namespace stp

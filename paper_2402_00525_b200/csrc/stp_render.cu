@@ -975,12 +975,135 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   if (grid > 0) k_render<QH, EXACT, QMX, QT><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
+// ---------------------------------------------------------------------------
+// K6 under GlobalZ (rasterizer.py:472-485): every pixel blends the bin in its
+// sorted (view z, rank) order -- the 3DGS baseline the paper compares with.
+// _TileCtx.alphas (:412-422: alpha capped, zeroed below eps) and
+// _blend_ordered (:432-459: T_k = prod(1 - alpha_i), an entry blends while the
+// T before it is >= termination, final T = the first value below); the depth
+// output blends the distance to the Gaussian's mean (:478-482).  One block of
+// 256 threads per 16x16 tile, one thread per pixel; the bin streams through
+// shared memory 256 entries at a time and the block stops when every pixel
+// has terminated.
+constexpr int kGzThreads = 256;
+
+struct GzArgs {
+  const SplatRec* __restrict__ recs;
+  const uint32_t* __restrict__ vals;
+  const uint2* __restrict__ ranges;
+  const double2* __restrict__ aux;  // (view z, |mean - origin|)
+  DevCam cam;
+  DevCfg cfg;
+  int gw, n_tiles;
+  StpOutputs out;
+  unsigned long long* counters;
+};
+
+__global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
+  __shared__ double s_tab[64];
+  __shared__ double s_mx[kGzThreads], s_my[kGzThreads], s_a[kGzThreads], s_b[kGzThreads],
+      s_c[kGzThreads], s_dist[kGzThreads];
+  __shared__ float4 s_oc[kGzThreads];  // opacity, colour
+  __shared__ uint32_t s_id[kGzThreads];
+  const int tid = threadIdx.x;
+  if (tid < 64) s_tab[tid] = kExp2Tab[tid];
+  for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+    const int tx = tile % A.gw, ty = tile / A.gw;
+    const int gx = tx * kTile + (tid & 15), gy = ty * kTile + (tid >> 4);
+    const bool in_img = gx < A.cam.W && gy < A.cam.H;
+    const int64_t pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
+    const double px = (double)gx + 0.5, py = (double)gy + 0.5;
+    double u = 0.0, w = 0.0, vn = 0.0;
+    if (A.cfg.rec_cap > 0) cam_ray(A.cam, px, py, u, w, vn);
+    double T = in_img ? 1.0 : 0.0;
+    float C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
+    int rc = 0;
+    const uint2 rg = A.ranges[tile];
+    for (uint32_t base = rg.x; base < rg.y; base += kGzThreads) {
+      // all pixels terminated: the rest of the bin blends nothing
+      if (__syncthreads_count(T >= A.cfg.term) == 0) break;
+      const uint32_t j = base + tid;
+      if (j < rg.y) {
+        const uint32_t id = A.vals[j];
+        const SplatRec* r = A.recs + id;
+        double mx, my, a, b;
+        ld256(&r->mx, mx, my, a, b);
+        s_mx[tid] = mx;
+        s_my[tid] = my;
+        s_a[tid] = a;
+        s_b[tid] = b;
+        s_c[tid] = __ldg(&r->cc);
+        s_oc[tid] = __ldg(reinterpret_cast<const float4*>(&r->op));
+        s_dist[tid] = A.aux[id].y;
+        s_id[tid] = id;
+      }
+      __syncthreads();
+      const int n = (int)min((uint32_t)kGzThreads, rg.y - base);
+      for (int k = 0; k < n && T >= A.cfg.term; ++k) {
+        const double dx = px - s_mx[k], dy = py - s_my[k];
+        const double pw = gpower(s_a[k], s_b[k], s_c[k], dx, dy);
+        const float4 oc = s_oc[k];
+        double al = (double)oc.x * exp_neg_nb(min_le(pw, 700.0), s_tab);
+        al = min_le(al, A.cfg.cap);
+        if (al < A.cfg.eps) continue;  // alpha 0: no weight, T unchanged
+        const double wt = al * T;
+        const float wf = (float)wt;
+        C0 += oc.y * wf;
+        C1 += oc.z * wf;
+        C2 += oc.w * wf;
+        D += (float)(s_dist[k] * wt);
+        if (A.cfg.rec_cap > 0) {
+          const SplatRec* r = A.recs + s_id[k];
+          const double t = key_rec(r->m, r->q0, r->q1, r->q2, u, w, vn);
+          write_record(A.out, A.cfg.rec_cap, pix, rc++, t, al, s_id[k]);
+        }
+        T = T * (1.0 - al);
+      }
+      __syncthreads();
+    }
+    if (pix >= 0) {
+      const float Tf = (float)T;
+      const float c0 = C0 + (float)(T * A.cfg.bg[0]);
+      const float c1 = C1 + (float)(T * A.cfg.bg[1]);
+      const float c2 = C2 + (float)(T * A.cfg.bg[2]);
+      A.out.color[pix * 3 + 0] = c0;
+      A.out.color[pix * 3 + 1] = c1;
+      A.out.color[pix * 3 + 2] = c2;
+      A.out.transmittance[pix] = Tf;
+      if (A.out.depth) A.out.depth[pix] = D;
+      if (A.cfg.rec_cap > 0) A.out.rec_count[pix] = rc;
+      if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(Tf)))
+        atomicAdd(A.counters + C_NONFINITE, 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStream_t s) {
+  GzArgs A;
+  A.recs = f.recs;
+  A.vals = f.vals;
+  A.ranges = f.ranges;
+  A.aux = f.aux;
+  A.cam = f.cam;
+  A.cfg = f.cfg;
+  A.gw = f.gw;
+  A.n_tiles = f.n_tiles;
+  A.out = out;
+  A.counters = f.counters;
+  if (f.n_tiles > 0) k_render_globalz<<<f.n_tiles, kGzThreads, 0, s>>>(A);
+}
+
 void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
 
 // K6: the float64 kernel over every (tile, pair) item; with STP_FLAG_FAST32
 // the fp32-state certified kernel first, then the float64 kernel over the
 // items it handed over (list mode).
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
+  if (f.globalz) {
+    launch_render_globalz(f, out, s);
+    return;
+  }
   if (!f.exact_only) launch_render_fast(f, buf, out, s);
   RenderArgs A;
   A.list = f.exact_only ? nullptr : f.fb_items;

@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
 // K5 tile ranges + float64 tie fix-up.
 
 __device__ __forceinline__ double entry_depth64(const SplatRec* __restrict__ recs, const DevCam& cam,
-                                                uint32_t id, int tile, int gw) {
+                                                uint32_t id, int tile, int gw,
+                                                const double2* __restrict__ aux) {
+  if (aux) return aux[id].x;  // GlobalZ: view z
   const SplatRec& r = recs[id];
   const int tx = tile % gw, ty = tile / gw;
   double ptx, pty;
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
                                                 uint2* __restrict__ ranges,
                                                 const SplatRec* __restrict__ recs, DevCam cam,
                                                 int gw, int depth_bits, int id_bits,
+                                                const double2* __restrict__ aux,
                                                 double* __restrict__ d64) {
   const int64_t E = n_entries(counters, ecap);
   const uint64_t id_mask = (1ull << id_bits) - 1ull;
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
       uint32_t ids[kTieLocal];
       for (int m = 0; m < L; ++m) {
         const uint32_t im = (uint32_t)(keys[i + m] & id_mask);
-        const double dv = entry_depth64(recs, cam, im, (int)tile, gw);
+        const double dv = entry_depth64(recs, cam, im, (int)tile, gw, aux);
         // insertion by (depth, rank); members arrive in rank order
         int p = m - 1;
         while (p >= 0 && d[p] > dv) {
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
       // long runs (coincident splats): insertion sort through memory
       for (int64_t m = 0; m < L; ++m) {
         const uint32_t iv = (uint32_t)(keys[i + m] & id_mask);
-        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw);
+        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw, aux);
         int64_t p = m - 1;
         while (p >= 0) {
           const double dp = d64[i + p];
@@ -334,7 +337,8 @@ void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
   // the other ping-pong key buffer (E x 8 B) is free: float64 depths of tie runs
   double* d64 = reinterpret_cast<double*>(f.keys[buf ^ 1]);
   k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, f.counters, f.ecap, f.ranges,
-                                            f.recs, f.cam, f.gw, f.depth_bits, f.id_bits, d64);
+                                            f.recs, f.cam, f.gw, f.depth_bits, f.id_bits,
+                                            f.globalz ? f.aux : nullptr, d64);
 }
 
 }  // namespace stp

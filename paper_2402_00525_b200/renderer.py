@@ -123,6 +123,14 @@ class BatchScene:
             if tuple(a.shape) != shapes[k]:
                 raise DataError(f"SplatBatch.{k} has shape {tuple(a.shape)}, expected {shapes[k]}")
             self.t[k] = a.to(dev).contiguous()
+        # GlobalZ inputs (view z keys, distance depth), when the batch has them
+        for k in ("global_depth", "center_dist"):
+            v = getattr(batch, k, None)
+            if v is not None:
+                a = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64))
+                if tuple(a.shape) != (n,):
+                    raise DataError(f"SplatBatch.{k} has shape {tuple(a.shape)}, expected {(n,)}")
+                self.t[k] = a.to(dev).contiguous()
         self.source_index = np.asarray(batch.source_index, dtype=np.int64).copy()
         self.device = dev
 
@@ -135,7 +143,21 @@ class BatchScene:
         for k in self.FIELDS:
             setattr(b, k, self.t[k].data_ptr())
         b.n = self.n
+        for k in ("global_depth", "center_dist"):
+            setattr(b, k, self.t[k].data_ptr() if k in self.t else None)
         return b
+
+
+def _is_globalz(mode) -> bool:
+    return type(mode).__name__ == "GlobalZ"
+
+
+def _check_supported(mode) -> None:
+    """The B200 path renders Hierarchical (the paper's pipeline) and GlobalZ
+    (the 3DGS baseline order); FullPerPixel and Window raise ConfigError."""
+    if not (_is_hier(mode) or _is_globalz(mode)):
+        raise ConfigError(f"the B200 path implements the Hierarchical and GlobalZ modes, got "
+                          f"{mode_name(mode)}")
 
 
 def _is_batch(scene) -> bool:
@@ -172,9 +194,11 @@ def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = Fa
     c.dilation = float(cfg.dilation)
     c.inv_scale_clamp = float(cfg.inv_scale_clamp)
     c.tile_size = int(cfg.tile_size)
-    c.q_tail, c.q_mid, c.q_head = int(mode.queue_tail), int(mode.queue_mid), int(mode.queue_head)
-    c.b_load, c.b_mid, c.b_head = int(mode.batch_load), int(mode.batch_mid), int(mode.batch_head)
-    c.mid_depth_at_center = int(bool(mode.mid_depth_at_center))
+    q = mode if _is_hier(mode) else Hierarchical()  # GlobalZ: queue fields unused
+    c.q_tail, c.q_mid, c.q_head = int(q.queue_tail), int(q.queue_mid), int(q.queue_head)
+    c.b_load, c.b_mid, c.b_head = int(q.batch_load), int(q.batch_mid), int(q.batch_head)
+    c.mid_depth_at_center = int(bool(q.mid_depth_at_center))
+    c.sort_mode = _lib.STP_MODE_GLOBALZ if _is_globalz(mode) else _lib.STP_MODE_HIERARCHICAL
     c.with_depth = int(bool(cfg.with_depth))
     c.exact_culling = int(bool(cfg.exact_culling(mode)))
     c.record_cap = int(record_cap)
@@ -247,9 +271,10 @@ class Renderer:
         self.device = self.scene.device
         self.mode = mode if mode is not None else Hierarchical()
         validate_mode(self.mode)
-        if not _is_hier(self.mode):
-            raise ConfigError(f"the B200 path implements the Hierarchical mode only, got "
-                              f"{mode_name(self.mode)}")
+        _check_supported(self.mode)
+        if _is_globalz(self.mode) and self.batch and not {"global_depth", "center_dist"} <= \
+                set(self.scene.t):
+            raise DataError("GlobalZ needs SplatBatch.global_depth and center_dist")
         self.cfg = cfg if cfg is not None else RenderConfig()
         self.lib = _lib.load()
         self.ws = Workspace(self.device)
@@ -434,7 +459,8 @@ def _scene_for(scene, device):
 
 def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
            device_output: bool = False, device=None) -> FrameOutput:
-    """Render one frame under the Hierarchical mode (rasterizer.py:595-698).
+    """Render one frame under the Hierarchical (default) or GlobalZ mode
+    (rasterizer.py:595-698).
 
     ``scene`` is a list of Gaussian3D, a dict of arrays/tensors in the drop-in
     layout, or a GaussianScene.  Returns float64 numpy arrays like the
@@ -442,9 +468,7 @@ def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
     mode = mode if mode is not None else Hierarchical()
     cfg = cfg or RenderConfig()
     validate_mode(mode)
-    if not _is_hier(mode):
-        raise ConfigError(f"the B200 path implements the Hierarchical mode only, got "
-                          f"{mode_name(mode)}")
+    _check_supported(mode)
     dev = _require_cuda(device)
     gs = _scene_for(scene, dev)
     r = Renderer(gs, mode, cfg, dev)

@@ -133,6 +133,8 @@ def save(name, arrs, cam, mode, cfg, sh_coeffs=16, rec_pixels=None, store_batch=
         out.update(b_mean2d=batch.mean2d, b_conic=batch.conic, b_color=batch.color,
                    b_radius=batch.radius, b_inv_cov3=batch.inv_cov3,
                    b_inv_cov_center=batch.inv_cov_center, bin_key=key)
+        if isinstance(mode, S.GlobalZ):
+            out.update(b_global_depth=batch.global_depth, b_center_dist=batch.center_dist)
     path = os.path.join(HERE, f"{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{name}: kept={pstats['kept']} entries={len(splat)} tiles={len(bins)} "

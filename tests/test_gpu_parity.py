@@ -164,9 +164,9 @@ def _golden_batch(scene, d):
     z = np.zeros(n)
     return SplatBatch(mean2d=d["b_mean2d"], conic=d["b_conic"], color=d["b_color"],
                       opacity=scene["opacity"][src].astype(np.float64), radius=d["b_radius"],
-                      global_depth=z, inv_cov3=d["b_inv_cov3"],
+                      global_depth=d.get("b_global_depth", z), inv_cov3=d["b_inv_cov3"],
                       inv_cov_center=d["b_inv_cov_center"], mean3d=np.zeros((n, 3)),
-                      center_dist=z, source_index=src)
+                      center_dist=d.get("b_center_dist", z), source_index=src)
 
 
 @PATHS
@@ -243,3 +243,18 @@ def test_oracle_parity_elongated_rows():
     out, ref = _oracle_compare(arrs, cam, RenderConfig(with_depth=True), Hierarchical(),
                                records=False)
     assert out.stats["bin_entries"] > 100_000
+
+
+@pytest.mark.parametrize("exact_cull", [None, True])
+def test_oracle_parity_globalz(exact_cull):
+    """GlobalZ (rasterizer.py:472-485, the 3DGS order) on the C3 layout at
+    60k Gaussians: coarse (default) and exact-culled bins, view-z order with
+    the float64 tie fix-up, ordered blend with the distance depth; blend
+    sequences checked."""
+    from paper_2402_00525_b200 import GlobalZ, RenderConfig, scenes
+    arrs = scenes.to_f32_scene(scenes.garden_scene(60_000, 3))
+    cam = scenes.orbit_cameras(8, width=320, height_px=180, f=183.0)[5]
+    out, ref = _oracle_compare(arrs, cam, RenderConfig(with_depth=True,
+                                                       exact_tile_culling=exact_cull),
+                               GlobalZ())
+    assert out.stats["mode"] == "globalz"
