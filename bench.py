@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=8)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="C3")
+    p.add_argument("--mode", default="hierarchical",
+                   help="sort mode: hierarchical (the paper's pipeline, default) or globalz "
+                        "(the 3DGS baseline order, for the paper's A/B)")
     p.add_argument("--gaussians", type=int, default=None, help="override N (debug)")
     p.add_argument("--views", type=int, default=256)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -190,6 +193,7 @@ def run_ours(args):
 
     from paper_2402_00525_b200 import Hierarchical, RenderConfig, _lib, scenes
     from paper_2402_00525_b200.renderer import GaussianScene, Renderer, make_camera, make_config
+    from paper_2402_00525_b200.types import mode_name, parse_mode
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -223,7 +227,7 @@ def run_ours(args):
     t_gen = time.perf_counter() - t_gen
     gs = GaussianScene(dev_t["means"], dev_t["quats"], dev_t["scales"], dev_t["opacity"],
                        dev_t["sh"], dev)
-    mode, cfg = Hierarchical(), RenderConfig()
+    mode, cfg = parse_mode(args.mode), RenderConfig()
     r = Renderer(gs, mode, cfg, dev, fast32=args.fast32)
     lib = _lib.load()
     W, H = cams[0].width, cams[0].height
@@ -347,8 +351,9 @@ def run_ours(args):
     k6_ms = stage_mean[3]
     achieved = k6_b / (k6_ms / 1e3) / 1e9
     traffic = None
+    gz = type(mode).__name__ == "GlobalZ"
     tr_path = os.path.join(ROOT, "profiles", "k6_traffic.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and not gz:  # the capture is of the hierarchical k_render
         try:
             with open(tr_path) as f:
                 traffic = json.load(f).get("bytes_per_launch")
@@ -394,7 +399,7 @@ def run_ours(args):
     # K0, K1 + row count, 3 x K2, K3 + row duplicate, K4 histogram + passes,
     # K5 (ranges with the tie fix-up), K6 (fast + list pass)
     launches_per_view = (1 + 2 + 3 + 2 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 1 +
-                         (2 if args.fast32 else 1))
+                         (2 if args.fast32 and not gz else 1))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": max_ms / steps, "higher_is_better": True,
@@ -405,7 +410,7 @@ def run_ours(args):
                    "height": H, "views": n_views, "views_per_step_per_gpu": 1,
                    "parallelism": f"views sharded over {world} GPU(s), no hot-path collective; "
                                   f"{n_str} views in flight per GPU (streams)",
-                   "mode": "hierarchical:64/8/4", "l2": "inputs larger than L2 "
+                   "mode": mode_name(mode), "l2": "inputs larger than L2 "
                    f"(scene {sum(x.numel() for x in dev_t.values()) * 4 / 1e6:.0f} MB > 126 MB)",
                    "mean_kept": float(n_v), "mean_entries": float(e),
                    "k6_path": "fp32-state certified + float64 list pass" if args.fast32
@@ -415,7 +420,9 @@ def run_ours(args):
         "stage_ms": {nm: float(x) for nm, x in zip(names, stage_mean)},
         "stage_ms_note": "one view at a time (CUDA events per stage)" + (
             f"; the timed region runs {n_str} views in flight" if n_str > 1 else ""),
-        "roofline": {"bound": "hbm", "kernel": "K6 render (k_render)", "achieved": achieved,
+        "roofline": {"bound": "hbm",
+                     "kernel": "K6 render (k_render_globalz)" if gz else "K6 render (k_render)",
+                     "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": float(k6_b),
