@@ -129,6 +129,9 @@ typedef struct {
   float* rec_alpha;      /* [H,W,record_cap]               */
   uint8_t* state;        /* [n] per-Gaussian cull state or NULL:
                             0 kept, 1 behind, 2 guard, 3 degenerate      */
+  float* sort_error;     /* [H,W] per-pixel sort error delta or NULL: the sum
+                            of positive depth inversions of consecutive blended
+                            contributions (metrics.py:46-73)             */
 } StpOutputs;
 
 /* stats dict of rasterizer.py:683-690 (+ projection stats

@@ -18,13 +18,14 @@ __all__ = [
     "GlobalZ", "Hierarchical", "PixelRecords", "RenderConfig", "SceneFormatError", "SortMode",
     "SplatBatch",
     "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
-    "render_trajectory", "Renderer", "GaussianScene",
+    "render_trajectory", "Renderer", "GaussianScene", "sort_error", "SortErrorStats",
 ]
 
 
 def __getattr__(name):
     # torch-dependent entry points load lazily
-    if name in ("render", "render_depth", "render_trajectory", "Renderer", "GaussianScene"):
+    if name in ("render", "render_depth", "render_trajectory", "Renderer", "GaussianScene",
+                "sort_error", "SortErrorStats"):
         from . import renderer
         return getattr(renderer, name)
     raise AttributeError(name)

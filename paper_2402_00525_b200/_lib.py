@@ -65,7 +65,8 @@ class StpOutputs(ctypes.Structure):
     _fields_ = [("color", ctypes.c_void_p), ("transmittance", ctypes.c_void_p),
                 ("depth", ctypes.c_void_p), ("rec_count", ctypes.c_void_p),
                 ("rec_splat", ctypes.c_void_p), ("rec_t", ctypes.c_void_p),
-                ("rec_alpha", ctypes.c_void_p), ("state", ctypes.c_void_p)]
+                ("rec_alpha", ctypes.c_void_p), ("state", ctypes.c_void_p),
+                ("sort_error", ctypes.c_void_p)]
 
 
 class StpStats(ctypes.Structure):

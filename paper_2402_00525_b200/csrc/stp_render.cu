@@ -93,7 +93,18 @@ struct Pixel {
   float C0, C1, C2, D;
   int rc;             // blend records written
   int64_t pix;        // y * W + x, -1 outside the image
+  double tprev, serr; // sort error (SERR kernels only): last blended t, sum of
+                      // positive inversions (metrics.py:46-73)
 };
+
+// sort error of one blended contribution: consecutive pairs out of t order
+template <bool SERR>
+__device__ __forceinline__ void serr_step(Pixel& P, double t) {
+  if (SERR) {
+    P.serr += fmax(P.tprev - t, 0.0);
+    P.tprev = t;
+  }
+}
 
 struct RenderArgs {
   const SplatRec* __restrict__ recs;
@@ -120,6 +131,7 @@ __device__ __noinline__ void write_record(StpOutputs out, int cap, int64_t pix, 
 }
 
 // blend (hierarchy.py:81-91)
+template <bool SERR>
 __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, double al,
                                       uint32_t id) {
   if (P.T < A.cfg.term) return;
@@ -131,10 +143,12 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
+  serr_step<SERR>(P, t);
   P.T = P.T * (1.0 - al);
 }
 
 // blend of a live pixel (P.T >= term checked by the caller)
+template <bool SERR>
 __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double t, double al,
                                            uint32_t id) {
   const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
@@ -145,6 +159,7 @@ __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
+  serr_step<SERR>(P, t);
   P.T = P.T * (1.0 - al);
 }
 
@@ -209,7 +224,7 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
 // overflow case blends min(e, H[0]) and, if H[0] left, shifts the queue and
 // re-inserts e; insertion is a compare-and-select bubble over the slots.
 // EXACT: the queue size equals QH; else runtime qh <= QH.
-template <int QH, bool EXACT>
+template <int QH, bool EXACT, bool SERR>
 __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArgs& A, int qh_rt,
                                           double t, double al, uint32_t id) {
   const int qh = EXACT ? QH : qh_rt;
@@ -222,7 +237,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     bool c[QH];
 #pragma unroll
     for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
-    blend_live(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
+    blend_live<SERR>(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
       const bool nx = i + 1 < QH;
@@ -236,7 +251,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
   }
   if (full) {
     const bool e_min = lt(t, id, H.t[0], H.id[0]);
-    blend(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
+    blend<SERR>(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
     if (e_min) return;
     // drop H[0], insert e at position c among H[1..qh-1]
     int c = 0;
@@ -404,7 +419,7 @@ struct SubQ {
 // QT > 0: the queue sizes are compile-time (tail QT, mid QMX), so every
 // shared-memory offset is an immediate (the default 64/8/4 configuration;
 // otherwise the compiler re-derives the offsets inside the hot loops).
-template <int QH, bool EXACT, int QMX, int QT>
+template <int QH, bool EXACT, int QMX, int QT, bool SERR>
 __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
@@ -491,6 +506,8 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       P.T = in_img ? 1.0 : 0.0;
       P.C0 = P.C1 = P.C2 = P.D = 0.f;
       P.rc = 0;
+      P.tprev = -INFINITY;
+      P.serr = 0.0;
     }
     Head<QH> H;
     H.n = 0;
@@ -712,7 +729,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
               }
 #pragma unroll
               for (int k = 0; k < STP_PIX_UNROLL; ++k)
-                if (ps[k] && P.T >= term) head_push<QH, EXACT>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
+                if (ps[k] && P.T >= term) head_push<QH, EXACT, SERR>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
             }
 #ifdef STP_WORK_STATS
             STAT_ADD(8, lane == 0);
@@ -933,7 +950,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
     // terminated sub-tiles
 #pragma unroll
     for (int i = 0; i < QH; ++i)
-      if (i < H.n) blend(P, A, H.t[i], H.a[i], H.id[i]);
+      if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
     PROF_ADD(4);
 
     if (P.pix >= 0) {
@@ -947,6 +964,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       A.out.transmittance[P.pix] = T;
       if (A.out.depth) A.out.depth[P.pix] = P.D;
       if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
+      if (SERR) A.out.sort_error[P.pix] = (float)P.serr;
       if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
         atomicAdd(A.counters + C_NONFINITE, 1ull);
     }
@@ -955,15 +973,15 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
 
 size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
 
-template <int QH, bool EXACT, int QMX, int QT = 0>
+template <int QH, bool EXACT, int QMX, int QT = 0, bool SERR = false>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
   static int blocks_per_sm = 0, n_sm = 0;
   if (smem != attr || blocks_per_sm == 0) {
-    cudaFuncSetAttribute(k_render<QH, EXACT, QMX, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_render<QH, EXACT, QMX, QT, SERR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT, SERR>,
                                                   kRenderThreads, smem);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -972,7 +990,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   }
   const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = min(want, n_sm * blocks_per_sm);
-  if (grid > 0) k_render<QH, EXACT, QMX, QT><<<grid, kRenderThreads, smem, s>>>(A);
+  if (grid > 0) k_render<QH, EXACT, QMX, QT, SERR><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
 // ---------------------------------------------------------------------------
@@ -1014,7 +1032,8 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
     const int64_t pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
     const double px = (double)gx + 0.5, py = (double)gy + 0.5;
     double u = 0.0, w = 0.0, vn = 0.0;
-    if (A.cfg.rec_cap > 0) cam_ray(A.cam, px, py, u, w, vn);
+    if (A.cfg.rec_cap > 0 || A.out.sort_error) cam_ray(A.cam, px, py, u, w, vn);
+    double tprev = -INFINITY, serr = 0.0;
     double T = in_img ? 1.0 : 0.0;
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
     int rc = 0;
@@ -1052,10 +1071,12 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
         C1 += oc.z * wf;
         C2 += oc.w * wf;
         D += (float)(s_dist[k] * wt);
-        if (A.cfg.rec_cap > 0) {
+        if (A.cfg.rec_cap > 0 || A.out.sort_error) {
           const SplatRec* r = A.recs + s_id[k];
           const double t = key_rec(r->m, r->q0, r->q1, r->q2, u, w, vn);
-          write_record(A.out, A.cfg.rec_cap, pix, rc++, t, al, s_id[k]);
+          if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, pix, rc++, t, al, s_id[k]);
+          serr += fmax(tprev - t, 0.0);
+          tprev = t;
         }
         T = T * (1.0 - al);
       }
@@ -1072,6 +1093,7 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
       A.out.transmittance[pix] = Tf;
       if (A.out.depth) A.out.depth[pix] = D;
       if (A.cfg.rec_cap > 0) A.out.rec_count[pix] = rc;
+      if (A.out.sort_error) A.out.sort_error[pix] = (float)serr;
       if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(Tf)))
         atomicAdd(A.counters + C_NONFINITE, 1ull);
     }
@@ -1104,9 +1126,11 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
     launch_render_globalz(f, out, s);
     return;
   }
-  if (!f.exact_only) launch_render_fast(f, buf, out, s);
+  // the sort-error diagnostics run the float64 kernel over every item
+  const bool exact_only = f.exact_only || out.sort_error != nullptr;
+  if (!exact_only) launch_render_fast(f, buf, out, s);
   RenderArgs A;
-  A.list = f.exact_only ? nullptr : f.fb_items;
+  A.list = exact_only ? nullptr : f.fb_items;
   A.recs = f.recs;
   A.log_eps = (float)log(f.cfg.eps);
   A.vals = f.vals;
@@ -1118,6 +1142,15 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.out = out;
   A.counters = f.counters;
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
+  if (out.sort_error) {
+    // sort-error diagnostics (metrics.py:46-73): the default queues or the
+    // generic kernel
+    if (f.cfg.q_tail == 64 && f.cfg.q_mid == 8 && f.cfg.q_head == 4)
+      launch_render_t<4, true, 8, 64, true>(A, smem, s);
+    else
+      launch_render_t<16, false, 0, 0, true>(A, smem, s);
+    return;
+  }
   if (f.cfg.q_mid > 8) {
     launch_render_t<16, false, 0>(A, smem, s);
     return;

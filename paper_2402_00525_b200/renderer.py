@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import time
-from dataclasses import replace
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
@@ -286,7 +286,8 @@ class Renderer:
         if rc != _lib.STP_OK:
             _raise(rc, "configuration")
 
-    def alloc_outputs(self, width, height, record_cap: int = 0, with_state: bool = False):
+    def alloc_outputs(self, width, height, record_cap: int = 0, with_state: bool = False,
+                      sort_error: bool = False):
         d = self.device
         o = {"color": torch.empty((height, width, 3), dtype=torch.float32, device=d),
              "transmittance": torch.empty((height, width), dtype=torch.float32, device=d)}
@@ -299,13 +300,15 @@ class Renderer:
             o["rec_alpha"] = torch.empty((height, width, record_cap), dtype=torch.float32, device=d)
         if with_state:
             o["state"] = torch.empty(max(1, self.scene.n), dtype=torch.uint8, device=d)
+        if sort_error:
+            o["sort_error"] = torch.empty((height, width), dtype=torch.float32, device=d)
         return o
 
     @staticmethod
     def outputs_struct(o: dict) -> _lib.StpOutputs:
         s = _lib.StpOutputs()
         for k in ("color", "transmittance", "depth", "rec_count", "rec_splat", "rec_t",
-                  "rec_alpha", "state"):
+                  "rec_alpha", "state", "sort_error"):
             if k in o:
                 setattr(s, k, o[k].data_ptr())
         return s
@@ -341,12 +344,16 @@ class Renderer:
             return st
         raise DataError("stp_render: workspace retry failed")
 
-    def frame(self, cam, device_output: bool = False) -> FrameOutput:
+    def frame(self, cam, device_output: bool = False, sort_error: bool = False) -> FrameOutput:
+        """One frame.  ``sort_error``: also the per-pixel sort error delta
+        (metrics.py:46-73), accumulated in the blend (FrameOutput.sort_error,
+        stats["sort_error"] = delta_max / delta_avg)."""
         cfg = self.cfg
         t0 = time.perf_counter()
         rec_cap = 64 if cfg.capture_records else 0
         while True:
-            outs = self.alloc_outputs(cam.width, cam.height, rec_cap, with_state=True)
+            outs = self.alloc_outputs(cam.width, cam.height, rec_cap, with_state=True,
+                                      sort_error=sort_error)
             st = self.render_into(cam, outs, stats=True, timings=True, record_cap=rec_cap)
             if rec_cap and int(outs["rec_count"].max().item()) > rec_cap:
                 rec_cap = int(outs["rec_count"].max().item())
@@ -374,9 +381,15 @@ class Renderer:
             "exact_items": int(st.exact_items),
             "resolves": int(st.resolves),
         }
+        if sort_error:
+            se = outs["sort_error"]
+            stats["sort_error"] = {"delta_max": float(se.max().item()) if se.numel() else 0.0,
+                                   "delta_avg": float(se.double().mean().item())
+                                   if se.numel() else 0.0}
         if device_output:
             out = FrameOutput(color=outs["color"], transmittance=outs["transmittance"],
-                              depth=outs.get("depth"), source_index=kept, stats=stats)
+                              depth=outs.get("depth"), source_index=kept, stats=stats,
+                              sort_error=outs.get("sort_error"))
             if rec_cap:
                 out.records = {k: outs[k] for k in ("rec_count", "rec_splat", "rec_t",
                                                     "rec_alpha")}
@@ -394,8 +407,9 @@ class Renderer:
         if rec_cap:
             records = self._records(outs, None if self.batch else src, cam)
         timings["total"] = time.perf_counter() - t0
+        se = outs["sort_error"].double().cpu().numpy() if sort_error else None
         return FrameOutput(color=color, transmittance=tn, depth=depth, records=records,
-                           source_index=src, stats=stats)
+                           source_index=src, stats=stats, sort_error=se)
 
     def debug_bins(self, cam):
         """Sorted (tile_id, gaussian_id, fp32 key bits) of the last frame rendered
@@ -458,7 +472,7 @@ def _scene_for(scene, device):
 
 
 def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
-           device_output: bool = False, device=None) -> FrameOutput:
+           device_output: bool = False, device=None, sort_error: bool = False) -> FrameOutput:
     """Render one frame under the Hierarchical (default) or GlobalZ mode
     (rasterizer.py:595-698).
 
@@ -474,7 +488,7 @@ def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
     r = Renderer(gs, mode, cfg, dev)
     ws = workspace_for(dev)
     r.ws = ws
-    return r.frame(cam, device_output=device_output)
+    return r.frame(cam, device_output=device_output, sort_error=sort_error)
 
 
 def render_depth(scene, cam, mode=None, cfg: RenderConfig | None = None, **kw) -> FrameOutput:
@@ -496,3 +510,37 @@ def render_trajectory(scene, cameras, mode=None, cfg: RenderConfig | None = None
         except Exception as exc:
             raise DataError(f"frame {i}: {exc}") from exc
     return frames
+
+
+@dataclass
+class SortErrorStats:
+    """metrics.py:37-43: out-of-order blend-depth mass per pixel."""
+
+    delta_max: float
+    delta_avg: float
+    per_pixel: np.ndarray
+
+
+def sort_error(frame) -> SortErrorStats:
+    """metrics.sort_error (metrics.py:46-73): the per-pixel sum of positive
+    depth inversions between consecutive blended contributions.  Uses the
+    map the GPU accumulated during the blend (render(..., sort_error=True)),
+    else the frame's blend records as the reference does."""
+    if isinstance(frame, FrameOutput) and frame.sort_error is not None:
+        pp = frame.sort_error
+        pp = pp.double().cpu().numpy() if hasattr(pp, "cpu") else np.asarray(pp, dtype=np.float64)
+    else:
+        recs = frame.records if isinstance(frame, FrameOutput) else frame
+        if recs is None:
+            raise ConfigError("sort_error needs blend records or render(..., sort_error=True)")
+        h = len(recs)
+        w = len(recs[0]) if h else 0
+        pp = np.zeros((h, w))
+        for y in range(h):
+            for x in range(w):
+                d = np.asarray(recs[y][x].depth, dtype=np.float64)
+                if len(d) > 1:
+                    g = d[:-1] - d[1:]
+                    pp[y, x] = g[g > 0].sum()
+    return SortErrorStats(delta_max=float(pp.max()) if pp.size else 0.0,
+                          delta_avg=float(pp.mean()) if pp.size else 0.0, per_pixel=pp)

@@ -305,3 +305,6 @@ class FrameOutput:
     records: list | None = None
     source_index: object | None = None
     stats: dict = field(default_factory=dict)
+    # per-pixel sort error delta (metrics.py:46-73), when rendered with
+    # sort_error=True: computed on the GPU during the blend, no records needed
+    sort_error: object | None = None

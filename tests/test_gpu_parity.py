@@ -258,3 +258,55 @@ def test_oracle_parity_globalz(exact_cull):
                                                        exact_tile_culling=exact_cull),
                                GlobalZ())
     assert out.stats["mode"] == "globalz"
+
+
+def _delta_from(counts, t, cap):
+    """metrics.sort_error per pixel from (count, t[..., cap]) record arrays."""
+    h, w = counts.shape
+    out = np.zeros((h, w))
+    for y in range(h):
+        for x in range(w):
+            n = min(int(counts[y, x]), cap)
+            if n > 1:
+                g = t[y, x, :n - 1] - t[y, x, 1:n]
+                out[y, x] = g[g > 0].sum()
+    return out
+
+
+@pytest.mark.parametrize("name", ["cloud300", "sh3_border", "gz_cloud300", "gz_sh3_border"])
+def test_sort_error_golden(name):
+    """Per-pixel sort error delta (metrics.py:46-73) accumulated in the GPU
+    blend == the reference's delta over its own blend records."""
+    from paper_2402_00525_b200 import sort_error
+    from paper_2402_00525_b200.renderer import Renderer
+    scene, cam, cfg, mode, d = golden_io.load(name)
+    out = Renderer(scene, mode, cfg).frame(cam, sort_error=True)
+    st = sort_error(out)
+    for i, (y, x) in enumerate(d["rec_pixels"]):
+        _, t, _ = golden_io.records_of(d, i)
+        t = t.astype(np.float64)
+        g = t[:-1] - t[1:]
+        ref = g[g > 0].sum() if len(t) > 1 else 0.0
+        assert abs(st.per_pixel[y, x] - ref) <= 1e-4 * max(1.0, ref), (name, y, x)
+    assert out.stats["sort_error"]["delta_max"] == pytest.approx(st.delta_max)
+
+
+def test_sort_error_scaled_globalz_vs_hierarchical():
+    """C3 layout at 60k: the GPU delta maps equal the oracle's record-based
+    ones for both modes, and the hierarchical resort has the smaller error."""
+    import oracle
+    from paper_2402_00525_b200 import GlobalZ, Hierarchical, RenderConfig, scenes
+    from paper_2402_00525_b200.renderer import Renderer
+    arrs = scenes.to_f32_scene(scenes.garden_scene(60_000, 3))
+    cam = scenes.orbit_cameras(8, width=256, height_px=144, f=146.0)[2]
+    cfg = RenderConfig()
+    avg = {}
+    for mode in (GlobalZ(), Hierarchical()):
+        out = Renderer(arrs, mode, cfg).frame(cam, sort_error=True)
+        ref = oracle.render(arrs, cam, cfg, mode, capture_records=True, rec_cap=512)
+        rec = ref["records"]
+        full = rec["count"] <= 512
+        dref = _delta_from(rec["count"], rec["t"], 512)
+        np.testing.assert_allclose(out.sort_error[full], dref[full], rtol=1e-5, atol=1e-6)
+        avg[type(mode).__name__] = float(out.sort_error.mean())
+    assert avg["Hierarchical"] < avg["GlobalZ"]
