@@ -79,6 +79,10 @@ def save(name, arrs, cam, mode, cfg, sh_coeffs=16, rec_pixels=None, store_batch=
                  exact_tile_culling=cfg.exact_tile_culling)
     if isinstance(mode, S.GlobalZ):
         mode_d = dict(mode="globalz")
+    elif isinstance(mode, S.FullPerPixel):
+        mode_d = dict(mode="full")
+    elif isinstance(mode, S.Window):
+        mode_d = dict(mode="window", size=mode.size)
     else:
         mode_d = dict(queue_tail=mode.queue_tail, queue_mid=mode.queue_mid,
                       queue_head=mode.queue_head, batch_load=mode.batch_load,
@@ -238,6 +242,26 @@ def main(only=None):
         save("gz_exact", from_gaussians(gs), cams[0], G,
              S.RenderConfig(with_depth=True, exact_tile_culling=True))
     jobs["globalz"] = globalz
+
+    # 10. FullPerPixel (the exact per-ray order) and Window(k) (per-pixel
+    #     resorting window over the per-tile-depth stream)
+    def pixelsort():
+        gs, cams, _ = random_cloud(300, seed=5)
+        a = from_gaussians(gs)
+        save("full_cloud300", a, cams[0], S.FullPerPixel(),
+             S.RenderConfig(with_depth=True, background=np.array([0.1, 0.2, 0.3])))
+        save("win8_cloud300", a, cams[0], S.Window(8), S.RenderConfig(with_depth=True))
+        save("win2_cloud300", a, cams[0], S.Window(2), S.RenderConfig(with_depth=True))
+        arrs = scenes.frustum_cloud(1500, 21, 203, 117, 150.0, z_lo=1.0, z_hi=5.0)
+        arrs["scales"] = arrs["scales"] * 4.0
+        pos = np.array([0.1, -0.05, -0.2])
+        R = scenes.look_at(pos, np.array([0.15, 0.0, 3.0]))
+        cam = axis_cam(203, 117, f=150.0, R=R, pos=pos, cx=97.3, cy=61.9)
+        save("full_sh3_border", scenes.to_f32_scene(arrs), cam, S.FullPerPixel(),
+             S.RenderConfig(with_depth=True))
+        save("win8_sh3_border", scenes.to_f32_scene(arrs), cam, S.Window(8),
+             S.RenderConfig(with_depth=True))
+    jobs["pixelsort"] = pixelsort
 
     for name, fn in jobs.items():
         if only and name not in only:

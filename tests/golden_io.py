@@ -9,7 +9,8 @@ import os
 
 import numpy as np
 
-from paper_2402_00525_b200.types import Camera, GlobalZ, Hierarchical, RenderConfig
+from paper_2402_00525_b200.types import (Camera, FullPerPixel, GlobalZ, Hierarchical,
+                                         RenderConfig, Window)
 
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -28,7 +29,9 @@ def load(name):
     cfg_d = json.loads(str(d["cfg_json"]))
     cfg = RenderConfig(**cfg_d)
     md = json.loads(str(d["mode_json"]))
-    mode = GlobalZ() if md.get("mode") == "globalz" else Hierarchical(**md)
+    kind = md.pop("mode", "hierarchical")
+    mode = {"globalz": GlobalZ, "full": FullPerPixel}.get(kind)
+    mode = mode() if mode else (Window(**md) if kind == "window" else Hierarchical(**md))
     scene = {k: d[k] for k in ("means", "quats", "scales", "opacity", "sh")}
     return scene, cam, cfg, mode, d
 
