@@ -101,10 +101,15 @@ typedef struct {
 
 /* Sort modes.  HIERARCHICAL: per-tile t_opt keys + the 3-level resort
  * (hierarchy.py); GLOBALZ: one view-space z key per splat and the bin's
- * order for every pixel (rasterizer.py:472-485, the 3DGS baseline; queue
- * fields are ignored). */
+ * order for every pixel (rasterizer.py:472-485, the 3DGS baseline);
+ * FULL: the exact per-pixel order (rasterizer.py:488-501); WINDOW: a
+ * per-pixel resorting window of q_head entries over the per-tile-key stream
+ * (rasterizer.py:504-588, Window.size -> q_head, 1..16).  Queue fields other
+ * than q_head (WINDOW) are ignored outside HIERARCHICAL. */
 #define STP_MODE_HIERARCHICAL 0
 #define STP_MODE_GLOBALZ 1
+#define STP_MODE_FULL 2
+#define STP_MODE_WINDOW 3
 
 #define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
 #define STP_FLAG_FAST32 2   /* K6 through the fp32-state certified kernel

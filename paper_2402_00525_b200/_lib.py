@@ -18,6 +18,8 @@ STP_FLAG_FAST32 = 2
 STP_FLAG_FB_TEST = 4
 STP_MODE_HIERARCHICAL = 0
 STP_MODE_GLOBALZ = 1
+STP_MODE_FULL = 2
+STP_MODE_WINDOW = 3
 
 EXPORTS = ("stp_abi_version", "stp_error_string", "stp_validate_config", "stp_workspace_bytes",
            "stp_workspace_layout", "stp_render", "stp_render_batch", "stp_render_views",

@@ -103,11 +103,14 @@ const char* kErrors[] = {"ok", "invalid configuration", "data error",
 int cfg_check(const StpConfig* c) {
   if (!c) return STP_ERR_CONFIG;
   if (c->tile_size != 16) return STP_ERR_CONFIG;
-  if (c->sort_mode != STP_MODE_HIERARCHICAL && c->sort_mode != STP_MODE_GLOBALZ)
+  if (c->sort_mode < STP_MODE_HIERARCHICAL || c->sort_mode > STP_MODE_WINDOW)
     return STP_ERR_CONFIG;
   if (!(c->alpha_cap > 0.0 && c->alpha_cap < 1.0)) return STP_ERR_CONFIG;
   if (c->record_cap < 0) return STP_ERR_CONFIG;
-  if (c->sort_mode == STP_MODE_GLOBALZ) return STP_OK;  // no queues
+  if (c->sort_mode == STP_MODE_GLOBALZ || c->sort_mode == STP_MODE_FULL) return STP_OK;
+  // Window(size): validate_mode (rasterizer.py:96-98) + the register window
+  if (c->sort_mode == STP_MODE_WINDOW) return (c->q_head >= 1 && c->q_head <= 16) ? STP_OK
+                                                                                 : STP_ERR_CONFIG;
   // validate_mode (rasterizer.py:98-115)
   if (c->q_tail < 64 || c->q_tail % 32 != 0) return STP_ERR_CONFIG;
   if (c->q_mid < 4 || c->q_mid % 4 != 0) return STP_ERR_CONFIG;
@@ -138,7 +141,9 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.rowlist = reinterpret_cast<uint32_t*>(b + L.rowlist);
   f.aux = reinterpret_cast<double2*>(b + L.aux);
   f.globalz = cfg->sort_mode == STP_MODE_GLOBALZ ? 1 : 0;
-  f.exact_only = ((cfg->flags & STP_FLAG_FAST32) && !f.globalz) ? 0 : 1;
+  f.sort_mode = cfg->sort_mode;
+  f.exact_only =
+      ((cfg->flags & STP_FLAG_FAST32) && cfg->sort_mode == STP_MODE_HIERARCHICAL) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);
@@ -198,7 +203,8 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   StpLayout L;
   if (!carve_frame(batch ? batch->n : sc->n, cam, cfg, ws, ws_bytes, f, L))
     return STP_ERR_WORKSPACE_TOO_SMALL;
-  if (!f.globalz && (size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024)
+  if (cfg->sort_mode == STP_MODE_HIERARCHICAL &&
+      (size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024)
     return STP_ERR_CONFIG;
   cudaEvent_t own[5];
   if (ms && !ev) {

@@ -461,6 +461,7 @@ struct Frame {
   uint32_t* rowlist;      // ids of kept Gaussians with a > 64-tile rect (C_ROWS of them)
   double2* aux;           // per Gaussian (view z, |mean - origin|), GlobalZ only
   int globalz;            // sort mode GlobalZ (view-z keys, ordered blend)
+  int sort_mode;          // STP_MODE_*
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;

@@ -1116,6 +1116,155 @@ static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStr
   if (f.n_tiles > 0) k_render_globalz<<<f.n_tiles, kGzThreads, 0, s>>>(A);
 }
 
+// ---------------------------------------------------------------------------
+// K6 under Window(size) (rasterizer.py:504-588) and FullPerPixel (:488-501).
+// The bins are the hierarchical ones (per-tile t_opt keys, exact culling).
+// One thread per pixel, warps independent (a warp stops when its 32 pixels
+// have terminated); every entry is evaluated exactly as the hierarchical
+// pixel stage does (alpha, eps test, cap, pixel-ray t_opt).
+//  Window: the valid entries of the bin stream through a per-pixel sorted
+//   window of `size` in registers; on overflow the smaller by (t, rank) of the
+//   incoming entry and the window minimum is blended -- head_push -- and the
+//   window drains in order at the end of the bin.
+//  FullPerPixel: the exact per-pixel order by repeated top-QH selection: a
+//   pass over the bin keeps the QH smallest (t, rank) above the last blended
+//   one in a sorted register buffer, blends them in order, and the next pass
+//   continues above the last; a pixel is done when a pass selects fewer than
+//   QH or it terminates.  Exact for any bin length, QH registers per pixel.
+template <int QH>
+__device__ __forceinline__ void topk_push(Head<QH>& H, double t, double al, uint32_t id) {
+  // bubble (t, id) into the sorted buffer; when full the largest falls off
+  double xt = t, xa = al;
+  uint32_t xi = id;
+#pragma unroll
+  for (int i = 0; i < QH; ++i) {
+    const bool sw = lt(xt, xi, H.t[i], H.id[i]);
+    const double ht = H.t[i], ha = H.a[i];
+    const uint32_t hi = H.id[i];
+    H.t[i] = sw ? xt : ht;
+    H.a[i] = sw ? xa : ha;
+    H.id[i] = sw ? xi : hi;
+    xt = sw ? ht : xt;
+    xa = sw ? ha : xa;
+    xi = sw ? hi : xi;
+  }
+  H.n = min(H.n + 1, QH);
+}
+
+template <int QH, bool EXACT, bool FULL, bool SERR>
+__global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
+  __shared__ double s_tab[64];
+  if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+  const int qh_rt = A.cfg.q_head;  // Window: the window size
+  const double term = A.cfg.term;
+  const int lane = threadIdx.x & 31;
+  for (int tile = blockIdx.x; tile < A.n_items; tile += gridDim.x) {
+    const int tx = tile % A.gw, ty = tile / A.gw;
+    Pixel P;
+    {
+      const int gx = tx * kTile + (threadIdx.x & 15), gy = ty * kTile + (threadIdx.x >> 4);
+      const bool in_img = gx < A.cam.W && gy < A.cam.H;
+      P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
+      P.px = (double)gx + 0.5;
+      P.py = (double)gy + 0.5;
+      cam_ray(A.cam, P.px, P.py, P.u, P.w, P.vn);
+      P.T = in_img ? 1.0 : 0.0;
+      P.C0 = P.C1 = P.C2 = P.D = 0.f;
+      P.rc = 0;
+      P.tprev = -INFINITY;
+      P.serr = 0.0;
+    }
+    Head<QH> H;
+    const uint2 rg = A.ranges[tile];
+    auto reset = [&]() {
+      H.n = 0;
+#pragma unroll
+      for (int i = 0; i < QH; ++i) {
+        H.t[i] = INFINITY;
+        H.a[i] = 0.0;
+        H.id[i] = kNoId;
+      }
+    };
+    reset();
+    if (!FULL) {
+      for (uint32_t j = rg.x; j < rg.y; ++j) {
+        if (!__any_sync(kFull, P.T >= term)) break;
+        const uint32_t id = A.vals[j];
+        double t, al;
+        const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
+        if (pass && P.T >= term) head_push<QH, EXACT, SERR>(P, H, A, qh_rt, t, al, id);
+      }
+#pragma unroll
+      for (int i = 0; i < QH; ++i)
+        if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
+    } else {
+      double lo_t = -INFINITY;
+      uint32_t lo_id = 0;
+      bool first = true, more = true;
+      while (__any_sync(kFull, more && P.T >= term)) {
+        reset();
+        if (more && P.T >= term) {
+          for (uint32_t j = rg.x; j < rg.y; ++j) {
+            const uint32_t id = A.vals[j];
+            double t, al;
+            const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
+            // entries already blended: (t, rank) <= the last one
+            if (pass && (first || lt(lo_t, lo_id, t, id))) topk_push<QH>(H, t, al, id);
+          }
+#pragma unroll
+          for (int i = 0; i < QH; ++i)
+            if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
+          if (H.n < QH) more = false;
+          lo_t = H.t[QH - 1];
+          lo_id = H.id[QH - 1];
+          first = false;
+        }
+      }
+    }
+    (void)lane;
+    if (P.pix >= 0) {
+      const float T = (float)P.T;
+      const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
+      const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
+      const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
+      A.out.color[P.pix * 3 + 0] = c0;
+      A.out.color[P.pix * 3 + 1] = c1;
+      A.out.color[P.pix * 3 + 2] = c2;
+      A.out.transmittance[P.pix] = T;
+      if (A.out.depth) A.out.depth[P.pix] = P.D;
+      if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
+      if (SERR) A.out.sort_error[P.pix] = (float)P.serr;
+      if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
+        atomicAdd(A.counters + C_NONFINITE, 1ull);
+    }
+  }
+}
+
+template <int QH, bool EXACT, bool FULL>
+static void launch_pixelsort_t(const RenderArgs& A, bool serr, cudaStream_t s) {
+  if (A.n_items <= 0) return;
+  if (serr) k_render_pixelsort<QH, EXACT, FULL, true><<<A.n_items, 256, 0, s>>>(A);
+  else k_render_pixelsort<QH, EXACT, FULL, false><<<A.n_items, 256, 0, s>>>(A);
+}
+
+static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, const StpOutputs& out,
+                                    cudaStream_t s) {
+  const bool serr = out.sort_error != nullptr;
+  if (f.sort_mode == STP_MODE_FULL) {
+    launch_pixelsort_t<16, true, true>(A, serr, s);
+    return;
+  }
+  switch (f.cfg.q_head) {  // the window size
+    case 1: launch_pixelsort_t<1, true, false>(A, serr, s); break;
+    case 2: launch_pixelsort_t<2, true, false>(A, serr, s); break;
+    case 4: launch_pixelsort_t<4, true, false>(A, serr, s); break;
+    case 8: launch_pixelsort_t<8, true, false>(A, serr, s); break;
+    case 16: launch_pixelsort_t<16, true, false>(A, serr, s); break;
+    default: launch_pixelsort_t<16, false, false>(A, serr, s); break;
+  }
+}
+
 void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
 
 // K6: the float64 kernel over every (tile, pair) item; with STP_FLAG_FAST32
@@ -1124,6 +1273,22 @@ void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStre
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
   if (f.globalz) {
     launch_render_globalz(f, out, s);
+    return;
+  }
+  if (f.sort_mode == STP_MODE_FULL || f.sort_mode == STP_MODE_WINDOW) {
+    RenderArgs A;
+    A.list = nullptr;
+    A.recs = f.recs;
+    A.log_eps = (float)log(f.cfg.eps);
+    A.vals = f.vals;
+    A.ranges = f.ranges;
+    A.cam = f.cam;
+    A.cfg = f.cfg;
+    A.gw = f.gw;
+    A.n_items = f.n_tiles;
+    A.out = out;
+    A.counters = f.counters;
+    launch_render_pixelsort(f, A, out, s);
     return;
   }
   // the sort-error diagnostics run the float64 kernel over every item

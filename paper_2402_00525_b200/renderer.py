@@ -153,10 +153,12 @@ def _is_globalz(mode) -> bool:
 
 
 def _check_supported(mode) -> None:
-    """The B200 path renders Hierarchical (the paper's pipeline) and GlobalZ
-    (the 3DGS baseline order); FullPerPixel and Window raise ConfigError."""
-    if not (_is_hier(mode) or _is_globalz(mode)):
-        raise ConfigError(f"the B200 path implements the Hierarchical and GlobalZ modes, got "
+    """All four sort modes run on the B200 path: Hierarchical (the paper's
+    pipeline), GlobalZ (the 3DGS order), FullPerPixel (the exact per-pixel
+    order) and Window(size) with 1 <= size <= 16 (a register window; larger
+    windows raise ConfigError)."""
+    if type(mode).__name__ == "Window" and not 1 <= int(mode.size) <= 16:
+        raise ConfigError(f"the B200 Window mode keeps at most 16 entries per pixel, got "
                           f"{mode_name(mode)}")
 
 
@@ -194,11 +196,15 @@ def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = Fa
     c.dilation = float(cfg.dilation)
     c.inv_scale_clamp = float(cfg.inv_scale_clamp)
     c.tile_size = int(cfg.tile_size)
-    q = mode if _is_hier(mode) else Hierarchical()  # GlobalZ: queue fields unused
+    q = mode if _is_hier(mode) else Hierarchical()  # other modes: queue fields unused
     c.q_tail, c.q_mid, c.q_head = int(q.queue_tail), int(q.queue_mid), int(q.queue_head)
     c.b_load, c.b_mid, c.b_head = int(q.batch_load), int(q.batch_mid), int(q.batch_head)
     c.mid_depth_at_center = int(bool(q.mid_depth_at_center))
-    c.sort_mode = _lib.STP_MODE_GLOBALZ if _is_globalz(mode) else _lib.STP_MODE_HIERARCHICAL
+    name = type(mode).__name__
+    c.sort_mode = {"GlobalZ": _lib.STP_MODE_GLOBALZ, "FullPerPixel": _lib.STP_MODE_FULL,
+                   "Window": _lib.STP_MODE_WINDOW}.get(name, _lib.STP_MODE_HIERARCHICAL)
+    if name == "Window":
+        c.q_head = int(mode.size)  # the window size (stp.h STP_MODE_WINDOW)
     c.with_depth = int(bool(cfg.with_depth))
     c.exact_culling = int(bool(cfg.exact_culling(mode)))
     c.record_cap = int(record_cap)

@@ -132,11 +132,13 @@ def test_deterministic_repeat():
 
 
 def test_config_errors_raise():
-    from paper_2402_00525_b200 import (ConfigError, FullPerPixel, Hierarchical, RenderConfig,
+    from paper_2402_00525_b200 import (ConfigError, Hierarchical, RenderConfig, Window,
                                        render)
     scene, cam, cfg, mode, d = golden_io.load("shallow")
     with pytest.raises(ConfigError):
-        render(scene, cam, FullPerPixel(), RenderConfig())
+        render(scene, cam, Window(0), RenderConfig())      # validate_mode
+    with pytest.raises(ConfigError):
+        render(scene, cam, Window(17), RenderConfig())     # B200 register window
     with pytest.raises(ConfigError):
         render(scene, cam, Hierarchical(queue_tail=48), RenderConfig())
     with pytest.raises(ConfigError):
@@ -310,3 +312,19 @@ def test_sort_error_scaled_globalz_vs_hierarchical():
         np.testing.assert_allclose(out.sort_error[full], dref[full], rtol=1e-5, atol=1e-6)
         avg[type(mode).__name__] = float(out.sort_error.mean())
     assert avg["Hierarchical"] < avg["GlobalZ"]
+
+
+@pytest.mark.parametrize("mode_name", ["full", "window:8", "window:3"])
+def test_oracle_parity_pixelsort_modes(mode_name):
+    """FullPerPixel (exact per-pixel order by repeated top-16 selection) and
+    Window(k) on the C3 layout at 60k Gaussians vs the oracle: tile lists,
+    order, blend sequences, pixels; FullPerPixel has zero sort error."""
+    from paper_2402_00525_b200 import RenderConfig, parse_mode, scenes, sort_error
+    from paper_2402_00525_b200.renderer import Renderer
+    arrs = scenes.to_f32_scene(scenes.garden_scene(60_000, 3))
+    cam = scenes.orbit_cameras(8, width=256, height_px=144, f=146.0)[6]
+    mode = parse_mode(mode_name)
+    _oracle_compare(arrs, cam, RenderConfig(with_depth=True), mode)
+    if mode_name == "full":
+        out = Renderer(arrs, mode, RenderConfig()).frame(cam, sort_error=True)
+        assert sort_error(out).delta_max == 0.0
