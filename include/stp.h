@@ -209,6 +209,30 @@ int stp_render_events(const StpScene* scene, const StpCamera* cam, const StpConf
                       void* workspace, size_t workspace_bytes, const StpOutputs* out,
                       void* const* events, void* stream);
 
+/* Backward pass (gradients.py:103-162): gradients of the loss w.r.t. the
+ * projected splat attributes, given dL/d(colour) of the frame.  The frame is
+ * rendered again into `out` and K6 is replayed twice over the same bins (the
+ * blend order is recomputed, no records are stored): first for each pixel's
+ * float64 colour sum and final T (pix_state), then with every blended
+ * contribution's gradients added (float64 atomics) by Gaussian id -- the
+ * SplatBatch index for stp_backward_batch.  d_background = sum upstream * T
+ * is left to the caller (pix_state[..., 3] holds T).  Any sort mode. */
+typedef struct {
+  const double* upstream;  /* [H,W,3] dL/d colour                          */
+  double* pix_state;       /* [H,W,4] scratch: colour sum (3), final T     */
+  double* d_color;         /* [n,3]   (zeroed by the call)                 */
+  double* d_opacity;       /* [n]                                          */
+  double* d_mean2d;        /* [n,2]                                        */
+  double* d_conic;         /* [n,3]   (a, b, c) of the conic               */
+} StpGrads;
+
+int stp_backward(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
+                 void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                 const StpGrads* grads, StpStats* stats, void* stream);
+int stp_backward_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
+                       void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                       const StpGrads* grads, StpStats* stats, void* stream);
+
 /* Thin cudart helpers so hosts without a CUDA binding can time stages. */
 int stp_events_create(int32_t n, void** events);
 int stp_events_destroy(int32_t n, void* const* events);

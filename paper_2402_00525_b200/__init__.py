@@ -19,6 +19,7 @@ __all__ = [
     "SplatBatch",
     "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
     "render_trajectory", "Renderer", "GaussianScene", "sort_error", "SortErrorStats",
+    "backward_render", "SplatGradients", "loss_l2",
 ]
 
 
@@ -28,4 +29,7 @@ def __getattr__(name):
                 "sort_error", "SortErrorStats"):
         from . import renderer
         return getattr(renderer, name)
+    if name in ("backward_render", "SplatGradients", "loss_l2"):
+        from . import gradients
+        return getattr(gradients, name)
     raise AttributeError(name)

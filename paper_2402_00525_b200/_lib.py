@@ -25,7 +25,7 @@ EXPORTS = ("stp_abi_version", "stp_error_string", "stp_validate_config", "stp_wo
            "stp_workspace_layout", "stp_render", "stp_render_batch", "stp_render_views",
            "stp_read_stats",
            "stp_render_events", "stp_events_create", "stp_events_destroy",
-           "stp_event_elapsed_ms")
+           "stp_event_elapsed_ms", "stp_backward", "stp_backward_batch")
 
 
 class StpScene(ctypes.Structure):
@@ -69,6 +69,12 @@ class StpOutputs(ctypes.Structure):
                 ("rec_splat", ctypes.c_void_p), ("rec_t", ctypes.c_void_p),
                 ("rec_alpha", ctypes.c_void_p), ("state", ctypes.c_void_p),
                 ("sort_error", ctypes.c_void_p)]
+
+
+class StpGrads(ctypes.Structure):
+    _fields_ = [("upstream", ctypes.c_void_p), ("pix_state", ctypes.c_void_p),
+                ("d_color", ctypes.c_void_p), ("d_opacity", ctypes.c_void_p),
+                ("d_mean2d", ctypes.c_void_p), ("d_conic", ctypes.c_void_p)]
 
 
 class StpStats(ctypes.Structure):
@@ -123,6 +129,11 @@ def load(build_if_missing: bool = True):
                              ctypes.POINTER(StpConfig), ctypes.c_void_p, ctypes.c_size_t,
                              ctypes.POINTER(StpOutputs), ctypes.POINTER(StpStats),
                              ctypes.c_void_p]
+    for fn, sc in (("stp_backward", StpScene), ("stp_backward_batch", StpSplatBatch)):
+        getattr(L, fn).argtypes = [ctypes.POINTER(sc), ctypes.POINTER(StpCamera),
+                                   ctypes.POINTER(StpConfig), ctypes.c_void_p, ctypes.c_size_t,
+                                   ctypes.POINTER(StpOutputs), ctypes.POINTER(StpGrads),
+                                   ctypes.c_void_p, ctypes.c_void_p]
     L.stp_render_batch.argtypes = [ctypes.POINTER(StpSplatBatch), ctypes.POINTER(StpCamera),
                                    ctypes.POINTER(StpConfig), ctypes.c_void_p, ctypes.c_size_t,
                                    ctypes.POINTER(StpOutputs), ctypes.POINTER(StpStats),

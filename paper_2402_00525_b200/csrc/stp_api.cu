@@ -198,7 +198,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
 // stage times returned.
 int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* cam,
                const StpConfig* cfg, void* ws, size_t ws_bytes, const StpOutputs* out,
-               cudaStream_t s, cudaEvent_t* ev, float* ms) {
+               cudaStream_t s, cudaEvent_t* ev, float* ms, const StpGrads* grads = nullptr) {
   Frame f;
   StpLayout L;
   if (!carve_frame(batch ? batch->n : sc->n, cam, cfg, ws, ws_bytes, f, L))
@@ -224,7 +224,29 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   const int buf = launch_sort(f, s);
   launch_ranges(f, buf, s);
   if (ev) cudaEventRecord(ev[3], s);
-  launch_render(f, buf, o, s);
+  if (grads) {
+    // backward (gradients.py:103-162): K6 replayed twice over the same bins,
+    // first for each pixel's float64 colour sum and final T, then with the
+    // per-contribution gradients scattered by Gaussian id
+    const int64_t n = f.n;
+    if (n > 0) {
+      cudaMemsetAsync(grads->d_color, 0, (size_t)n * 3 * sizeof(double), s);
+      cudaMemsetAsync(grads->d_opacity, 0, (size_t)n * sizeof(double), s);
+      cudaMemsetAsync(grads->d_mean2d, 0, (size_t)n * 2 * sizeof(double), s);
+      cudaMemsetAsync(grads->d_conic, 0, (size_t)n * 3 * sizeof(double), s);
+    }
+    DevGrads g;
+    g.upstream = grads->upstream;
+    g.pix = grads->pix_state;
+    g.d_color = grads->d_color;
+    g.d_opacity = grads->d_opacity;
+    g.d_mean2d = grads->d_mean2d;
+    g.d_conic = grads->d_conic;
+    launch_render(f, buf, o, s, XM_FWD, &g);
+    launch_render(f, buf, o, s, XM_BWD, &g);
+  } else {
+    launch_render(f, buf, o, s);
+  }
   if (ev) cudaEventRecord(ev[4], s);
   if (ms) {
     cudaEventSynchronize(ev[4]);
@@ -453,6 +475,55 @@ int stp_read_stats(const void* workspace, size_t workspace_bytes, int64_t n, int
   memset(stats, 0, sizeof(*stats));
   return fill_stats(workspace, workspace_bytes, n, width, height, stats,
                     static_cast<cudaStream_t>(stream));
+}
+
+
+static int check_grads(const StpGrads* g, int64_t n) {
+  if (!g || !g->upstream || !g->pix_state) return STP_ERR_DATA;
+  if (n > 0 && (!g->d_color || !g->d_opacity || !g->d_mean2d || !g->d_conic)) return STP_ERR_DATA;
+  return STP_OK;
+}
+
+int stp_backward(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
+                 void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                 const StpGrads* grads, StpStats* stats, void* stream) {
+  int rc = check_inputs(scene, cam, cfg, out);
+  if (rc != STP_OK) return rc;
+  if ((rc = check_grads(grads, scene->n)) != STP_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr, nullptr,
+                  grads);
+  if (rc != STP_OK) return rc;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    rc = fill_stats(workspace, workspace_bytes, scene->n, cam->width, cam->height, stats, s);
+    if (rc != STP_OK) return rc;
+    if (stats->overflow) return STP_ERR_WORKSPACE_TOO_SMALL;
+  }
+  return STP_OK;
+}
+
+int stp_backward_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
+                       void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                       const StpGrads* grads, StpStats* stats, void* stream) {
+  if (!batch || !cam || !cfg || !out) return STP_ERR_CONFIG;
+  int rc = cfg_check(cfg);
+  if (rc != STP_OK) return rc;
+  if (batch->n < 0 || batch->n >= (int64_t)0x7fffffff) return STP_ERR_DATA;
+  if (!out->color || !out->transmittance) return STP_ERR_DATA;
+  if (cfg->with_depth && !out->depth) return STP_ERR_DATA;
+  if ((rc = check_grads(grads, batch->n)) != STP_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr, nullptr,
+                  grads);
+  if (rc != STP_OK) return rc;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    rc = fill_stats(workspace, workspace_bytes, batch->n, cam->width, cam->height, stats, s);
+    if (rc != STP_OK) return rc;
+    if (stats->overflow) return STP_ERR_WORKSPACE_TOO_SMALL;
+  }
+  return STP_OK;
 }
 
 }  // extern "C"

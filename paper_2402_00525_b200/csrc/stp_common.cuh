@@ -493,5 +493,16 @@ void launch_scan(const Frame& f, cudaStream_t s);
 void launch_duplicate(const Frame& f, cudaStream_t s);
 int launch_sort(const Frame& f, cudaStream_t s);  // returns the buffer holding the result
 void launch_ranges(const Frame& f, int buf, cudaStream_t s);
-void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
+// K6 extra modes (stp_render.cu) and the backward pass's buffers
+constexpr int XM_NONE = 0, XM_SERR = 1, XM_FWD = 2, XM_BWD = 3;
+struct DevGrads {
+  const double* upstream;  // [H,W,3] dL/d colour
+  double* pix;             // [H,W,4]: float64 blended colour sum (3) + final T
+  double* d_color;         // [n,3]   (indexed by Gaussian id)
+  double* d_opacity;       // [n]
+  double* d_mean2d;        // [n,2]
+  double* d_conic;         // [n,3] (a, b, c)
+};
+void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s,
+                   int xm = XM_NONE, const DevGrads* g = nullptr);
 }  // namespace stp

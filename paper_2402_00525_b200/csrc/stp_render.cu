@@ -85,6 +85,14 @@ struct Head {
   int n;
 };
 
+// Extra per-blend work of a K6 instantiation (template int XM):
+//   XM_NONE  the forward render
+//   XM_SERR  + the sort error delta (metrics.py:46-73)
+//   XM_FWD   + the float64 blended colour sum and final T per pixel (the
+//            backward pass's first replay)
+//   XM_BWD   the backward replay (gradients.py:103-162): the same blend order
+//            recomputed, each contribution's gradients scattered
+
 struct Pixel {
   double px, py;
   double u, w, vn;    // camera ray (u, w, 1) of the pixel centre, |(u, w, 1)|
@@ -93,18 +101,12 @@ struct Pixel {
   float C0, C1, C2, D;
   int rc;             // blend records written
   int64_t pix;        // y * W + x, -1 outside the image
-  double tprev, serr; // sort error (SERR kernels only): last blended t, sum of
-                      // positive inversions (metrics.py:46-73)
+  double tprev, serr; // XM_SERR: last blended t, sum of positive inversions
+  double f0, f1, f2;  // XM_FWD: sum of colour * w; XM_BWD: that sum (full)
+  double a0, a1, a2;  // XM_BWD: running sum (acc)
+  double g0, g1, g2;  // XM_BWD: upstream dL/dcolour of the pixel
+  double tn;          // XM_BWD: the pixel's final T
 };
-
-// sort error of one blended contribution: consecutive pairs out of t order
-template <bool SERR>
-__device__ __forceinline__ void serr_step(Pixel& P, double t) {
-  if (SERR) {
-    P.serr += fmax(P.tprev - t, 0.0);
-    P.tprev = t;
-  }
-}
 
 struct RenderArgs {
   const SplatRec* __restrict__ recs;
@@ -117,7 +119,91 @@ struct RenderArgs {
   StpOutputs out;
   unsigned long long* counters;
   const uint32_t* list;   // list mode: (tile*8 + pair) items handed over by the fast path
+  DevGrads grad;          // XM_FWD / XM_BWD
 };
+
+// per-pixel state of the extra modes at the start of a pixel
+template <int XM>
+__device__ __forceinline__ void xm_init(Pixel& P, const RenderArgs& A) {
+  P.tprev = -INFINITY;
+  P.serr = 0.0;
+  P.f0 = P.f1 = P.f2 = 0.0;
+  P.a0 = P.a1 = P.a2 = 0.0;
+  P.g0 = P.g1 = P.g2 = 0.0;
+  P.tn = 0.0;
+  if (XM == XM_BWD && P.pix >= 0) {
+    const double* g = A.grad.upstream + P.pix * 3;
+    P.g0 = g[0];
+    P.g1 = g[1];
+    P.g2 = g[2];
+    const double* q = A.grad.pix + P.pix * 4;
+    P.f0 = q[0];
+    P.f1 = q[1];
+    P.f2 = q[2];
+    P.tn = q[3];
+  }
+}
+
+// gradients of one blended contribution (gradients.py:124-162, the
+// front-to-back form: trailing colour = full - acc - term)
+__device__ __noinline__ void bwd_step(Pixel& P, const RenderArgs& A, double al, uint32_t id,
+                                      float4 oc) {
+  const double T = P.T, w = al * T;
+  const double c0 = oc.y, c1 = oc.z, c2 = oc.w;
+  P.a0 += c0 * w;
+  P.a1 += c1 * w;
+  P.a2 += c2 * w;
+  const double om = fmax(1.0 - al, 1e-6);
+  const double d_alpha = P.g0 * (c0 * T - (P.f0 - P.a0 + A.cfg.bg[0] * P.tn) / om) +
+                         P.g1 * (c1 * T - (P.f1 - P.a1 + A.cfg.bg[1] * P.tn) / om) +
+                         P.g2 * (c2 * T - (P.f2 - P.a2 + A.cfg.bg[2] * P.tn) / om);
+  if (!isfinite(d_alpha)) atomicAdd(A.counters + C_NONFINITE, 1ull);
+  atomicAdd(A.grad.d_color + id * 3 + 0, P.g0 * w);
+  atomicAdd(A.grad.d_color + id * 3 + 1, P.g1 * w);
+  atomicAdd(A.grad.d_color + id * 3 + 2, P.g2 * w);
+  if (al < A.cfg.cap) {
+    const SplatRec& r = A.recs[id];
+    const double dx = P.px - r.mx, dy = P.py - r.my;
+    atomicAdd(A.grad.d_opacity + id, d_alpha * (al / (double)oc.x));
+    const double da = d_alpha * al;
+    atomicAdd(A.grad.d_mean2d + id * 2 + 0, da * (r.ca * dx + r.cb * dy));
+    atomicAdd(A.grad.d_mean2d + id * 2 + 1, da * (r.cb * dx + r.cc * dy));
+    atomicAdd(A.grad.d_conic + id * 3 + 0, -da * 0.5 * dx * dx);
+    atomicAdd(A.grad.d_conic + id * 3 + 1, -da * dx * dy);
+    atomicAdd(A.grad.d_conic + id * 3 + 2, -da * 0.5 * dy * dy);
+  }
+}
+
+// the extra work of one blended contribution (before T is updated)
+template <int XM>
+__device__ __forceinline__ void xm_step(Pixel& P, const RenderArgs& A, double t, double al,
+                                        uint32_t id, float4 oc) {
+  if (XM == XM_SERR) {
+    P.serr += fmax(P.tprev - t, 0.0);
+    P.tprev = t;
+  } else if (XM == XM_FWD) {
+    const double w = al * P.T;
+    P.f0 += (double)oc.y * w;
+    P.f1 += (double)oc.z * w;
+    P.f2 += (double)oc.w * w;
+  } else if (XM == XM_BWD) {
+    bwd_step(P, A, al, id, oc);
+  }
+}
+
+// per-pixel outputs of the extra modes at the end of a pixel
+template <int XM>
+__device__ __forceinline__ void xm_done(const Pixel& P, const RenderArgs& A) {
+  if (P.pix < 0) return;
+  if (XM == XM_SERR) A.out.sort_error[P.pix] = (float)P.serr;
+  if (XM == XM_FWD) {
+    double* q = A.grad.pix + P.pix * 4;
+    q[0] = P.f0;
+    q[1] = P.f1;
+    q[2] = P.f2;
+    q[3] = P.T;
+  }
+}
 
 // debug blend-record capture (cold path, kept out of line)
 __device__ __noinline__ void write_record(StpOutputs out, int cap, int64_t pix, int rc, double t,
@@ -131,7 +217,7 @@ __device__ __noinline__ void write_record(StpOutputs out, int cap, int64_t pix, 
 }
 
 // blend (hierarchy.py:81-91)
-template <bool SERR>
+template <int XM>
 __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, double al,
                                       uint32_t id) {
   if (P.T < A.cfg.term) return;
@@ -143,12 +229,12 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
-  serr_step<SERR>(P, t);
+  xm_step<XM>(P, A, t, al, id, oc);
   P.T = P.T * (1.0 - al);
 }
 
 // blend of a live pixel (P.T >= term checked by the caller)
-template <bool SERR>
+template <int XM>
 __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double t, double al,
                                            uint32_t id) {
   const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
@@ -159,7 +245,7 @@ __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
-  serr_step<SERR>(P, t);
+  xm_step<XM>(P, A, t, al, id, oc);
   P.T = P.T * (1.0 - al);
 }
 
@@ -224,7 +310,7 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
 // overflow case blends min(e, H[0]) and, if H[0] left, shifts the queue and
 // re-inserts e; insertion is a compare-and-select bubble over the slots.
 // EXACT: the queue size equals QH; else runtime qh <= QH.
-template <int QH, bool EXACT, bool SERR>
+template <int QH, bool EXACT, int XM>
 __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArgs& A, int qh_rt,
                                           double t, double al, uint32_t id) {
   const int qh = EXACT ? QH : qh_rt;
@@ -237,7 +323,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     bool c[QH];
 #pragma unroll
     for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
-    blend_live<SERR>(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
+    blend_live<XM>(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
       const bool nx = i + 1 < QH;
@@ -251,7 +337,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
   }
   if (full) {
     const bool e_min = lt(t, id, H.t[0], H.id[0]);
-    blend<SERR>(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
+    blend<XM>(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
     if (e_min) return;
     // drop H[0], insert e at position c among H[1..qh-1]
     int c = 0;
@@ -419,7 +505,7 @@ struct SubQ {
 // QT > 0: the queue sizes are compile-time (tail QT, mid QMX), so every
 // shared-memory offset is an immediate (the default 64/8/4 configuration;
 // otherwise the compiler re-derives the offsets inside the hot loops).
-template <int QH, bool EXACT, int QMX, int QT, bool SERR>
+template <int QH, bool EXACT, int QMX, int QT, int XM>
 __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
@@ -506,8 +592,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       P.T = in_img ? 1.0 : 0.0;
       P.C0 = P.C1 = P.C2 = P.D = 0.f;
       P.rc = 0;
-      P.tprev = -INFINITY;
-      P.serr = 0.0;
+      xm_init<XM>(P, A);
     }
     Head<QH> H;
     H.n = 0;
@@ -729,7 +814,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
               }
 #pragma unroll
               for (int k = 0; k < STP_PIX_UNROLL; ++k)
-                if (ps[k] && P.T >= term) head_push<QH, EXACT, SERR>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
+                if (ps[k] && P.T >= term) head_push<QH, EXACT, XM>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
             }
 #ifdef STP_WORK_STATS
             STAT_ADD(8, lane == 0);
@@ -950,10 +1035,11 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
     // terminated sub-tiles
 #pragma unroll
     for (int i = 0; i < QH; ++i)
-      if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
+      if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
     PROF_ADD(4);
 
-    if (P.pix >= 0) {
+    xm_done<XM>(P, A);
+    if (P.pix >= 0 && XM != XM_BWD) {
       const float T = (float)P.T;
       const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
       const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
@@ -964,7 +1050,6 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       A.out.transmittance[P.pix] = T;
       if (A.out.depth) A.out.depth[P.pix] = P.D;
       if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
-      if (SERR) A.out.sort_error[P.pix] = (float)P.serr;
       if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
         atomicAdd(A.counters + C_NONFINITE, 1ull);
     }
@@ -973,15 +1058,15 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
 
 size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
 
-template <int QH, bool EXACT, int QMX, int QT = 0, bool SERR = false>
+template <int QH, bool EXACT, int QMX, int QT = 0, int XM = XM_NONE>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
   static int blocks_per_sm = 0, n_sm = 0;
   if (smem != attr || blocks_per_sm == 0) {
-    cudaFuncSetAttribute(k_render<QH, EXACT, QMX, QT, SERR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_render<QH, EXACT, QMX, QT, XM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT, SERR>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT, XM>,
                                                   kRenderThreads, smem);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -990,7 +1075,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   }
   const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int grid = min(want, n_sm * blocks_per_sm);
-  if (grid > 0) k_render<QH, EXACT, QMX, QT, SERR><<<grid, kRenderThreads, smem, s>>>(A);
+  if (grid > 0) k_render<QH, EXACT, QMX, QT, XM><<<grid, kRenderThreads, smem, s>>>(A);
 }
 
 // ---------------------------------------------------------------------------
@@ -1006,6 +1091,8 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
 constexpr int kGzThreads = 256;
 
 struct GzArgs {
+  int xm;          // XM_* (runtime: the GlobalZ kernel is not register bound)
+  DevGrads grad;
   const SplatRec* __restrict__ recs;
   const uint32_t* __restrict__ vals;
   const uint2* __restrict__ ranges;
@@ -1025,22 +1112,36 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
   __shared__ uint32_t s_id[kGzThreads];
   const int tid = threadIdx.x;
   if (tid < 64) s_tab[tid] = kExp2Tab[tid];
+  // the per-blend helpers take RenderArgs
+  RenderArgs R;
+  R.recs = A.recs;
+  R.cam = A.cam;
+  R.cfg = A.cfg;
+  R.out = A.out;
+  R.counters = A.counters;
+  R.grad = A.grad;
+  const bool need_t = A.cfg.rec_cap > 0 || A.xm == XM_SERR;
   for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
     const int tx = tile % A.gw, ty = tile / A.gw;
     const int gx = tx * kTile + (tid & 15), gy = ty * kTile + (tid >> 4);
     const bool in_img = gx < A.cam.W && gy < A.cam.H;
-    const int64_t pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
-    const double px = (double)gx + 0.5, py = (double)gy + 0.5;
-    double u = 0.0, w = 0.0, vn = 0.0;
-    if (A.cfg.rec_cap > 0 || A.out.sort_error) cam_ray(A.cam, px, py, u, w, vn);
-    double tprev = -INFINITY, serr = 0.0;
-    double T = in_img ? 1.0 : 0.0;
-    float C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f;
-    int rc = 0;
+    Pixel P;
+    P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
+    P.px = (double)gx + 0.5;
+    P.py = (double)gy + 0.5;
+    P.u = P.w = P.vn = 0.0;
+    if (need_t) cam_ray(A.cam, P.px, P.py, P.u, P.w, P.vn);
+    P.T = in_img ? 1.0 : 0.0;
+    P.C0 = P.C1 = P.C2 = P.D = 0.f;
+    P.rc = 0;
+    switch (A.xm) {
+      case XM_BWD: xm_init<XM_BWD>(P, R); break;
+      default: xm_init<XM_NONE>(P, R); break;
+    }
     const uint2 rg = A.ranges[tile];
     for (uint32_t base = rg.x; base < rg.y; base += kGzThreads) {
       // all pixels terminated: the rest of the bin blends nothing
-      if (__syncthreads_count(T >= A.cfg.term) == 0) break;
+      if (__syncthreads_count(P.T >= A.cfg.term) == 0) break;
       const uint32_t j = base + tid;
       if (j < rg.y) {
         const uint32_t id = A.vals[j];
@@ -1058,42 +1159,51 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
       }
       __syncthreads();
       const int n = (int)min((uint32_t)kGzThreads, rg.y - base);
-      for (int k = 0; k < n && T >= A.cfg.term; ++k) {
-        const double dx = px - s_mx[k], dy = py - s_my[k];
+      for (int k = 0; k < n && P.T >= A.cfg.term; ++k) {
+        const double dx = P.px - s_mx[k], dy = P.py - s_my[k];
         const double pw = gpower(s_a[k], s_b[k], s_c[k], dx, dy);
         const float4 oc = s_oc[k];
         double al = (double)oc.x * exp_neg_nb(min_le(pw, 700.0), s_tab);
         al = min_le(al, A.cfg.cap);
         if (al < A.cfg.eps) continue;  // alpha 0: no weight, T unchanged
-        const double wt = al * T;
+        const double wt = al * P.T;
         const float wf = (float)wt;
-        C0 += oc.y * wf;
-        C1 += oc.z * wf;
-        C2 += oc.w * wf;
-        D += (float)(s_dist[k] * wt);
-        if (A.cfg.rec_cap > 0 || A.out.sort_error) {
+        P.C0 += oc.y * wf;
+        P.C1 += oc.z * wf;
+        P.C2 += oc.w * wf;
+        P.D += (float)(s_dist[k] * wt);
+        double t = 0.0;
+        if (need_t) {
           const SplatRec* r = A.recs + s_id[k];
-          const double t = key_rec(r->m, r->q0, r->q1, r->q2, u, w, vn);
-          if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, pix, rc++, t, al, s_id[k]);
-          serr += fmax(tprev - t, 0.0);
-          tprev = t;
+          t = key_rec(r->m, r->q0, r->q1, r->q2, P.u, P.w, P.vn);
+          if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, s_id[k]);
         }
-        T = T * (1.0 - al);
+        switch (A.xm) {
+          case XM_SERR: xm_step<XM_SERR>(P, R, t, al, s_id[k], oc); break;
+          case XM_FWD: xm_step<XM_FWD>(P, R, t, al, s_id[k], oc); break;
+          case XM_BWD: xm_step<XM_BWD>(P, R, t, al, s_id[k], oc); break;
+          default: break;
+        }
+        P.T = P.T * (1.0 - al);
       }
       __syncthreads();
     }
-    if (pix >= 0) {
-      const float Tf = (float)T;
-      const float c0 = C0 + (float)(T * A.cfg.bg[0]);
-      const float c1 = C1 + (float)(T * A.cfg.bg[1]);
-      const float c2 = C2 + (float)(T * A.cfg.bg[2]);
-      A.out.color[pix * 3 + 0] = c0;
-      A.out.color[pix * 3 + 1] = c1;
-      A.out.color[pix * 3 + 2] = c2;
-      A.out.transmittance[pix] = Tf;
-      if (A.out.depth) A.out.depth[pix] = D;
-      if (A.cfg.rec_cap > 0) A.out.rec_count[pix] = rc;
-      if (A.out.sort_error) A.out.sort_error[pix] = (float)serr;
+    switch (A.xm) {
+      case XM_SERR: xm_done<XM_SERR>(P, R); break;
+      case XM_FWD: xm_done<XM_FWD>(P, R); break;
+      default: break;
+    }
+    if (P.pix >= 0 && A.xm != XM_BWD) {
+      const float Tf = (float)P.T;
+      const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
+      const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
+      const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
+      A.out.color[P.pix * 3 + 0] = c0;
+      A.out.color[P.pix * 3 + 1] = c1;
+      A.out.color[P.pix * 3 + 2] = c2;
+      A.out.transmittance[P.pix] = Tf;
+      if (A.out.depth) A.out.depth[P.pix] = P.D;
+      if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
       if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(Tf)))
         atomicAdd(A.counters + C_NONFINITE, 1ull);
     }
@@ -1101,8 +1211,11 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
   }
 }
 
-static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStream_t s) {
+static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStream_t s, int xm,
+                                  const DevGrads* g) {
   GzArgs A;
+  A.xm = xm;
+  if (g) A.grad = *g;
   A.recs = f.recs;
   A.vals = f.vals;
   A.ranges = f.ranges;
@@ -1151,7 +1264,7 @@ __device__ __forceinline__ void topk_push(Head<QH>& H, double t, double al, uint
   H.n = min(H.n + 1, QH);
 }
 
-template <int QH, bool EXACT, bool FULL, bool SERR>
+template <int QH, bool EXACT, bool FULL, int XM>
 __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
   __shared__ double s_tab[64];
   if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];
@@ -1172,8 +1285,7 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
       P.T = in_img ? 1.0 : 0.0;
       P.C0 = P.C1 = P.C2 = P.D = 0.f;
       P.rc = 0;
-      P.tprev = -INFINITY;
-      P.serr = 0.0;
+      xm_init<XM>(P, A);
     }
     Head<QH> H;
     const uint2 rg = A.ranges[tile];
@@ -1193,11 +1305,11 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
         const uint32_t id = A.vals[j];
         double t, al;
         const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
-        if (pass && P.T >= term) head_push<QH, EXACT, SERR>(P, H, A, qh_rt, t, al, id);
+        if (pass && P.T >= term) head_push<QH, EXACT, XM>(P, H, A, qh_rt, t, al, id);
       }
 #pragma unroll
       for (int i = 0; i < QH; ++i)
-        if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
+        if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
     } else {
       double lo_t = -INFINITY;
       uint32_t lo_id = 0;
@@ -1214,7 +1326,7 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
           }
 #pragma unroll
           for (int i = 0; i < QH; ++i)
-            if (i < H.n) blend<SERR>(P, A, H.t[i], H.a[i], H.id[i]);
+            if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
           if (H.n < QH) more = false;
           lo_t = H.t[QH - 1];
           lo_id = H.id[QH - 1];
@@ -1223,7 +1335,8 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
       }
     }
     (void)lane;
-    if (P.pix >= 0) {
+    xm_done<XM>(P, A);
+    if (P.pix >= 0 && XM != XM_BWD) {
       const float T = (float)P.T;
       const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
       const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
@@ -1234,7 +1347,6 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
       A.out.transmittance[P.pix] = T;
       if (A.out.depth) A.out.depth[P.pix] = P.D;
       if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
-      if (SERR) A.out.sort_error[P.pix] = (float)P.serr;
       if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
         atomicAdd(A.counters + C_NONFINITE, 1ull);
     }
@@ -1242,26 +1354,29 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
 }
 
 template <int QH, bool EXACT, bool FULL>
-static void launch_pixelsort_t(const RenderArgs& A, bool serr, cudaStream_t s) {
+static void launch_pixelsort_t(const RenderArgs& A, int xm, cudaStream_t s) {
   if (A.n_items <= 0) return;
-  if (serr) k_render_pixelsort<QH, EXACT, FULL, true><<<A.n_items, 256, 0, s>>>(A);
-  else k_render_pixelsort<QH, EXACT, FULL, false><<<A.n_items, 256, 0, s>>>(A);
+  switch (xm) {
+    case XM_SERR: k_render_pixelsort<QH, EXACT, FULL, XM_SERR><<<A.n_items, 256, 0, s>>>(A); break;
+    case XM_FWD: k_render_pixelsort<QH, EXACT, FULL, XM_FWD><<<A.n_items, 256, 0, s>>>(A); break;
+    case XM_BWD: k_render_pixelsort<QH, EXACT, FULL, XM_BWD><<<A.n_items, 256, 0, s>>>(A); break;
+    default: k_render_pixelsort<QH, EXACT, FULL, XM_NONE><<<A.n_items, 256, 0, s>>>(A); break;
+  }
 }
 
-static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, const StpOutputs& out,
+static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
                                     cudaStream_t s) {
-  const bool serr = out.sort_error != nullptr;
   if (f.sort_mode == STP_MODE_FULL) {
-    launch_pixelsort_t<16, true, true>(A, serr, s);
+    launch_pixelsort_t<16, true, true>(A, xm, s);
     return;
   }
   switch (f.cfg.q_head) {  // the window size
-    case 1: launch_pixelsort_t<1, true, false>(A, serr, s); break;
-    case 2: launch_pixelsort_t<2, true, false>(A, serr, s); break;
-    case 4: launch_pixelsort_t<4, true, false>(A, serr, s); break;
-    case 8: launch_pixelsort_t<8, true, false>(A, serr, s); break;
-    case 16: launch_pixelsort_t<16, true, false>(A, serr, s); break;
-    default: launch_pixelsort_t<16, false, false>(A, serr, s); break;
+    case 1: launch_pixelsort_t<1, true, false>(A, xm, s); break;
+    case 2: launch_pixelsort_t<2, true, false>(A, xm, s); break;
+    case 4: launch_pixelsort_t<4, true, false>(A, xm, s); break;
+    case 8: launch_pixelsort_t<8, true, false>(A, xm, s); break;
+    case 16: launch_pixelsort_t<16, true, false>(A, xm, s); break;
+    default: launch_pixelsort_t<16, false, false>(A, xm, s); break;
   }
 }
 
@@ -1270,32 +1385,16 @@ void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStre
 // K6: the float64 kernel over every (tile, pair) item; with STP_FLAG_FAST32
 // the fp32-state certified kernel first, then the float64 kernel over the
 // items it handed over (list mode).
-void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s) {
+// K6 dispatch.  xm: XM_NONE (render), or with `g` the backward replays
+// XM_FWD / XM_BWD; a non-null out.sort_error selects XM_SERR.
+void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s, int xm,
+                   const DevGrads* g) {
+  if (xm == XM_NONE && out.sort_error) xm = XM_SERR;
   if (f.globalz) {
-    launch_render_globalz(f, out, s);
+    launch_render_globalz(f, out, s, xm, g);
     return;
   }
-  if (f.sort_mode == STP_MODE_FULL || f.sort_mode == STP_MODE_WINDOW) {
-    RenderArgs A;
-    A.list = nullptr;
-    A.recs = f.recs;
-    A.log_eps = (float)log(f.cfg.eps);
-    A.vals = f.vals;
-    A.ranges = f.ranges;
-    A.cam = f.cam;
-    A.cfg = f.cfg;
-    A.gw = f.gw;
-    A.n_items = f.n_tiles;
-    A.out = out;
-    A.counters = f.counters;
-    launch_render_pixelsort(f, A, out, s);
-    return;
-  }
-  // the sort-error diagnostics run the float64 kernel over every item
-  const bool exact_only = f.exact_only || out.sort_error != nullptr;
-  if (!exact_only) launch_render_fast(f, buf, out, s);
   RenderArgs A;
-  A.list = exact_only ? nullptr : f.fb_items;
   A.recs = f.recs;
   A.log_eps = (float)log(f.cfg.eps);
   A.vals = f.vals;
@@ -1306,14 +1405,36 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.n_items = f.n_tiles;
   A.out = out;
   A.counters = f.counters;
+  A.list = nullptr;
+  if (g) A.grad = *g;
+  if (f.sort_mode == STP_MODE_FULL || f.sort_mode == STP_MODE_WINDOW) {
+    launch_render_pixelsort(f, A, xm, s);
+    return;
+  }
+  // the extra modes run the float64 kernel over every item
+  const bool exact_only = f.exact_only || xm != XM_NONE;
+  if (!exact_only) {
+    launch_render_fast(f, buf, out, s);
+    A.list = f.fb_items;
+  }
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
-  if (out.sort_error) {
-    // sort-error diagnostics (metrics.py:46-73): the default queues or the
-    // generic kernel
-    if (f.cfg.q_tail == 64 && f.cfg.q_mid == 8 && f.cfg.q_head == 4)
-      launch_render_t<4, true, 8, 64, true>(A, smem, s);
-    else
-      launch_render_t<16, false, 0, 0, true>(A, smem, s);
+  if (xm != XM_NONE) {
+    // diagnostics / backward: the default queues or the generic kernel
+    const bool dflt = f.cfg.q_tail == 64 && f.cfg.q_mid == 8 && f.cfg.q_head == 4;
+    switch (xm) {
+      case XM_SERR:
+        if (dflt) launch_render_t<4, true, 8, 64, XM_SERR>(A, smem, s);
+        else launch_render_t<16, false, 0, 0, XM_SERR>(A, smem, s);
+        break;
+      case XM_FWD:
+        if (dflt) launch_render_t<4, true, 8, 64, XM_FWD>(A, smem, s);
+        else launch_render_t<16, false, 0, 0, XM_FWD>(A, smem, s);
+        break;
+      default:
+        if (dflt) launch_render_t<4, true, 8, 64, XM_BWD>(A, smem, s);
+        else launch_render_t<16, false, 0, 0, XM_BWD>(A, smem, s);
+        break;
+    }
     return;
   }
   if (f.cfg.q_mid > 8) {

@@ -417,6 +417,56 @@ class Renderer:
         return FrameOutput(color=color, transmittance=tn, depth=depth, records=records,
                            source_index=src, stats=stats, sort_error=se)
 
+    def backward(self, cam, upstream):
+        """Gradients of the loss w.r.t. the projected splat attributes
+        (gradients.py:103-162) for dL/d(colour) ``upstream`` [H,W,3]: the frame
+        is re-rendered and K6 replayed (stp_backward); returns the per-splat
+        SplatGradients in batch (kept-splat) order, float64 numpy."""
+        from .gradients import SplatGradients
+        H, W = int(cam.height), int(cam.width)
+        up = torch.as_tensor(upstream, dtype=torch.float64).to(self.device).contiguous()
+        if tuple(up.shape) != (H, W, 3):
+            raise DataError(f"upstream gradient dims {tuple(up.shape)} do not match the frame")
+        n = self.scene.n
+        d = self.device
+        pix = torch.empty((H, W, 4), dtype=torch.float64, device=d)
+        gt = {k: torch.empty((max(n, 1), c), dtype=torch.float64, device=d)
+              for k, c in (("d_color", 3), ("d_opacity", 1), ("d_mean2d", 2), ("d_conic", 3))}
+        g = _lib.StpGrads()
+        g.upstream, g.pix_state = up.data_ptr(), pix.data_ptr()
+        for k, t in gt.items():
+            setattr(g, k, t.data_ptr())
+        outs = self.alloc_outputs(W, H, with_state=True)
+        c_cam = make_camera(cam)
+        self._ensure(cam)
+        c_cfg = make_config(self.cfg, self.mode)
+        c_out = self.outputs_struct(outs)
+        s = torch.cuda.current_stream(d).cuda_stream
+        st = _lib.StpStats()
+        fn = self.lib.stp_backward_batch if self.batch else self.lib.stp_backward
+        for _ in range(3):
+            rc = fn(ctypes.byref(self.c_scene), ctypes.byref(c_cam), ctypes.byref(c_cfg),
+                    ctypes.c_void_p(self.ws.ptr), self.ws.nbytes, ctypes.byref(c_out),
+                    ctypes.byref(g), ctypes.byref(st), ctypes.c_void_p(s))
+            if rc == _lib.STP_ERR_WORKSPACE_TOO_SMALL:
+                need = int(st.bin_entries * 1.25) + 4096
+                self.entry_capacity = need
+                self.ws.ensure(self.scene.n, cam.width, cam.height, need)
+                continue
+            if rc != _lib.STP_OK:
+                _raise(rc, "stp_backward")
+            break
+        if st.nonfinite_pixels:
+            raise DataError("non-finite gradient or pixel in the backward pass")
+        if self.batch:
+            kept = torch.arange(n, device=d)
+        else:
+            kept = torch.nonzero(outs["state"][:n] == 0).flatten()
+        f = lambda k: gt[k][kept].cpu().numpy()  # noqa: E731
+        d_bg = (up * pix[..., 3:4]).sum(dim=(0, 1)).cpu().numpy()
+        return SplatGradients(d_color=f("d_color"), d_opacity=f("d_opacity")[:, 0],
+                              d_mean2d=f("d_mean2d"), d_conic=f("d_conic"), d_background=d_bg)
+
     def debug_bins(self, cam):
         """Sorted (tile_id, gaussian_id, fp32 key bits) of the last frame rendered
         with this renderer's workspace (parity dumps of K3-K5)."""

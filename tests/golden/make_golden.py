@@ -263,6 +263,38 @@ def main(only=None):
              S.RenderConfig(with_depth=True))
     jobs["pixelsort"] = pixelsort
 
+    # 11. backward pass (gradients.py:84-162): reference gradients w.r.t. the
+    #     projected batch for a seeded upstream dL/dcolour, per fixture/mode
+    def grads():
+        from splatsort import gradients as SG
+        for fx in ("cloud300", "shallow", "sh3_border", "gz_cloud300", "win8_cloud300",
+                   "edges"):
+            z = np.load(os.path.join(HERE, f"{fx}.npz"))
+            d = {k: z[k] for k in z.files}
+            arrs = {k: d[k] for k in ("means", "quats", "scales", "opacity", "sh")}
+            gs = to_gaussians(arrs)
+            fxi, fyi, cxi, cyi = d["cam_intr"]
+            w, h = (int(v) for v in d["cam_size"])
+            cam = S.Camera(rotation=d["cam_R"], position=d["cam_pos"], fx=fxi, fy=fyi,
+                           width=w, height=h, cx=cxi, cy=cyi)
+            cfg = S.RenderConfig(**json.loads(str(d["cfg_json"])))
+            md = json.loads(str(d["mode_json"]))
+            kind = md.pop("mode", "hierarchical")
+            mode = {"globalz": S.GlobalZ, "full": S.FullPerPixel}.get(kind)
+            mode = mode() if mode else (S.Window(**md) if kind == "window" else S.Hierarchical(**md))
+            batch, _ = S.project_scene(gs, cam, near=cfg.near, guard=cfg.guard_band,
+                                       dilation=cfg.dilation,
+                                       inv_scale_clamp=cfg.inv_scale_clamp, eps=cfg.opacity_eps)
+            up = np.random.default_rng(99).normal(0, 1, (h, w, 3))
+            g = SG.backward_render(batch, cam, mode, up, cfg)
+            path = os.path.join(HERE, f"grad_{fx}.npz")
+            np.savez_compressed(path, upstream=up, d_color=g.d_color, d_opacity=g.d_opacity,
+                                d_mean2d=g.d_mean2d, d_conic=g.d_conic,
+                                d_background=g.d_background)
+            print(f"grad_{fx}: n={len(g.d_opacity)} -> {os.path.getsize(path) / 1e6:.2f} MB",
+                  flush=True)
+    jobs["grads"] = grads
+
     for name, fn in jobs.items():
         if only and name not in only:
             continue

@@ -16,7 +16,19 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if not os.path.basename(p).startswith("grad_"))
+
+
+def grad_names():
+    """Fixtures with reference gradients (grad_<name>.npz)."""
+    return sorted(os.path.basename(p)[5:-4]
+                  for p in glob.glob(os.path.join(GOLDEN_DIR, "grad_*.npz")))
+
+
+def load_grad(name):
+    z = np.load(os.path.join(GOLDEN_DIR, f"grad_{name}.npz"))
+    return {k: z[k] for k in z.files}
 
 
 def load(name):
