@@ -243,6 +243,10 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
     g.d_mean2d = grads->d_mean2d;
     g.d_conic = grads->d_conic;
     launch_render(f, buf, o, s, XM_FWD, &g);
+    // the persistent K6 hands out (tile, pair) items from frame counters and
+    // per-SM rings: clear them for the second replay
+    cudaMemsetAsync(f.counters + C_TILE, 0, sizeof(unsigned long long), s);
+    cudaMemsetAsync(f.counters + C_SM, 0, (size_t)(C_SMT + 256 * 16 - C_SM) * 8, s);
     launch_render(f, buf, o, s, XM_BWD, &g);
   } else {
     launch_render(f, buf, o, s);

@@ -456,6 +456,8 @@ class Renderer:
             if rc != _lib.STP_OK:
                 _raise(rc, "stp_backward")
             break
+        else:
+            raise DataError("stp_backward: workspace retry failed")
         if st.nonfinite_pixels:
             raise DataError("non-finite gradient or pixel in the backward pass")
         if self.batch:
