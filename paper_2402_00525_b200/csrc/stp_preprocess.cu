@@ -11,6 +11,8 @@
 // The (splat, tile) pairs of a warp's 32 splats are enumerated cooperatively
 // (warp_expand), so lanes stay busy whatever the rect sizes (the paper's
 // load balancing, applied to every splat).
+#include <atomic>
+
 #include "stp_common.cuh"
 
 namespace stp {
@@ -38,11 +40,13 @@ __constant__ double c_SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.457
 // K0: zero the per-frame counters / histograms / tile ranges, bump the epoch
 // that tags the sort's look-back words (so they never need clearing).
 __global__ void k_init(unsigned long long* counters, uint32_t* hist, int hist_n, uint2* ranges,
-                       int n_tiles, DevCam cam, DevCam* camp) {
+                       int n_tiles, DevCam cam, DevCam* camp, unsigned long long epoch) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int stride = gridDim.x * blockDim.x;
   if (tid == 0) {
-    counters[C_EPOCH] += 1;
+    // process-wide frame number: look-back words left in a recycled
+    // workspace buffer (another workspace's frames) can never match it
+    counters[C_EPOCH] = epoch;
     *camp = cam;
   }
   for (int i = tid; i < C_COUNT; i += stride)
@@ -932,10 +936,16 @@ __global__ void __launch_bounds__(256) k_rows_dup(const SplatRec* __restrict__ r
 // launchers
 
 void launch_init(const Frame& f, cudaStream_t s) {
+  // epoch tags of the onesweep look-back (never cleared): unique per frame in
+  // the process, never 0 (0 reads as "not published")
+  static std::atomic<unsigned long long> g_epoch{0};
+  unsigned long long ep = ++g_epoch & 0xffffffffull;
+  if (ep == 0) ep = ++g_epoch & 0xffffffffull;
   const int hist_n = f.passes * 256;
   const int work = max(max(hist_n, f.n_tiles), (int)C_COUNT);
   const int blocks = min((work + 255) / 256, 1024);
-  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp);
+  k_init<<<blocks, 256, 0, s>>>(f.counters, f.hist, hist_n, f.ranges, f.n_tiles, f.cam, f.camp,
+                                ep);
 }
 
 // grid of the row-culling kernels: the list length is on the device, so a

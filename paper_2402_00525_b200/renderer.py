@@ -13,6 +13,7 @@ entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, replace
 

@@ -403,3 +403,23 @@ def test_backward_oracle_scaled():
     g["d_background"] = np.einsum("hwc,hw->c", up, ref["transmittance"])
     got = backward_render(arrs, cam, Hierarchical(), up, cfg)
     _grad_close(got, g, "c3-60k")
+
+
+def test_recycled_workspace_is_safe():
+    """A workspace buffer holding stale data of another workspace (the torch
+    caching allocator recycles blocks) must not leak into a frame: the
+    onesweep look-back words are epoch-tagged with a process-wide frame
+    number, so stale words never match.  The poison makes every 64-bit word
+    look like a published prefix whose tag equals (its own low word + 1),
+    which a per-buffer epoch counter would accept."""
+    import torch
+    scene, cam, cfg, mode, d = golden_io.load("sh3_border")
+    r = _renderer(scene, mode, cfg)
+    r.frame(cam)
+    t0, g0, _ = r.debug_bins(cam)
+    r.ws.buf.view(torch.int64).fill_(int(0x80000008_80000007 - (1 << 64)))
+    out = r.frame(cam)
+    t1, g1, _ = r.debug_bins(cam)
+    np.testing.assert_array_equal(t0, t1)
+    np.testing.assert_array_equal(g0, g1)
+    np.testing.assert_allclose(out.color, d["color"], atol=TOL, rtol=0)
