@@ -463,14 +463,21 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
 // ---------------------------------------------------------------------------
 // Shared-memory queues of one sub-tile, addressed arithmetically (units of
 // one element: doubles in the key region, uint32 in the id region):
-//   [tail0 qt | tail1 qt | batch 32 | mid 4 x MS | scratch 4 x SS | pad |
+//   [tail qt (x2 unless qt == 64) | mid 4 x MS | scratch 4 x SS | pad |
 //    groups 4 x GS]  and, ids only, [rings 4 x RS].
 // The per-quad strides are odd (MS = qm+1, SS = qm+5, GS = 17, RS = R+1)
 // and the group base sits 4 elements past a 16-element boundary relative to
 // the mids, so the 4 quads' arrays -- read by the same instruction in the
 // mid merge and the pixel stage -- fall on distinct shared-memory banks.
+// The sorted load batch (<= 32) lives in the group region (groups exist only
+// inside push_mid, the batch only inside a merge).  With qt == 64 a merge
+// reads at most 32 + 32 entries, two per lane, so it runs in place (read and
+// rank everything, then write) and the tail is single-buffered.  Shared
+// memory is traded against L1: the records the warps re-read live in the
+// rest of the SM's 256 KB (measured: 32 KB less L1 per SM = +5.5% K6).
 __host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? 64 : 128; }
-__host__ __device__ inline int q_mid0(int qt) { return 2 * qt + 32; }
+__host__ __device__ inline bool tail_inplace(int qt) { return qt == 64; }
+__host__ __device__ inline int q_mid0(int qt) { return (tail_inplace(qt) ? 1 : 2) * qt; }
 __host__ __device__ inline int q_scr0(int qt, int qm) { return q_mid0(qt) + 4 * (qm + 1); }
 __host__ __device__ inline int q_grp0(int qt, int qm) {
   const int b = q_scr0(qt, qm) + 4 * (qm + 5);
@@ -491,8 +498,8 @@ struct SubQ {
   int qt, qm;
   __device__ __forceinline__ double* td(int c) const { return d + c * qt; }
   __device__ __forceinline__ uint32_t* ti(int c) const { return i + c * qt; }
-  __device__ __forceinline__ double* bd() const { return d + 2 * qt; }
-  __device__ __forceinline__ uint32_t* bi() const { return i + 2 * qt; }
+  __device__ __forceinline__ double* bd() const { return d + q_grp0(qt, qm); }
+  __device__ __forceinline__ uint32_t* bi() const { return i + q_grp0(qt, qm); }
   __device__ __forceinline__ int o_mid(int q) const { return q_mid0(qt) + q * (qm + 1); }
   __device__ __forceinline__ int o_scr(int q) const { return q_scr0(qt, qm) + q * (qm + 5); }
   __device__ __forceinline__ int o_grp(int q) const { return q_grp0(qt, qm) + 17 * q; }
@@ -971,6 +978,67 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
             Q.bi()[xS1] = iS1;
           }
           __syncwarp();
+          if (tail_inplace(qt)) {
+            // qt == 64: tails hold <= 32 here, so every lane reads and ranks
+            // at most one new element per sub-tile and two tail elements,
+            // then all lanes write (single buffer)
+            int rk1 = 0, rk2 = 0;
+            if (v1)
+              rk1 = count_below(Q1.td(0) + (s1 ? th1 : th0), Q1.ti(0) + (s1 ? th1 : th0),
+                                s1 ? nt1 : nt0, d1, i1);
+            if (!cpt && vS1) {
+              const SubQ Q = subq(1);
+              rk2 = count_below(Q.td(0) + th1, Q.ti(0) + th1, nt1, dS1, iS1);
+            }
+            const int n0 = nkA ? nt0 : 0, n1 = nkB ? nt1 : 0;
+            double tv[2];
+            uint32_t tiv[2];
+            int trk[2], tpos[2], tst[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int u = lane + 32 * k;
+              tst[k] = u >= n0;
+              tpos[k] = -1;
+              if (u < n0 + n1) {
+                const int st = tst[k];
+                const int t = u - (st ? n0 : 0);
+                const SubQ Q = subq(st);
+                const int th = st ? th1 : th0;
+                tv[k] = Q.td(0)[th + t];
+                tiv[k] = Q.ti(0)[th + t];
+                trk[k] = count_below(Q.bd(), Q.bi(), st ? nkB : nkA, tv[k], tiv[k]);
+                tpos[k] = t;
+              }
+            }
+            __syncwarp();
+            if (v1) {
+              Q1.td(0)[x1 + rk1] = d1;
+              Q1.ti(0)[x1 + rk1] = i1;
+            }
+            if (!cpt && vS1) {
+              const SubQ Q = subq(1);
+              Q.td(0)[xS1 + rk2] = dS1;
+              Q.ti(0)[xS1 + rk2] = iS1;
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              if (tpos[k] >= 0) {
+                const SubQ Q = subq(tst[k]);
+                Q.td(0)[tpos[k] + trk[k]] = tv[k];
+                Q.ti(0)[tpos[k] + trk[k]] = tiv[k];
+              }
+            __syncwarp();
+            if (nkA) {
+              th0 = 0;
+              nt0 += nkA;
+            }
+            if (nkB) {
+              th1 = 0;
+              nt1 += nkB;
+            }
+            PROF_ADD(1);
+            continue;
+          }
           if (v1) {
             const int cur = s1 ? cur1 : cur0, th = s1 ? th1 : th0, nt = s1 ? nt1 : nt0;
             const int rk = count_below(Q1.td(cur) + th, Q1.ti(cur) + th, nt, d1, i1);
@@ -1056,7 +1124,12 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
   }
 }
 
-size_t render_smem_bytes(int qt, int qm) { return kWarpsPerBlock * warp_smem_bytes(qt, qm); }
+#ifndef STP_SMEM_PAD
+#define STP_SMEM_PAD 0  // experiments: extra shared memory per block (less L1)
+#endif
+size_t render_smem_bytes(int qt, int qm) {
+  return kWarpsPerBlock * warp_smem_bytes(qt, qm) + STP_SMEM_PAD;
+}
 
 template <int QH, bool EXACT, int QMX, int QT = 0, int XM = XM_NONE>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
