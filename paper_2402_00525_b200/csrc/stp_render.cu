@@ -475,7 +475,13 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
 // rank everything, then write) and the tail is single-buffered.  Shared
 // memory is traded against L1: the records the warps re-read live in the
 // rest of the SM's 256 KB (measured: 32 KB less L1 per SM = +5.5% K6).
-__host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? 64 : 128; }
+#ifndef STP_RING
+#define STP_RING 64
+#endif
+#ifndef STP_READY
+#define STP_READY 16  // consume once every producing sub-tile has this many emits
+#endif
+__host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? STP_RING : 128; }
 __host__ __device__ inline bool tail_inplace(int qt) { return qt == 64; }
 __host__ __device__ inline int q_mid0(int qt) { return (tail_inplace(qt) ? 1 : 2) * qt; }
 __host__ __device__ inline int q_scr0(int qt, int qm) { return q_mid0(qt) + 4 * (qm + 1); }
@@ -781,7 +787,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
     const int ring_full = R - 16 - qm;
     for (;;) {
       const int pa = rt0 - rh0, pb = rt1 - rh1;
-      const bool ready = (!prod0 || pa >= 16) && (!prod1 || pb >= 16);
+      const bool ready = (!prod0 || pa >= STP_READY) && (!prod1 || pb >= STP_READY);
       if (pa > ring_full || pb > ring_full || (ready && pa + pb > 0)) {
         // ================= consume: pixels take emits from their quad rings
         const int rounds = (pa > 0 && pb > 0) ? min(pa, pb) : max(pa, pb);
