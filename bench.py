@@ -139,16 +139,18 @@ def b_alg(n, sh_k, n_v, e, p, with_depth=False):
 # ----------------------------------------------------------------------------
 # reference arm: the reference's algorithm on the host cores (oracle port)
 
-def cpu_view_rate(scene, cams, views, budget_s, threads):
-    """Full views (project + bin_and_sort + hierarchical render of every tile)
-    of the C++ restatement of the reference, all host threads."""
+def cpu_view_rate(scene, cams, views, budget_s, threads, mode=None):
+    """Full views (project + bin_and_sort + render of every tile under the
+    sort mode, hierarchical by default) of the C++ restatement of the
+    reference, all host threads."""
     import oracle
     from paper_2402_00525_b200 import Hierarchical, RenderConfig
+    mode = mode if mode is not None else Hierarchical()
     times = []
     t_all = time.perf_counter()
     for v in views:
         t0 = time.perf_counter()
-        oracle.render(scene, cams[v], RenderConfig(), Hierarchical(), threads=threads)
+        oracle.render(scene, cams[v], RenderConfig(), mode, threads=threads)
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_all > budget_s:
             break
@@ -162,20 +164,22 @@ def run_reference(args):
     from paper_2402_00525_b200 import scenes
     scene, cams = scenes.config_scene(args.config, n=args.gaussians, n_views=args.views)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    from paper_2402_00525_b200.types import mode_name, parse_mode
+    mode = parse_mode(args.mode)
     # warmup (bounded: at most 2 views)
-    cpu_view_rate(scene, cams, list(range(min(args.warmup, 2))), 1e9, threads)
+    cpu_view_rate(scene, cams, list(range(min(args.warmup, 2))), 1e9, threads, mode)
     views = [s % len(cams) for s in range(args.steps)]
-    rate, done, times = cpu_view_rate(scene, cams, views, args.cpu_seconds, threads)
+    rate, done, times = cpu_view_rate(scene, cams, views, args.cpu_seconds, threads, mode)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
         "steps": done, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOADS[args.config.upper()], "gaussians": len(scene["opacity"]),
                                         "width": cams[0].width, "height": cams[0].height,
-                                        "views": len(cams), "mode": "hierarchical:64/8/4"},
+                                        "views": len(cams), "mode": mode_name(mode)},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{done} full {args.config.upper()} views (project + bin_and_sort + "
-                                   f"hierarchical render of all tiles) by oracle/stp_oracle.cpp, "
+                                   f"{mode_name(mode)} render of all tiles) by oracle/stp_oracle.cpp, "
                                    f"the float64 C++ restatement of the reference pinned to its "
                                    f"golden outputs; requested steps={args.steps}, timed within "
                                    f"{args.cpu_seconds:.0f} s"},
