@@ -19,7 +19,8 @@ __all__ = [
     "SplatBatch",
     "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
     "render_trajectory", "Renderer", "GaussianScene", "sort_error", "SortErrorStats",
-    "backward_render", "SplatGradients", "loss_l2",
+    "backward_render", "SplatGradients", "loss_l2", "load_ply", "load_ply_arrays",
+    "load_ply_scene", "load_cameras",
 ]
 
 
@@ -29,6 +30,9 @@ def __getattr__(name):
                 "sort_error", "SortErrorStats"):
         from . import renderer
         return getattr(renderer, name)
+    if name in ("load_ply", "load_ply_arrays", "load_ply_scene", "load_cameras"):
+        from . import scene_io
+        return getattr(scene_io, name)
     if name in ("backward_render", "SplatGradients", "loss_l2"):
         from . import gradients
         return getattr(gradients, name)

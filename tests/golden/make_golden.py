@@ -295,6 +295,32 @@ def main(only=None):
                   flush=True)
     jobs["grads"] = grads
 
+    # 12. scene / camera I/O (scene_io.py:189-417): a 3DGS PLY checkpoint and a
+    #     cameras.json written by the reference, plus what its loaders return
+    def io():
+        from splatsort import scene_io as SIO
+        gs, cams, _ = random_cloud(200, seed=17)
+        for g in gs:   # full SH so f_rest carries data
+            g.sh[1:] = np.random.default_rng(len(g.sh)).normal(0, 0.2, (15, 3))
+        ply = os.path.join(HERE, "io_cloud200.ply")
+        SIO.save_ply(gs, ply)
+        back = SIO.load_ply(ply)
+        cj = os.path.join(HERE, "io_cams.json")
+        SIO.save_cameras(cams, cj)
+        cb = SIO.load_cameras(cj)
+        np.savez_compressed(os.path.join(HERE, "io_expected.npz"),
+                            means=np.stack([g.mean for g in back]),
+                            quats=np.stack([g.rotation for g in back]),
+                            scales=np.stack([g.scale for g in back]),
+                            opacity=np.array([g.opacity for g in back]),
+                            sh=np.stack([g.sh for g in back]),
+                            cam_R=np.stack([c.rotation for c in cb]),
+                            cam_pos=np.stack([c.position for c in cb]),
+                            cam_intr=np.array([[c.fx, c.fy, c.cx, c.cy] for c in cb]),
+                            cam_size=np.array([[c.width, c.height] for c in cb]))
+        print(f"io: {len(back)} Gaussians, {len(cb)} cameras", flush=True)
+    jobs["io"] = io
+
     for name, fn in jobs.items():
         if only and name not in only:
             continue

@@ -423,3 +423,22 @@ def test_recycled_workspace_is_safe():
     np.testing.assert_array_equal(t0, t1)
     np.testing.assert_array_equal(g0, g1)
     np.testing.assert_allclose(out.color, d["color"], atol=TOL, rtol=0)
+
+
+def test_ply_checkpoint_renders_like_oracle():
+    """A 3DGS PLY written by the reference, decoded and uploaded once
+    (scene_io.load_ply_scene), renders like the oracle on the same arrays."""
+    import os
+    import oracle
+    from paper_2402_00525_b200 import Hierarchical, RenderConfig
+    from paper_2402_00525_b200.renderer import Renderer
+    from paper_2402_00525_b200.scene_io import load_cameras, load_ply_arrays, load_ply_scene
+    g = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    ply = os.path.join(g, "io_cloud200.ply")
+    cam = load_cameras(os.path.join(g, "io_cams.json"))[0]
+    cfg = RenderConfig(with_depth=True)
+    out = Renderer(load_ply_scene(ply), Hierarchical(), cfg).frame(cam)
+    ref = oracle.render(load_ply_arrays(ply), cam, cfg, Hierarchical())
+    assert out.stats["bin_entries"] == ref["stats"]["bin_entries"] > 0
+    np.testing.assert_allclose(out.color, ref["color"], atol=TOL, rtol=0)
+    np.testing.assert_allclose(out.transmittance, ref["transmittance"], atol=TOL, rtol=0)
