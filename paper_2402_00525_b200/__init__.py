@@ -20,7 +20,7 @@ __all__ = [
     "TileBin", "Window", "mode_name", "parse_mode", "validate_mode", "render", "render_depth",
     "render_trajectory", "Renderer", "GaussianScene", "sort_error", "SortErrorStats",
     "backward_render", "SplatGradients", "loss_l2", "load_ply", "load_ply_arrays",
-    "load_ply_scene", "load_cameras",
+    "load_ply_scene", "load_cameras", "consistency",
 ]
 
 
@@ -30,6 +30,9 @@ def __getattr__(name):
                 "sort_error", "SortErrorStats"):
         from . import renderer
         return getattr(renderer, name)
+    if name == "consistency":
+        from . import consistency
+        return consistency
     if name in ("load_ply", "load_ply_arrays", "load_ply_scene", "load_cameras"):
         from . import scene_io
         return getattr(scene_io, name)

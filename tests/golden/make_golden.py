@@ -321,6 +321,40 @@ def main(only=None):
         print(f"io: {len(back)} Gaussians, {len(cb)} cameras", flush=True)
     jobs["io"] = io
 
+    # 13. view consistency (metrics.py:80-255): three depth frames of a small
+    #     yaw sweep rendered by the reference, its analytic flows, warps,
+    #     occlusion masks and the squared-error consistency score
+    def consistency():
+        from splatsort import metrics as SM
+        arrs = scenes.frustum_cloud(2000, 31, 96, 72, 80.0, z_lo=2.0, z_hi=6.0)
+        gs = to_gaussians(scenes.to_f32_scene(arrs))
+        cams = []
+        for k in range(3):
+            a = np.deg2rad(1.5 * k)
+            R = np.array([[np.cos(a), 0, -np.sin(a)], [0, 1, 0], [np.sin(a), 0, np.cos(a)]])
+            cams.append(axis_cam(96, 72, f=80.0, R=R, pos=np.array([0.02 * k, 0.0, 0.0])))
+        cfg = S.RenderConfig(with_depth=True)
+        fr = [S.render(gs, c, S.Hierarchical(), cfg) for c in cams]
+        out = {}
+        for k, f in enumerate(fr):
+            out[f"color{k}"], out[f"depth{k}"], out[f"tn{k}"] = f.color, f.depth, f.transmittance
+            out[f"R{k}"], out[f"pos{k}"] = cams[k].rotation, cams[k].position
+        fw, bw = {}, {}
+        for i in range(3):
+            for j in range(3):
+                if i != j:
+                    fl, va = SM.analytic_flow(fr[i], cams[i], cams[j])
+                    out[f"flow{i}{j}"], out[f"valid{i}{j}"] = fl, va
+                    (fw if j > i else bw)[(i, j)] = (fl, va)
+        wa, wv = SM.warp_frame(fr[1].color, out["flow01"])
+        out["warp01"], out["warpvalid01"] = wa, wv
+        out["occ01"] = SM.occlusion_mask(out["flow01"], out["flow10"])
+        rep = SM.view_consistency(fr, fw, bw, offsets=(1, 2), metric="mse", crop=4)
+        out["mse_t"] = np.array([rep.mse_t[1], rep.mse_t[2]])
+        np.savez_compressed(os.path.join(HERE, "io_consistency.npz"), **out)
+        print("consistency:", rep.mse_t, flush=True)
+    jobs["consistency"] = consistency
+
     for name, fn in jobs.items():
         if only and name not in only:
             continue

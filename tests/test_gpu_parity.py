@@ -442,3 +442,40 @@ def test_ply_checkpoint_renders_like_oracle():
     assert out.stats["bin_entries"] == ref["stats"]["bin_entries"] > 0
     np.testing.assert_allclose(out.color, ref["color"], atol=TOL, rtol=0)
     np.testing.assert_allclose(out.transmittance, ref["transmittance"], atol=TOL, rtol=0)
+
+
+def test_consistency_on_device():
+    """consistency.py on CUDA tensors: the reference fixture's flows, warp,
+    occlusion mask and score (as tests/test_consistency.py on the host), and
+    the C5-style sweep rendered by the B200 path scores like the reference's
+    frames (same scene, frames within the 1e-4 pixel bar)."""
+    import os
+    import torch
+    from paper_2402_00525_b200 import Camera, FrameOutput, Hierarchical, RenderConfig
+    from paper_2402_00525_b200 import consistency as C
+    from paper_2402_00525_b200 import scenes
+    from paper_2402_00525_b200.renderer import Renderer
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "io_consistency.npz"))
+    d = {k: z[k] for k in z.files}
+    dev = torch.device("cuda")
+    cams = [Camera(rotation=d[f"R{k}"], position=d[f"pos{k}"], fx=80.0, fy=80.0, width=96,
+                   height=72) for k in range(3)]
+    ref_frames = [FrameOutput(color=d[f"color{k}"], transmittance=d[f"tn{k}"],
+                              depth=d[f"depth{k}"]) for k in range(3)]
+    fl, va = C.analytic_flow(ref_frames[0], cams[0], cams[1], device=dev)
+    assert fl.is_cuda
+    np.testing.assert_allclose(fl.cpu().numpy(), d["flow01"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(va.cpu().numpy(), d["valid01"])
+    # our own frames of the same sweep
+    arrs = scenes.to_f32_scene(scenes.frustum_cloud(2000, 31, 96, 72, 80.0, z_lo=2.0, z_hi=6.0))
+    r = Renderer(arrs, Hierarchical(), RenderConfig(with_depth=True))
+    fr = [r.frame(c) for c in cams]
+    for k in range(3):
+        np.testing.assert_allclose(fr[k].color, d[f"color{k}"], atol=TOL, rtol=0)
+    fw = {(i, j): C.analytic_flow(fr[i], cams[i], cams[j], device=dev)
+          for i in range(3) for j in range(3) if j > i}
+    bw = {(i, j): C.analytic_flow(fr[i], cams[i], cams[j], device=dev)
+          for i in range(3) for j in range(3) if j < i}
+    rep = C.view_consistency(fr, fw, bw, offsets=(1, 2), metric="mse", crop=4, device=dev)
+    np.testing.assert_allclose(rep.mse_t[1], d["mse_t"][0], rtol=0.05, atol=1e-7)
