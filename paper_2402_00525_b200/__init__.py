@@ -31,8 +31,8 @@ def __getattr__(name):
         from . import renderer
         return getattr(renderer, name)
     if name == "consistency":
-        from . import consistency
-        return consistency
+        import importlib
+        return importlib.import_module(".consistency", __name__)
     if name in ("load_ply", "load_ply_arrays", "load_ply_scene", "load_cameras"):
         from . import scene_io
         return getattr(scene_io, name)
