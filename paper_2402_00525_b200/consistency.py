@@ -3,8 +3,8 @@ reference's metrics.py:80-255): analytic flow from rendered depth, bilinear
 backward warping, the forward-backward occlusion test and the
 warp-and-compare consistency score over a trajectory (the C5 popping
 evaluation), as batched torch tensor ops on the frames the renderer already
-holds on the GPU.  The squared-error score is supported; the FLIP score
-(flip.py) is not and raises ConfigError.
+holds on the GPU, with the FLIP perceptual difference (flip.py) restated in
+torch (``flip_error_map``) and the squared-error score.
 
 Functions take numpy arrays or torch tensors and return torch tensors
 (float64) on the input's device unless ``numpy=True``.
@@ -98,6 +98,135 @@ def occlusion_mask(flow_fwd, flow_bwd, rel: float = 0.01, offset: float = 0.5, d
     return (lhs <= rhs + offset) & valid
 
 
+# ---------------------------------------------------------------------------
+# FLIP perceptual difference (flip.py): the colour pipeline (CSF-filtered
+# opponent channels, Hunt-adjusted L*a*b*, HyAB distance redistributed around
+# the green/blue maximum) and the feature pipeline (edge / point detector
+# magnitudes of the achromatic channel), combined as dc ** (1 - df).
+
+_M_SRGB2XYZ = torch.tensor([[0.41238656, 0.35759149, 0.18045049],
+                            [0.21263682, 0.71518298, 0.07218020],
+                            [0.01933062, 0.11919716, 0.95037259]], dtype=torch.float64)
+
+
+def _white(dev):
+    return (_M_SRGB2XYZ.to(dev) @ torch.ones(3, dtype=torch.float64, device=dev))
+
+
+def _lin(img):
+    x = img.clamp(0.0, 1.0)
+    return torch.where(x <= 0.04045, x / 12.92, ((x + 0.055) / 1.055) ** 2.4)
+
+
+def _xyz(rgb):
+    return rgb @ _M_SRGB2XYZ.to(rgb.device).T
+
+
+def _ycxcz(xyz):
+    n = xyz / _white(xyz.device)
+    return torch.stack([116.0 * n[..., 1] - 16.0, 500.0 * (n[..., 0] - n[..., 1]),
+                        200.0 * (n[..., 1] - n[..., 2])], dim=-1)
+
+
+def _ycxcz_to_rgb(v):
+    yn = (v[..., 0] + 16.0) / 116.0
+    xyz = torch.stack([v[..., 1] / 500.0 + yn, yn, yn - v[..., 2] / 200.0], dim=-1)
+    xyz = xyz * _white(v.device)
+    return xyz @ torch.linalg.inv(_M_SRGB2XYZ.to(v.device)).T
+
+
+def _lab_hunt(xyz):
+    n = xyz / _white(xyz.device)
+    d = 6.0 / 29.0
+    f = torch.where(n > d ** 3, torch.sign(n) * n.abs() ** (1.0 / 3.0), n / (3 * d * d) + 4.0 / 29.0)
+    L = 116.0 * f[..., 1] - 16.0
+    s = L / 100.0
+    return torch.stack([L, 500.0 * (f[..., 0] - f[..., 1]) * s,
+                        200.0 * (f[..., 1] - f[..., 2]) * s], dim=-1)
+
+
+def _hyab(a, b):
+    d = a - b
+    return d[..., 0].abs() + torch.sqrt(d[..., 1] ** 2 + d[..., 2] ** 2)
+
+
+def _csf(a1, b1, a2, b2, ppd, dev):
+    r = int(np.ceil(3 * np.sqrt(0.04 / (2 * np.pi ** 2)) * ppd))
+    t = torch.arange(-r, r + 1, dtype=torch.float64, device=dev) / ppd
+    zz = t[None, :] ** 2 + t[:, None] ** 2
+    g = (a1 * np.sqrt(np.pi / b1) * torch.exp(-np.pi ** 2 * zz / b1) +
+         a2 * np.sqrt(np.pi / b2) * torch.exp(-np.pi ** 2 * zz / b2))
+    return g / g.sum()
+
+
+def _detectors(ppd, dev):
+    sd = 0.5 * 0.082 * ppd
+    r = int(np.ceil(3 * sd))
+    t = torch.arange(-r, r + 1, dtype=torch.float64, device=dev)
+    x, y = t[None, :].expand(2 * r + 1, -1), t[:, None].expand(-1, 2 * r + 1)
+    g = torch.exp(-(x * x + y * y) / (2 * sd * sd))
+
+    def unit(k):  # negative lobe sums to -1, positive to +1
+        neg, pos = -k[k < 0].sum(), k[k > 0].sum()
+        return torch.where(k < 0, k / neg, k / pos)
+
+    return unit(-x * g), unit((x * x / (sd * sd) - 1) * g)
+
+
+def _conv(img, k):
+    """scipy.ndimage.convolve(img, k, mode="reflect") for a 2D plane: true
+    convolution, the border mirrored including the edge sample."""
+    ry, rx = k.shape[0] // 2, k.shape[1] // 2
+    h, w = img.shape
+
+    def sym(n, r):
+        i = torch.arange(-r, n + r, device=img.device)
+        m = 2 * n
+        i = torch.remainder(i, m)
+        return torch.where(i >= n, m - 1 - i, i)
+
+    p = img[sym(h, ry)][:, sym(w, rx)]
+    kf = torch.flip(k, dims=(0, 1))
+    return torch.nn.functional.conv2d(p[None, None], kf[None, None])[0, 0]
+
+
+def flip_error_map(a, b, ppd: float = 67.0, device=None):
+    """flip.flip_error_map (flip.py:105-156): per-pixel perceptual difference
+    in [0, 1] of two RGB images in [0, 1], viewed at ``ppd`` pixels/degree."""
+    A, B = _t(a, device), _t(b, device)
+    if A.shape != B.shape or A.dim() != 3 or A.shape[2] != 3:
+        raise ValueError(f"need matching HxWx3 images, got {tuple(A.shape)} and {tuple(B.shape)}")
+    dev = A.device
+    ks = (_csf(1.0, 0.0047, 0.0, 1e-5, ppd, dev), _csf(1.0, 0.0053, 0.0, 1e-5, ppd, dev),
+          _csf(34.1, 0.04, 13.5, 0.025, ppd, dev))
+
+    def colour(img):
+        v = _ycxcz(_xyz(_lin(img)))
+        f = torch.stack([_conv(v[..., c], ks[c]) for c in range(3)], dim=-1)
+        return _lab_hunt(_xyz(_ycxcz_to_rgb(f).clamp(0.0, 1.0)))
+
+    qc, qf, pc, pt = 0.7, 0.5, 0.4, 0.95
+    d = _hyab(colour(A), colour(B))
+    g = _lab_hunt(_xyz(torch.tensor([[[0.0, 1.0, 0.0]]], dtype=torch.float64, device=dev)))
+    bl = _lab_hunt(_xyz(torch.tensor([[[0.0, 0.0, 1.0]]], dtype=torch.float64, device=dev)))
+    cmax = float(_hyab(g, bl).reshape(()) ** qc)
+    dc = d ** qc
+    dc = torch.where(dc < pc * cmax, (pt / (pc * cmax)) * dc,
+                     pt + ((dc - pc * cmax) / (cmax - pc * cmax)) * (1.0 - pt))
+    ke, kp = _detectors(ppd, dev)
+
+    def ach(img):
+        return (_ycxcz(_xyz(_lin(img)))[..., 0] + 16.0) / 116.0
+
+    def mag(y, k):
+        return torch.sqrt(_conv(y, k) ** 2 + _conv(y, k.T) ** 2)
+
+    ya, yb = ach(A), ach(B)
+    df = (torch.maximum((mag(ya, ke) - mag(yb, ke)).abs(), (mag(ya, kp) - mag(yb, kp)).abs())
+          / np.sqrt(2.0)) ** qf
+    return (dc ** (1.0 - df)).clamp(0.0, 1.0)
+
+
 def border_crop(height: int, width: int, crop: int = BORDER_CROP) -> int:
     """metrics.border_crop (metrics.py:128-133)."""
     side = min(height, width)
@@ -114,20 +243,18 @@ class ConsistencyReport:
 
 
 def view_consistency(frames, flows_fwd: dict, flows_bwd: dict, offsets=(1, 7),
-                     metric: str = "mse", crop: int | None = None,
+                     metric: str = "both", crop: int | None = None,
                      device=None) -> ConsistencyReport:
-    """metrics.view_consistency (metrics.py:145-215) with the squared-error
-    score: frame i is compared with frame i+t warped onto it, over the
+    """metrics.view_consistency (metrics.py:145-215), FLIP and / or
+    squared-error scores: frame i is compared with frame i+t warped onto it, over the
     cropped, flow-valid, occlusion-free pixels, after subtracting the
     per-pixel minimum over the sequence (static error cancels)."""
-    if metric in ("flip", "both"):
-        raise ConfigError("the FLIP score is not implemented on the B200 path; use metric='mse'")
-    if metric != "mse":
+    if metric not in ("flip", "mse", "both"):
         raise ConfigError(f"unknown metric {metric!r}")
     cols = [_t(f.color if isinstance(f, FrameOutput) else f, device) for f in frames]
     n = len(cols)
     offsets = (offsets,) if isinstance(offsets, int) else tuple(offsets)
-    mse_t = {}
+    mse_t, flip_t = {}, {}
     for t in offsets:
         if t < 1:
             raise ConfigError(f"offset must be >= 1, got {t}")
@@ -135,7 +262,7 @@ def view_consistency(frames, flows_fwd: dict, flows_bwd: dict, offsets=(1, 7),
             raise ConfigError(f"need at least {t + 1} frames for offset {t}, have {n}")
         h, w = cols[0].shape[:2]
         c = border_crop(h, w) if crop is None else crop
-        maps, masks = [], []
+        maps, fmaps, masks = [], [], []
         for i in range(n - t):
             j = i + t
             flow, fvalid = flows_fwd[(i, j)]
@@ -147,15 +274,19 @@ def view_consistency(frames, flows_fwd: dict, flows_bwd: dict, offsets=(1, 7),
             bw, _ = warp_frame(torch.as_tensor(bvalid, device=cols[0].device).double(), flow)
             m = fvalid & wvalid & usable & (bw > 0.999)
             masks.append(m[c:h - c, c:w - c])
-            maps.append(((cols[i] - warped) ** 2).mean(-1)[c:h - c, c:w - c])
-        if not maps:
-            continue
-        st, ms = torch.stack(maps), torch.stack(masks)
-        minmap = torch.where(ms, st, torch.full_like(st, float("inf"))).min(0).values
-        vals = []
-        for i in range(len(maps)):
-            sel = ms[i] & torch.isfinite(minmap)
-            if bool(sel.any()):
-                vals.append(float((st[i][sel] - minmap[sel]).mean()))
-        mse_t[t] = float(np.mean(vals)) if vals else 0.0
-    return ConsistencyReport(flip_t={}, mse_t=mse_t, frames_used=n)
+            if metric in ("flip", "both"):
+                fmaps.append(flip_error_map(cols[i], warped)[c:h - c, c:w - c])
+            if metric in ("mse", "both"):
+                maps.append(((cols[i] - warped) ** 2).mean(-1)[c:h - c, c:w - c])
+        for mp, out in ((fmaps, flip_t), (maps, mse_t)):
+            if not mp:
+                continue
+            st, ms = torch.stack(mp), torch.stack(masks)
+            minmap = torch.where(ms, st, torch.full_like(st, float("inf"))).min(0).values
+            vals = []
+            for i in range(len(mp)):
+                sel = ms[i] & torch.isfinite(minmap)
+                if bool(sel.any()):
+                    vals.append(float((st[i][sel] - minmap[sel]).mean()))
+            out[t] = float(np.mean(vals)) if vals else 0.0
+    return ConsistencyReport(flip_t=flip_t, mse_t=mse_t, frames_used=n)

@@ -349,8 +349,11 @@ def main(only=None):
         wa, wv = SM.warp_frame(fr[1].color, out["flow01"])
         out["warp01"], out["warpvalid01"] = wa, wv
         out["occ01"] = SM.occlusion_mask(out["flow01"], out["flow10"])
-        rep = SM.view_consistency(fr, fw, bw, offsets=(1, 2), metric="mse", crop=4)
+        rep = SM.view_consistency(fr, fw, bw, offsets=(1, 2), metric="both", crop=4)
         out["mse_t"] = np.array([rep.mse_t[1], rep.mse_t[2]])
+        out["flip_t"] = np.array([rep.flip_t[1], rep.flip_t[2]])
+        from splatsort.flip import flip_error_map
+        out["flip01"] = flip_error_map(fr[0].color, wa)
         np.savez_compressed(os.path.join(HERE, "io_consistency.npz"), **out)
         print("consistency:", rep.mse_t, flush=True)
     jobs["consistency"] = consistency

@@ -53,9 +53,23 @@ def test_view_consistency_mse(fx):
           if j > i}
     bw = {(i, j): (d[f"flow{i}{j}"], d[f"valid{i}{j}"]) for i in range(3) for j in range(3)
           if j < i}
-    rep = C.view_consistency(frames, fw, bw, offsets=(1, 2), metric="mse", crop=4)
+    rep = C.view_consistency(frames, fw, bw, offsets=(1, 2), metric="both", crop=4)
     np.testing.assert_allclose([rep.mse_t[1], rep.mse_t[2]], d["mse_t"], rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose([rep.flip_t[1], rep.flip_t[2]], d["flip_t"], rtol=1e-7,
+                               atol=1e-12)
     with pytest.raises(ConfigError):
-        C.view_consistency(frames, fw, bw, metric="flip")
+        C.view_consistency(frames, fw, bw, metric="psnr")
     with pytest.raises(ConfigError):
         C.view_consistency(frames, fw, bw, offsets=(5,))
+
+
+def test_flip_error_map(fx):
+    """flip.flip_error_map (colour + feature pipelines) == the reference's
+    map for frame 0 against frame 1 warped onto it; symmetric, zero on
+    identical inputs."""
+    d, frames, cams = fx
+    m = C.flip_error_map(d["color0"], d["warp01"]).numpy()
+    np.testing.assert_allclose(m, d["flip01"], rtol=1e-7, atol=1e-9)
+    m2 = C.flip_error_map(d["warp01"], d["color0"]).numpy()
+    np.testing.assert_allclose(m, m2, rtol=1e-12, atol=1e-12)
+    assert float(C.flip_error_map(d["color0"], d["color0"]).abs().max()) == 0.0

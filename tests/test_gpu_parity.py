@@ -477,5 +477,9 @@ def test_consistency_on_device():
           for i in range(3) for j in range(3) if j > i}
     bw = {(i, j): C.analytic_flow(fr[i], cams[i], cams[j], device=dev)
           for i in range(3) for j in range(3) if j < i}
-    rep = C.view_consistency(fr, fw, bw, offsets=(1, 2), metric="mse", crop=4, device=dev)
+    rep = C.view_consistency(fr, fw, bw, offsets=(1, 2), metric="both", crop=4, device=dev)
     np.testing.assert_allclose(rep.mse_t[1], d["mse_t"][0], rtol=0.05, atol=1e-7)
+    np.testing.assert_allclose(rep.flip_t[1], d["flip_t"][0], rtol=0.05, atol=1e-6)
+    m = C.flip_error_map(d["color0"], d["warp01"], device=dev)
+    assert m.is_cuda
+    np.testing.assert_allclose(m.cpu().numpy(), d["flip01"], rtol=1e-7, atol=1e-9)
