@@ -759,6 +759,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
 // ---------------------------------------------------------------------------
 // K3 duplicate.
 
+// GZ: GlobalZ keys (view z from aux) -- a template parameter so the
+// hierarchical instantiation carries no GlobalZ code
+template <bool GZ>
 __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     const SplatRec* __restrict__ recs, const uint64_t* __restrict__ masks,
     const uint32_t* __restrict__ counts,
@@ -797,7 +800,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
         const int b = select_bit64(s_m[wbase + owner], local);
         tx = r.rx0 + b % w;
         ty = r.ry0 + b / w;
-        if (!aux)  // the peak only feeds the t_opt key
+        if (!GZ)  // the peak only feeds the t_opt key
           max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
                     (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
         keep = true;
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     __syncwarp();
     if (keep) {
       // rasterizer.py:343-350: view z (GlobalZ) or t_opt at the 16x16 peak
-      const double depth = aux ? aux[(int64_t)blockIdx.x * kPreThreads + wbase + owner].x
+      const double depth = GZ ? aux[(int64_t)blockIdx.x * kPreThreads + wbase + owner].x
                                : key_rec_at(cam, r, ptx, pty);
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
@@ -996,7 +999,7 @@ void launch_scan(const Frame& f, cudaStream_t s) {
 void launch_duplicate(const Frame& f, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
-  k_duplicate<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
+  (f.globalz ? k_duplicate<true> : k_duplicate<false>)<<<(unsigned)blocks, kPreThreads, 0, s>>>(f.recs, f.masks, f.counts, f.offsets, f.n,
                                                      f.cam,
                                                      f.cfg, f.gw, f.depth_bits, f.id_bits, f.ecap,
                                                      f.globalz ? f.aux : nullptr, f.keys[0]);
