@@ -478,6 +478,9 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
 #ifndef STP_RING
 #define STP_RING 64
 #endif
+#ifndef STP_RANK16
+#define STP_RANK16 1  // batch order by all-pairs ranking (else a bitonic network)
+#endif
 #ifndef STP_READY
 #define STP_READY 16  // consume once every producing sub-tile has this many emits
 #endif
@@ -943,10 +946,26 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
             d = INFINITY;
             id = kNoId;
           }
+#if STP_RANK16
+          // position of (d, id) among its half's candidates: 16 independent
+          // shuffle + compare rounds instead of a 10-stage bitonic network
+          // (the dependency chain, not the instruction count, was the cost)
+          int rank = 0;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const double od = __shfl_sync(kFull, d, jj, 16);
+            const uint32_t oi = __shfl_sync(kFull, id, jj, 16);
+            rank += lt(od, oi, d, id);
+          }
+          dS0 = dS1 = d;
+          iS0 = iS1 = id;
+          xS0 = xS1 = rank;
+#else
           half_sort16(d, id, L);
           dS0 = dS1 = d;
           iS0 = iS1 = id;
           xS0 = xS1 = L;
+#endif
           vS0 = (h == 0) && L < nkA;
           vS1 = (h == 1) && L < nkB;
         } else {
