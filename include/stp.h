@@ -97,6 +97,11 @@ typedef struct {
   int32_t record_cap;       /* per-pixel blend-record capacity, 0 = off    */
   int32_t flags;            /* STP_FLAG_*                                  */
   int32_t sort_mode;        /* STP_MODE_* (rasterizer.py:89 SortMode)      */
+  int32_t tile_begin;       /* K6 renders tiles [tile_begin, tile_end) only */
+  int32_t tile_end;         /*   (row-major tile ids; 0, 0 = every tile):   */
+                            /*   a band of a view split across GPUs; K1-K5 */
+                            /*   run for the whole view, only the band's   */
+                            /*   pixels are written                        */
 } StpConfig;
 
 /* Sort modes.  HIERARCHICAL: per-tile t_opt keys + the 3-level resort

@@ -60,7 +60,8 @@ class StpConfig(ctypes.Structure):
                 ("b_head", ctypes.c_int32), ("mid_depth_at_center", ctypes.c_int32),
                 ("with_depth", ctypes.c_int32), ("exact_culling", ctypes.c_int32),
                 ("record_cap", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("sort_mode", ctypes.c_int32)]
+                ("sort_mode", ctypes.c_int32), ("tile_begin", ctypes.c_int32),
+                ("tile_end", ctypes.c_int32)]
 
 
 class StpOutputs(ctypes.Structure):

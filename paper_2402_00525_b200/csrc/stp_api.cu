@@ -3,6 +3,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <algorithm>
+
 #include "stp_common.cuh"
 
 namespace stp {
@@ -107,6 +109,8 @@ int cfg_check(const StpConfig* c) {
     return STP_ERR_CONFIG;
   if (!(c->alpha_cap > 0.0 && c->alpha_cap < 1.0)) return STP_ERR_CONFIG;
   if (c->record_cap < 0) return STP_ERR_CONFIG;
+  if (c->tile_end > 0 && (c->tile_begin < 0 || c->tile_begin >= c->tile_end))
+    return STP_ERR_CONFIG;
   if (c->sort_mode == STP_MODE_GLOBALZ || c->sort_mode == STP_MODE_FULL) return STP_OK;
   // Window(size): validate_mode (rasterizer.py:96-98) + the register window
   if (c->sort_mode == STP_MODE_WINDOW) return (c->q_head >= 1 && c->q_head <= 16) ? STP_OK
@@ -142,8 +146,14 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   f.aux = reinterpret_cast<double2*>(b + L.aux);
   f.globalz = cfg->sort_mode == STP_MODE_GLOBALZ ? 1 : 0;
   f.sort_mode = cfg->sort_mode;
-  f.exact_only =
-      ((cfg->flags & STP_FLAG_FAST32) && cfg->sort_mode == STP_MODE_HIERARCHICAL) ? 0 : 1;
+  f.tile0 = 0;
+  f.tile1 = L.n_tiles;
+  if (cfg->tile_end > 0) {
+    f.tile0 = std::max(0, std::min(cfg->tile_begin, L.n_tiles));
+    f.tile1 = std::max(f.tile0, std::min(cfg->tile_end, L.n_tiles));
+  }
+  f.exact_only = ((cfg->flags & STP_FLAG_FAST32) && cfg->sort_mode == STP_MODE_HIERARCHICAL &&
+                  cfg->tile_end <= 0) ? 0 : 1;
   f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);

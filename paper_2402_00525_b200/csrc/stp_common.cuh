@@ -462,6 +462,7 @@ struct Frame {
   double2* aux;           // per Gaussian (view z, |mean - origin|), GlobalZ only
   int globalz;            // sort mode GlobalZ (view-z keys, ordered blend)
   int sort_mode;          // STP_MODE_*
+  int tile0, tile1;       // K6 tile band [tile0, tile1)
   DevCam* camp;           // device copy of `cam` (written by K0)
   uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;

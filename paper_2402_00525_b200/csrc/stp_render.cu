@@ -115,6 +115,7 @@ struct RenderArgs {
   DevCam cam;
   DevCfg cfg;
   int gw, n_items;
+  int tile0;              // first tile of the band (items are band-relative)
   float log_eps;
   StpOutputs out;
   unsigned long long* counters;
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
       unsigned long long* slot = sm_ring + (tl & 15);
       if (pair == 0) {
         const int g = (int)atomicAdd(A.counters + C_TILE, 1ull);
-        const int gt = g < A.n_items ? g : -1;
+        const int gt = g < A.n_items ? g + A.tile0 : -1;
         atomicExch(slot, (tl << 32) | (unsigned long long)(gt + 2));
         tile = gt;
       } else {
@@ -1190,6 +1191,7 @@ constexpr int kGzThreads = 256;
 
 struct GzArgs {
   int xm;          // XM_* (runtime: the GlobalZ kernel is not register bound)
+  int tile0;       // first tile of the band; n_tiles = band length
   DevGrads grad;
   const SplatRec* __restrict__ recs;
   const uint32_t* __restrict__ vals;
@@ -1219,7 +1221,8 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
   R.counters = A.counters;
   R.grad = A.grad;
   const bool need_t = A.cfg.rec_cap > 0 || A.xm == XM_SERR;
-  for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+  for (int band = blockIdx.x; band < A.n_tiles; band += gridDim.x) {
+    const int tile = band + A.tile0;
     const int tx = tile % A.gw, ty = tile / A.gw;
     const int gx = tx * kTile + (tid & 15), gy = ty * kTile + (tid >> 4);
     const bool in_img = gx < A.cam.W && gy < A.cam.H;
@@ -1321,10 +1324,11 @@ static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStr
   A.cam = f.cam;
   A.cfg = f.cfg;
   A.gw = f.gw;
-  A.n_tiles = f.n_tiles;
+  A.tile0 = f.tile0;
+  A.n_tiles = f.tile1 - f.tile0;
   A.out = out;
   A.counters = f.counters;
-  if (f.n_tiles > 0) k_render_globalz<<<f.n_tiles, kGzThreads, 0, s>>>(A);
+  if (A.n_tiles > 0) k_render_globalz<<<A.n_tiles, kGzThreads, 0, s>>>(A);
 }
 
 // ---------------------------------------------------------------------------
@@ -1370,7 +1374,8 @@ __global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
   const int qh_rt = A.cfg.q_head;  // Window: the window size
   const double term = A.cfg.term;
   const int lane = threadIdx.x & 31;
-  for (int tile = blockIdx.x; tile < A.n_items; tile += gridDim.x) {
+  for (int band = blockIdx.x; band < A.n_items; band += gridDim.x) {
+    const int tile = band + A.tile0;
     const int tx = tile % A.gw, ty = tile / A.gw;
     Pixel P;
     {
@@ -1500,7 +1505,8 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.cam = f.cam;
   A.cfg = f.cfg;
   A.gw = f.gw;
-  A.n_items = f.n_tiles;
+  A.tile0 = f.tile0;
+  A.n_items = f.tile1 - f.tile0;
   A.out = out;
   A.counters = f.counters;
   A.list = nullptr;

@@ -113,3 +113,48 @@ def device_render_fn(scene: dict, mode=None, cfg=None, device=None) -> Callable:
         return outs
 
     return fn
+
+
+# ---------------------------------------------------------------------------
+# One view split across GPUs (the C4 latency option): every
+# rank runs K1-K5 for the whole view (redundant, cheap next to K6) and K6 for
+# a band of tile rows; the bands are then all-gathered so every rank (or rank
+# 0) holds the frame.  The band is the only exchange and happens after the
+# render, not inside it.
+
+def band_rows(grid_h: int, world: int, rank: int) -> tuple[int, int]:
+    """Tile rows [r0, r1) of ``rank``: contiguous, sizes differ by at most one."""
+    return (rank * grid_h) // world, ((rank + 1) * grid_h) // world
+
+
+def band_tiles(grid_w: int, grid_h: int, world: int, rank: int) -> tuple[int, int]:
+    """Row-major tile ids [t0, t1) of ``rank``'s band (whole tile rows)."""
+    r0, r1 = band_rows(grid_h, world, rank)
+    return r0 * grid_w, r1 * grid_w
+
+
+def gather_band_frame(outs: dict, width: int, height: int, world: int, rank: int,
+                      tile: int = 16, group=None, keys=("color", "transmittance", "depth")) -> dict:
+    """All-gather the band pixels rendered by each rank into full frames
+    (in place in ``outs``).  Bands are whole tile rows, i.e. contiguous
+    image rows [16 r0, min(16 r1, H))."""
+    gh = (height + tile - 1) // tile
+    if not dist.is_initialized() or world == 1:
+        return outs
+    for k in keys:
+        t = outs.get(k)
+        if t is None:
+            continue
+        rows = [(min(band_rows(gh, world, q)[0] * tile, height),
+                 min(band_rows(gh, world, q)[1] * tile, height)) for q in range(world)]
+        # all_gather needs equal sizes: pad every band to the largest
+        hmax = max(b - a for a, b in rows)
+        shape = (hmax,) + tuple(t.shape[1:])
+        a, b = rows[rank]
+        mine = torch.zeros(shape, dtype=t.dtype, device=t.device)
+        mine[: b - a] = t[a:b]
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+        for q, (a, b) in enumerate(rows):
+            t[a:b] = parts[q][: b - a]
+    return outs

@@ -184,7 +184,7 @@ def make_camera(cam) -> _lib.StpCamera:
 
 
 def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = False,
-                fast32: bool = False, fb_test: bool = False):
+                fast32: bool = False, fb_test: bool = False, tiles=None):
     c = _lib.StpConfig()
     c.eps = float(cfg.opacity_eps)
     c.termination = float(cfg.termination)
@@ -206,6 +206,8 @@ def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = Fa
                    "Window": _lib.STP_MODE_WINDOW}.get(name, _lib.STP_MODE_HIERARCHICAL)
     if name == "Window":
         c.q_head = int(mode.size)  # the window size (stp.h STP_MODE_WINDOW)
+    if tiles is not None:          # K6 tile band [t0, t1) (multi-GPU view split)
+        c.tile_begin, c.tile_end = int(tiles[0]), int(tiles[1])
     c.with_depth = int(bool(cfg.with_depth))
     c.exact_culling = int(bool(cfg.exact_culling(mode)))
     c.record_cap = int(record_cap)
@@ -325,12 +327,15 @@ class Renderer:
         self.ws.ensure(self.scene.n, cam.width, cam.height, guess)
 
     def render_into(self, cam, outs: dict, stats: bool = False, timings: bool = False,
-                    record_cap: int = 0, stream=None):
+                    record_cap: int = 0, stream=None, tiles=None):
         """One view into preallocated device outputs.  Returns StpStats when
-        ``stats`` (synchronising), else None (asynchronous)."""
+        ``stats`` (synchronising), else None (asynchronous).  ``tiles`` =
+        (t0, t1) renders only that band of row-major tile ids (the pixels of
+        the other tiles are left untouched)."""
         c_cam = make_camera(cam)
         self._ensure(cam)
-        c_cfg = make_config(self.cfg, self.mode, record_cap, timings, self.fast32, self.fb_test)
+        c_cfg = make_config(self.cfg, self.mode, record_cap, timings, self.fast32, self.fb_test,
+                            tiles)
         c_out = self.outputs_struct(outs)
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         st = _lib.StpStats() if stats else None

@@ -483,3 +483,31 @@ def test_consistency_on_device():
     m = C.flip_error_map(d["color0"], d["warp01"], device=dev)
     assert m.is_cuda
     np.testing.assert_allclose(m.cpu().numpy(), d["flip01"], rtol=1e-7, atol=1e-9)
+
+
+@pytest.mark.parametrize("mode_name", ["hierarchical", "globalz", "window:8"])
+def test_tile_band_rendering(mode_name):
+    """A view split into tile-row bands (multiview.band_tiles; StpConfig
+    tile_begin/tile_end): rendering every band into the same buffers equals
+    the whole-view render bit for bit, and a band leaves the other pixels
+    untouched."""
+    import torch
+    from paper_2402_00525_b200 import RenderConfig, multiview, parse_mode, scenes
+    from paper_2402_00525_b200.renderer import Renderer
+    arrs = scenes.to_f32_scene(scenes.garden_scene(60_000, 3))
+    cam = scenes.orbit_cameras(8, width=320, height_px=180, f=183.0)[4]
+    r = Renderer(arrs, parse_mode(mode_name), RenderConfig(with_depth=True))
+    full = r.alloc_outputs(cam.width, cam.height)
+    r.render_into(cam, full, stats=True)
+    gw, gh = (cam.width + 15) // 16, (cam.height + 15) // 16
+    world = 3
+    band = {k: torch.full_like(v, -1.0) for k, v in full.items()}
+    for q in range(world):
+        t0, t1 = multiview.band_tiles(gw, gh, world, q)
+        r.render_into(cam, band, stats=True, tiles=(t0, t1))
+        if q == 0:   # only band 0's rows are written so far
+            y1 = min(16 * multiview.band_rows(gh, world, 0)[1], cam.height)
+            assert bool((band["transmittance"][y1:] == -1.0).all())
+    torch.cuda.synchronize()
+    for k in full:
+        assert torch.equal(band[k], full[k]), k

@@ -97,3 +97,51 @@ def test_gloo_two_ranks_equal_serial():
         np.testing.assert_array_equal(gathered[v]["transmittance"], ref["transmittance"].numpy())
     # the scene is visible in at least some views (not a vacuous comparison)
     assert any((gathered[v]["transmittance"] < 0.999).any() for v in gathered)
+
+
+@pytest.mark.parametrize("gh,world", [(68, 2), (68, 8), (135, 8), (3, 8), (1, 2)])
+def test_band_partition(gh, world):
+    rows = [multiview.band_rows(gh, world, r) for r in range(world)]
+    assert rows[0][0] == 0 and rows[-1][1] == gh
+    assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    assert max(b - a for a, b in rows) - min(b - a for a, b in rows) <= 1
+    assert multiview.band_tiles(120, gh, world, world - 1)[1] == 120 * gh
+
+
+def _band_worker(rank, world, port, q):
+    """Each rank 'renders' only its band (a copy of the oracle frame inside
+    the band, garbage elsewhere) and the all-gather assembles the frame."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, cams = _scene_and_cams()
+        full = _oracle_fn({k: torch.from_numpy(v) for k, v in sc.items()})(cams[1], 1)
+        H, W = full["transmittance"].shape
+        gh = (H + 15) // 16
+        r0, r1 = multiview.band_rows(gh, world, rank)
+        outs = {k: torch.full_like(v, -7.0) for k, v in full.items()}
+        a, b = min(16 * r0, H), min(16 * r1, H)
+        for k in outs:
+            outs[k][a:b] = full[k][a:b]
+        multiview.gather_band_frame(outs, W, H, world, rank, keys=tuple(outs))
+        q.put((rank, {k: v.numpy() for k, v in outs.items()},
+               {k: v.numpy() for k, v in full.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_band_gather():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got, full in res:
+        for k in full:
+            np.testing.assert_array_equal(got[k], full[k])
