@@ -482,6 +482,10 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
 #ifndef STP_RANK16
 #define STP_RANK16 1  // batch order by all-pairs ranking (else a bitonic network)
 #endif
+#ifndef STP_RANK_UNROLL
+#define STP_RANK_UNROLL 4  // measured equal to 16, less code
+#endif
+constexpr int kRankUnroll = STP_RANK_UNROLL;
 #ifndef STP_READY
 #define STP_READY 16  // consume once every producing sub-tile has this many emits
 #endif
@@ -952,7 +956,7 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
           // shuffle + compare rounds instead of a 10-stage bitonic network
           // (the dependency chain, not the instruction count, was the cost)
           int rank = 0;
-#pragma unroll
+#pragma unroll kRankUnroll
           for (int jj = 0; jj < 16; ++jj) {
             const double od = __shfl_sync(kFull, d, jj, 16);
             const uint32_t oi = __shfl_sync(kFull, id, jj, 16);
