@@ -711,9 +711,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partials(const uint32_t* 
   __shared__ uint32_t s_warp[32];
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t sum = 0;
+  if (base + kScanItems <= n) {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (base + k < n) sum += counts[base + k];
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const uint4 c = *reinterpret_cast<const uint4*>(counts + base + 4 * q);
+      sum += c.x + c.y + c.z + c.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (base + k < n) sum += counts[base + k];
+  }
   uint32_t total;
   block_excl_scan(sum, s_warp, total);
   if (threadIdx.x == 0) partials[blockIdx.x] = total;
@@ -742,17 +750,41 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   uint32_t sum = 0;
+  // a thread's 16 counts are one 64-B run: 128-bit loads and stores where
+  // the run is whole (the arrays are 16-B aligned)
+  const bool whole = base + kScanItems <= n;
+  if (whole) {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (base + k < n) ? counts[base + k] : 0;
-    sum += v[k];
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      const uint4 c = *reinterpret_cast<const uint4*>(counts + base + 4 * q);
+      v[4 * q] = c.x;
+      v[4 * q + 1] = c.y;
+      v[4 * q + 2] = c.z;
+      v[4 * q + 3] = c.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = (base + k < n) ? counts[base + k] : 0;
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) sum += v[k];
   uint32_t total;
   uint32_t run = block_excl_scan(sum, s_warp, total) + partials[blockIdx.x];
+  uint32_t o[kScanItems];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) offsets[base + k] = run;
+    o[k] = run;
     run += v[k];
+  }
+  if (whole) {
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q)
+      *reinterpret_cast<uint4*>(offsets + base + 4 * q) =
+          make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (base + k < n) offsets[base + k] = o[k];
   }
 }
 
