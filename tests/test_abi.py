@@ -105,6 +105,25 @@ def test_validate_config_rejects(lib, field, value):
     assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_ERR_CONFIG
 
 
+def test_validate_config_modes_and_bands(lib):
+    """Sort modes (GlobalZ / FullPerPixel / Window <= 16) and K6 tile bands
+    through the host-side config check (no device work)."""
+    from paper_2402_00525_b200 import FullPerPixel, GlobalZ, Window
+    from paper_2402_00525_b200.renderer import make_config
+    for m in (GlobalZ(), FullPerPixel(), Window(1), Window(8), Window(16)):
+        c = make_config(RenderConfig(), m)
+        assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_OK, m
+    c = make_config(RenderConfig(), Window(17))
+    assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_ERR_CONFIG
+    c = _cfg()
+    c.sort_mode = 7
+    assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_ERR_CONFIG
+    for band, ok in (((0, 10), True), ((5, 5), False), ((-1, 4), False), ((0, 0), True)):
+        c = make_config(RenderConfig(), Hierarchical(), tiles=band)
+        want = _lib.STP_OK if ok else _lib.STP_ERR_CONFIG
+        assert lib.stp_validate_config(ctypes.byref(c)) == want, band
+
+
 def test_validate_config_alpha_cap(lib):
     c = _cfg()
     for bad in (0.0, 1.0, 1.5):
