@@ -39,7 +39,10 @@ namespace stp {
 #ifndef STP_EXACT_MINB
 #define STP_EXACT_MINB 4
 #endif
-constexpr int kWarpsPerBlock = 4;
+#ifndef STP_WARPS_PER_BLOCK
+#define STP_WARPS_PER_BLOCK 4
+#endif
+constexpr int kWarpsPerBlock = STP_WARPS_PER_BLOCK;
 constexpr int kRenderThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kNoId = 0xffffffffu;
 
