@@ -12,7 +12,9 @@ by an NCCL broadcast from rank 0.
     python bench.py [--gpus N --steps K --warmup W]           # this framework
     python bench.py --impl reference [...]                     # CPU oracle arm
 
-Prints ONE JSON line (rank 0).
+``--gpus N`` without a torchrun environment spawns N ranks itself (one
+process per GPU, 127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal
+N.  Prints ONE JSON line (rank 0).
 """
 
 from __future__ import annotations
@@ -21,6 +23,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,8 +41,11 @@ WORKLOADS = {
     "C2": "C2: synthetic 1M Gaussians (SH3), single 1920x1080 view",
     "C3": "C3: synthetic 3M-Gaussian garden-scale scene (SH3), 256-view 1920x1080 orbit",
     "C4": "C4: synthetic 6M Gaussians (SH3) at 3840x2160, culling / queue stress",
-    "C5": "C5: synthetic 1.5M half-density scene (SH3), 1080p rotation sweep",
+    "C5": "C5: synthetic 1.5M half-density scene (SH3), 1080p fixed-position yaw sweep",
 }
+KERNELS = ("K0 init", "K1 preprocess", "K2 scan", "K3 duplicate", "K4 sort", "K5 ranges",
+           "K6 render")
+STAGES = ("K0+K1 preprocess", "K2+K3 scan+duplicate", "K4+K5 sort+ranges", "K6 render")
 
 
 def parse():
@@ -50,13 +56,11 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="C3")
     p.add_argument("--mode", default="hierarchical",
-                   help="sort mode: hierarchical (the paper's pipeline, default) or globalz "
-                        "(the 3DGS baseline order, for the paper's A/B)")
+                   help="sort mode: hierarchical (the paper's pipeline, default), globalz "
+                        "(the 3DGS baseline order), full, window:k")
     p.add_argument("--gaussians", type=int, default=None, help="override N (debug)")
     p.add_argument("--views", type=int, default=256)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--fast32", action="store_true",
-                   help="K6 via the fp32-state certified kernel (A/B against the float64 one)")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--streams", type=int, default=2,
                    help="views in flight per GPU (one workspace + stream each): the next "
@@ -79,9 +83,13 @@ def peaks():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
 class ClockSampler:
@@ -128,33 +136,57 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def b_alg(n, sh_k, n_v, e, p, with_depth=False):
-    """SURVEY.md 8(d) algorithmic bytes of one view and of the K6 launch."""
+def kernel_bytes(n, sh_k, n_v, e, p, n_tiles, with_depth=False):
+    """Algorithmic HBM bytes per launch of each kernel (80 B
+    splat record written once / read once, a 12 B (key, value) entry pair
+    touched 4x, 16-20 B per output pixel)."""
     out_px = 20 if with_depth else 16
-    view = n * 4 * (11 + 3 * sh_k) + 2 * 80 * n_v + 48 * e + out_px * p
-    k6 = 80 * n_v + 12 * e + out_px * p
-    return view, k6
+    return {
+        "K0 init": 8 * n_tiles,                                   # tile ranges reset
+        "K1 preprocess": n * 4 * (11 + 3 * sh_k) + 80 * n_v + 4 * n,   # scene read, record + count write
+        "K2 scan": 8 * n,                                         # counts read, offsets write
+        "K3 duplicate": 80 * n_v + 12 * e,                        # record read, entry write
+        "K4 sort": 24 * e,                                        # entries read + written once
+        "K5 ranges": 12 * e + 8 * n_tiles,                        # sorted keys read, ids + ranges written
+        "K6 render": 80 * n_v + 12 * e + out_px * p,              # records + entries read, pixels written
+    }
+
+
+def view_bytes(n, sh_k, n_v, e, p, with_depth=False):
+    """SURVEY.md 8(d) B_alg of one view."""
+    out_px = 20 if with_depth else 16
+    return n * 4 * (11 + 3 * sh_k) + 2 * 80 * n_v + 48 * e + out_px * p
+
+
+def config_dict(args, n, W, H, n_views, mode_nm):
+    """The same config for both arms (the driver compares them)."""
+    return {"workload": WORKLOADS[args.config.upper()], "gaussians": int(n), "width": int(W),
+            "height": int(H), "views": int(n_views), "mode": mode_nm,
+            "views_per_step_per_gpu": 1,
+            "l2": "inputs larger than L2 (scene > 126 MB, per-view records/entries > 126 MB)"}
 
 
 # ----------------------------------------------------------------------------
 # reference arm: the reference's algorithm on the host cores (oracle port)
 
-def cpu_view_rate(scene, cams, views, budget_s, threads, mode=None):
+def cpu_view_rate(scene, cams, views, budget_s, threads, mode=None, keep_first=False):
     """Full views (project + bin_and_sort + render of every tile under the
     sort mode, hierarchical by default) of the C++ restatement of the
     reference, all host threads."""
     import oracle
     from paper_2402_00525_b200 import Hierarchical, RenderConfig
     mode = mode if mode is not None else Hierarchical()
-    times = []
+    times, first = [], None
     t_all = time.perf_counter()
     for v in views:
         t0 = time.perf_counter()
-        oracle.render(scene, cams[v], RenderConfig(), mode, threads=threads)
+        out = oracle.render(scene, cams[v], RenderConfig(), mode, threads=threads)
         times.append(time.perf_counter() - t0)
+        if keep_first and first is None:
+            first = out
         if time.perf_counter() - t_all > budget_s:
             break
-    return len(times) / sum(times), len(times), times
+    return len(times) / sum(times), len(times), times, first
 
 
 def run_reference(args):
@@ -162,21 +194,22 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2402_00525_b200 import scenes
-    scene, cams = scenes.config_scene(args.config, n=args.gaussians, n_views=args.views)
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     from paper_2402_00525_b200.types import mode_name, parse_mode
+    scene, cams = scenes.config_scene(args.config, n=args.gaussians, n_views=args.views)
+    threads = host_threads()
     mode = parse_mode(args.mode)
-    # warmup (bounded: at most 2 views)
-    cpu_view_rate(scene, cams, list(range(min(args.warmup, 2))), 1e9, threads, mode)
-    views = [s % len(cams) for s in range(args.steps)]
-    rate, done, times = cpu_view_rate(scene, cams, views, args.cpu_seconds, threads, mode)
+    warm = min(args.warmup, 2)
+    cpu_view_rate(scene, cams, list(range(warm)), 1e9, threads, mode)   # bounded warmup
+    # the views our arm times: rank 0's views after its warmup
+    views = [(args.warmup + s) * args.gpus % len(cams) for s in range(args.steps)]
+    rate, done, times, _ = cpu_view_rate(scene, cams, views, args.cpu_seconds, threads, mode)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws,
-        "steps": done, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 / rate,
+        "steps": done, "warmup": warm, "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOADS[args.config.upper()], "gaussians": len(scene["opacity"]),
-                                        "width": cams[0].width, "height": cams[0].height,
-                                        "views": len(cams), "mode": mode_name(mode)},
+        "data": "synthetic (seeded scene generator, paper_2402_00525_b200/scenes.py)",
+        "config": config_dict(args, len(scene["opacity"]), cams[0].width, cams[0].height,
+                              len(cams), mode_name(mode)),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{done} full {args.config.upper()} views (project + bin_and_sort + "
                                    f"{mode_name(mode)} render of all tiles) by oracle/stp_oracle.cpp, "
@@ -191,12 +224,42 @@ def run_reference(args):
 # ----------------------------------------------------------------------------
 # our arm
 
+def _profile_json(name):
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def frame_parity(r, gpu_out, cam, ref):
+    """GPU frame (benched path) vs the oracle frame of the same view."""
+    tile, gid, _ = r.debug_bins(cam)
+    src = ref["batch"].source_index
+    rank = np.searchsorted(src, gid)
+    t_ref, s_ref = ref["bins"][0], ref["bins"][1]
+    tiles_equal = bool(len(tile) == len(t_ref) and np.array_equal(tile, t_ref))
+    order_equal = bool(tiles_equal and np.array_equal(rank, s_ref))
+    col = gpu_out["color"].double().cpu().numpy()
+    tn = gpu_out["transmittance"].double().cpu().numpy()
+    return {"max_abs_color": float(np.abs(col - ref["color"]).max()),
+            "max_abs_transmittance": float(np.abs(tn - ref["transmittance"]).max()),
+            "tiles_equal": tiles_equal, "order_equal": order_equal,
+            "entries": int(len(t_ref)), "pixels": int(col.shape[0] * col.shape[1]),
+            "tolerance": 1e-4,
+            "pass": bool(tiles_equal and order_equal and
+                         float(np.abs(col - ref["color"]).max()) <= 1e-4 and
+                         float(np.abs(tn - ref["transmittance"]).max()) <= 1e-4)}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2402_00525_b200 import Hierarchical, RenderConfig, _lib, scenes
-    from paper_2402_00525_b200.renderer import GaussianScene, Renderer, make_camera, make_config
+    from paper_2402_00525_b200 import RenderConfig, _lib, scenes
+    from paper_2402_00525_b200.renderer import (GaussianScene, Renderer, Workspace, make_camera,
+                                                make_config)
     from paper_2402_00525_b200.types import mode_name, parse_mode
 
     world, rank, local = dist_env()
@@ -232,7 +295,7 @@ def run_ours(args):
     gs = GaussianScene(dev_t["means"], dev_t["quats"], dev_t["scales"], dev_t["opacity"],
                        dev_t["sh"], dev)
     mode, cfg = parse_mode(args.mode), RenderConfig()
-    r = Renderer(gs, mode, cfg, dev, fast32=args.fast32)
+    r = Renderer(gs, mode, cfg, dev)
     lib = _lib.load()
     W, H = cams[0].width, cams[0].height
     n_views = len(cams)
@@ -244,48 +307,51 @@ def run_ours(args):
     stat = {}
     for v in sorted(set(my_views)):
         st = r.render_into(cams[v], outs, stats=True)
-        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles), int(st.exact_items),
-                   int(st.resolves))
+        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles))
     need = max(s_[1] for s_ in stat.values())
     r.ws.ensure(gs.n, W, H, int(need * 1.1) + 4096)
 
-    # views in flight: one (stream, workspace, output buffers) per slot
-    from paper_2402_00525_b200.renderer import Workspace
+    # views in flight: one (stream, workspace, output buffers, status word) per slot
     n_str = max(1, args.streams)
     streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(n_str - 1)]
-    wss, c_outs, keep = [r.ws], [r.outputs_struct(outs)], [outs]
+    wss, c_outs, keep = [r.ws], [], [outs]
     for _ in range(n_str - 1):
         w_ = Workspace(dev)
         w_.ensure(gs.n, W, H, int(need * 1.1) + 4096)
-        o_ = r.alloc_outputs(W, H)
         wss.append(w_)
-        c_outs.append(r.outputs_struct(o_))
-        keep.append(o_)
+        keep.append(r.alloc_outputs(W, H))
+    # per-step device status words (StpOutputs.status): every timed frame's
+    # overflow report, checked after the timed region
+    status = torch.zeros((steps + warm, 2), dtype=torch.int64, device=dev)
+    for k in range(n_str):
+        c_outs.append(r.outputs_struct(keep[k]))
     c_scene = r.c_scene
-    c_cfg = make_config(cfg, mode, fast32=args.fast32)
-    c_out = c_outs[0]
+    c_cfg = make_config(cfg, mode)
     c_cams = [make_camera(c) for c in cams]
-    stream = streams[0]
     s_ptrs = [ctypes.c_void_p(st.cuda_stream) for st in streams]
-    n_ev = 5 * steps + 2
+    NE = _lib.STP_KERNEL_EVENTS
+    n_ev = NE * min(steps, 16)
     ev = (ctypes.c_void_p * n_ev)()
     assert lib.stp_events_create(n_ev, ev) == 0
+    launches = [0]
 
-    def one(v, events=None, slot=0):
+    def one(v, step, slot=0, events=None):
+        co = c_outs[slot]
+        co.status = status[step].data_ptr()
         ws_ = wss[slot]
         if events is None:
             rc = lib.stp_render(ctypes.byref(c_scene), ctypes.byref(c_cams[v]), ctypes.byref(c_cfg),
-                                ctypes.c_void_p(ws_.ptr), ws_.nbytes, ctypes.byref(c_outs[slot]),
+                                ctypes.c_void_p(ws_.ptr), ws_.nbytes, ctypes.byref(co),
                                 None, s_ptrs[slot])
         else:
             rc = lib.stp_render_events(ctypes.byref(c_scene), ctypes.byref(c_cams[v]),
                                        ctypes.byref(c_cfg), ctypes.c_void_p(ws_.ptr), ws_.nbytes,
-                                       ctypes.byref(c_outs[slot]), events, s_ptrs[slot])
+                                       ctypes.byref(co), events, NE, s_ptrs[slot])
         if rc != 0:
             raise RuntimeError(f"stp_render failed: {_lib.error_string(rc)}")
 
     for s in range(warm):
-        one(my_views[s], slot=s % n_str)
+        one(my_views[s], s, slot=s % n_str)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -294,17 +360,15 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     t_wall = time.perf_counter()
-    # stage events of every timed view on its own stream; the region runs from
-    # an event on stream 0 that every stream waits for to an event on stream 0
-    # that waits for every stream
+    # the region runs from an event on stream 0 that every stream waits for
+    # to an event on stream 0 that waits for every stream
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(streams[0])
     for st in streams[1:]:
         st.wait_event(t_start)
     for s in range(steps):
-        evs = (ctypes.c_void_p * 5)(*ev[5 * s: 5 * s + 5])
-        one(my_views[warm + s], evs, slot=s % n_str)
+        one(my_views[warm + s], warm + s, slot=s % n_str)
     for st in streams[1:]:
         j = torch.cuda.Event()
         j.record(st)
@@ -315,6 +379,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    st_codes = status[:, 0].cpu().numpy()
+    if (st_codes != 0).any():
+        raise RuntimeError(f"timed frames reported status {sorted(set(st_codes.tolist()))} "
+                           "(entry overflow): the measurement is invalid")
 
     def el(a, b):
         ms = ctypes.c_float()
@@ -322,19 +390,16 @@ def run_ours(args):
         return ms.value
 
     total_ms = t_start.elapsed_time(t_end)
-    if n_str > 1:
-        # with several views in flight the per-view stage events overlap: the
-        # per-kernel times (stage_ms, roofline) come from a separate pass with
-        # one view at a time on stream 0 (outside the timed region)
-        n_stage = min(steps, 16)
-        for s in range(n_stage):
-            evs = (ctypes.c_void_p * 5)(*ev[5 * s: 5 * s + 5])
-            one(my_views[warm + s], evs, slot=0)
-        torch.cuda.synchronize()
-    else:
-        n_stage = steps
-    stage = np.array([[el(ev[5 * s + i], ev[5 * s + i + 1]) for i in range(4)]
-                      for s in range(n_stage)])
+    # per-kernel times (CUDA events at every kernel boundary, on the launching
+    # stream): a separate pass with one view at a time outside the timed
+    # region, because with several views in flight the intervals overlap
+    n_stage = min(steps, 16)
+    for s in range(n_stage):
+        evs = (ctypes.c_void_p * NE)(*ev[NE * s: NE * s + NE])
+        one(my_views[warm + s], warm + s, slot=0, events=evs)
+    torch.cuda.synchronize()
+    kms = np.array([[el(ev[NE * s + i], ev[NE * s + i + 1]) for i in range(NE - 1)]
+                    for s in range(n_stage)])
     lib.stp_events_destroy(n_ev, ev)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -342,38 +407,47 @@ def run_ours(args):
     max_ms = float(t.item())
     value = world * steps / (max_ms / 1e3)
 
-    # roofline of the dominant kernel (K6 hierarchical render) and of the view
-    stage_mean = stage.mean(axis=0)
+    # rooflines: per kernel (algorithmic bytes / event-timed duration) and the view
+    kmean = kms.mean(axis=0)
+    stage_mean = [kmean[0] + kmean[1], kmean[2] + kmean[3], kmean[4] + kmean[5], kmean[6]]
     timed_views = my_views[warm:warm + n_stage]
-    n_v = np.mean([stat[v][0] for v in timed_views])
-    e = np.mean([stat[v][1] for v in timed_views])
+    n_v = float(np.mean([stat[v][0] for v in timed_views]))
+    e = float(np.mean([stat[v][1] for v in timed_views]))
     P = W * H
-    view_b, k6_b = b_alg(gs.n, gs.sh_coeffs, n_v, e, P, cfg.with_depth)
+    L = r.ws.layout(gs.n, W, H)
+    kb = kernel_bytes(gs.n, gs.sh_coeffs, n_v, e, P, L.n_tiles, cfg.with_depth)
+    vb = view_bytes(gs.n, gs.sh_coeffs, n_v, e, P, cfg.with_depth)
     peak, peak_src = peaks()
-    names = ["K0+K1 preprocess", "K2+K3 scan+duplicate", "K4+K5 sort+ranges", "K6 render"]
-    dom = int(np.argmax(stage_mean))
-    k6_ms = stage_mean[3]
-    achieved = k6_b / (k6_ms / 1e3) / 1e9
-    traffic = None
+    ncu = _profile_json("ncu_kernels.json") or {}
     gz = type(mode).__name__ == "GlobalZ"
-    tr_path = os.path.join(ROOT, "profiles", "k6_traffic.json")
-    if os.path.exists(tr_path) and not gz:  # the capture is of the hierarchical k_render
-        try:
-            with open(tr_path) as f:
-                traffic = json.load(f).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    per_kernel = {}
+    for name, ms in zip(KERNELS, kmean):
+        a = kb[name] / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        d = {"ms": float(ms), "algorithmic_bytes": float(kb[name]), "achieved": a,
+             "frac": a / peak, "share_of_view": float(ms / kmean.sum())}
+        cap = ncu.get("kernels", {}).get(name)
+        if cap and (not gz or name != "K6 render"):
+            d["traffic"] = cap.get("dram_bytes_per_view")
+            for k2 in ("issue_active_frac", "fp64_pipe_frac", "achieved_occupancy", "top_stalls",
+                       "dram_frac_of_peak_ncu"):
+                if k2 in cap:
+                    d[k2] = cap[k2]
+        per_kernel[name] = d
+    k6 = per_kernel["K6 render"]
+    dom = max(per_kernel, key=lambda k_: per_kernel[k_]["ms"])
 
     # e2e: the public render path (Renderer.render_into, one per view slot)
     # with host output buffers (pinned): per step the camera goes host->device
-    # (by-value launch params) and colour + transmittance come back
-    # device->host, on the same streams / views-in-flight as the timed region.
+    # (by-value launch params) and colour + transmittance + the status word
+    # come back device->host, on the same streams / views-in-flight as the
+    # timed region; every step's status is checked.
     e2e_steps = args.e2e_steps or min(steps, 32)
-    rs = [r] + [Renderer(gs, mode, cfg, dev, fast32=args.fast32) for _ in range(n_str - 1)]
+    rs = [r] + [Renderer(gs, mode, cfg, dev) for _ in range(n_str - 1)]
     for k in range(1, n_str):
         rs[k].ws = wss[k]
     host = [(torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True),
              torch.empty((H, W), dtype=torch.float32, pin_memory=True)) for _ in range(n_str)]
+    host_status = torch.zeros((e2e_steps, 2), dtype=torch.int64, pin_memory=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -389,79 +463,131 @@ def run_ours(args):
                               stream=streams[k].cuda_stream)
             host[k][0].copy_(keep[k]["color"], non_blocking=True)
             host[k][1].copy_(keep[k]["transmittance"], non_blocking=True)
+            host_status[s].copy_(rs[k].status, non_blocking=True)
     for st in streams[1:]:
         j = torch.cuda.Event()
         j.record(st)
         streams[0].wait_event(j)
     e1.record(streams[0])
     torch.cuda.synchronize()
+    if (host_status[:, 0] != 0).any():
+        raise RuntimeError("e2e frames reported an entry overflow")
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_steps / (float(e2e_ms.item()) / 1e3)
 
-    # K0, K1 + row count, 3 x K2, K3 + row duplicate, K4 histogram + passes,
-    # K5 (ranges with the tie fix-up), K6 (fast + list pass)
-    launches_per_view = (1 + 2 + 3 + 2 + 1 + r.ws.layout(gs.n, W, H).sort_passes + 1 +
-                         (2 if args.fast32 and not gz else 1))
+    # launches per view: K0, K1 + K1b row count, 3 x K2, K3 + K3b, K4
+    # histogram + passes, K5, K6
+    launches_per_view = 1 + 2 + 3 + 2 + 1 + L.sort_passes + 1 + 1
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": max_ms / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 geometry/decisions + f32 blend",
         "data": "synthetic (seeded scene generator, paper_2402_00525_b200/scenes.py)",
-        "config": {"workload": WORKLOADS[args.config.upper()], "gaussians": gs.n, "sh_degree": int(round(gs.sh_coeffs ** 0.5)) - 1, "width": W,
-                   "height": H, "views": n_views, "views_per_step_per_gpu": 1,
-                   "parallelism": f"views sharded over {world} GPU(s), no hot-path collective; "
-                                  f"{n_str} views in flight per GPU (streams)",
-                   "mode": mode_name(mode), "l2": "inputs larger than L2 "
-                   f"(scene {sum(x.numel() for x in dev_t.values()) * 4 / 1e6:.0f} MB > 126 MB)",
-                   "mean_kept": float(n_v), "mean_entries": float(e),
-                   "k6_path": "fp32-state certified + float64 list pass" if args.fast32
-                   else "float64",
-                   "mean_exact_items": float(np.mean([stat[v][3] for v in timed_views])),
-                   "mean_resolves": float(np.mean([stat[v][4] for v in timed_views]))},
-        "stage_ms": {nm: float(x) for nm, x in zip(names, stage_mean)},
-        "stage_ms_note": "one view at a time (CUDA events per stage)" + (
+        "config": config_dict(args, gs.n, W, H, n_views, mode_name(mode)),
+        "workload_stats": {"sh_degree": int(round(gs.sh_coeffs ** 0.5)) - 1,
+                           "mean_kept": n_v, "mean_entries": e,
+                           "parallelism": f"views sharded over {world} GPU(s), no hot-path "
+                                          f"collective; {n_str} views in flight per GPU (streams)"},
+        "stage_ms": {nm: float(x) for nm, x in zip(STAGES, stage_mean)},
+        "kernel_ms": {nm: float(x) for nm, x in zip(KERNELS, kmean)},
+        "stage_ms_note": "one view at a time, CUDA events at every kernel boundary on the "
+                         f"launching stream ({n_stage} views)" + (
             f"; the timed region runs {n_str} views in flight" if n_str > 1 else ""),
         "roofline": {"bound": "hbm",
                      "kernel": "K6 render (k_render_globalz)" if gz else "K6 render (k_render)",
-                     "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "achieved": k6["achieved"], "peak": peak, "unit": "GB/s",
+                     "frac": k6["achieved"] / peak, "traffic": k6.get("traffic"),
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": float(k6_b),
-                     "dominant_stage": names[dom]},
-        "view_roofline": {"achieved": view_b / (max_ms / steps / 1e3) / 1e9, "peak": peak,
-                          "unit": "GB/s", "frac": view_b / (max_ms / steps / 1e3) / 1e9 / peak,
-                          "algorithmic_bytes_per_view": float(view_b)},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ctypes.sizeof(_lib.StpCamera),
-                "d2h_bytes_per_step": H * W * 16, "steps": e2e_steps},
+                     "algorithmic_bytes_per_launch": k6["algorithmic_bytes"],
+                     "dominant_kernel": dom,
+                     "note": "K6 is bound by float64 dependent latency / issue, not HBM: its "
+                             "issue-slot and FP64-pipe fractions (committed ncu capture) are in "
+                             "per_kernel['K6 render']",
+                     "per_kernel": per_kernel},
+        "view_roofline": {"achieved": vb / (max_ms / steps / 1e3) / 1e9, "peak": peak,
+                          "unit": "GB/s", "frac": vb / (max_ms / steps / 1e3) / 1e9 / peak,
+                          "algorithmic_bytes_per_view": float(vb)},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": ctypes.sizeof(_lib.StpCamera),
+                "d2h_bytes_per_step": H * W * 16 + 16, "steps": e2e_steps,
+                "path": "Renderer.render_into (C ABI stp_render) -> pinned host colour + T"},
         "gpu_launches": launches_per_view * steps,
         "clocks": clk,
         "wall_s_timed_region": t_wall,
         "scene_setup_s": t_gen,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        host = {k: dev_t[k].cpu().numpy() for k in keys}
-        rate, done, times = cpu_view_rate(host, cams, [my_views[warm]] * 3, 30.0, threads)
+        # drop-in API throughput: render(GaussianScene, cam, mode, cfg) returning
+        # the reference's float64 numpy FrameOutput (allocation, sync, stats,
+        # float64 conversion and D2H included)
+        from paper_2402_00525_b200.renderer import render as dropin_render
+        n_api = 4
+        dropin_render(gs, cams[my_views[warm]], mode, cfg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(n_api):
+            dropin_render(gs, cams[my_views[warm + s]], mode, cfg)
+        line["e2e_render_api"] = {"value": n_api / (time.perf_counter() - t0), "unit": UNIT,
+                                  "steps": n_api, "timer": "host wall clock",
+                                  "path": "paper_2402_00525_b200.render (drop-in), float64 "
+                                          "numpy outputs"}
+        # CPU baseline on the host cores, and parity of the benched frame:
+        # the same view rendered by the benched path and by the oracle
+        threads = host_threads()
+        host_sc = {k: dev_t[k].cpu().numpy() for k in keys}
+        v0 = my_views[warm]
+        rate, done, times, ref = cpu_view_rate(host_sc, cams, [v0] * 3, 30.0, threads, mode,
+                                               keep_first=True)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"{done} full {args.config.upper()} view(s) (view {my_views[warm]}): "
-                                          "project + bin_and_sort + hierarchical render of "
-                                          "all tiles by the float64 C++ restatement "
+                                "sample": f"{done} full {args.config.upper()} view(s) (view {v0}): "
+                                          f"project + bin_and_sort + {mode_name(mode)} render "
+                                          "of all tiles by the float64 C++ restatement "
                                           "(oracle/stp_oracle.cpp)"}
+        pouts = r.alloc_outputs(W, H)
+        r.render_into(cams[v0], pouts)
+        torch.cuda.synchronize()
+        if not r.check_status():
+            raise RuntimeError("parity frame overflowed")
+        line["parity"] = dict(frame_parity(r, pouts, cams[v0], ref), view=int(v0),
+                              path="stp_render (benched kernels) vs oracle/stp_oracle.cpp")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawned(local_rank, world, port, argv):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(local_rank), LOCAL_RANK=str(local_rank),
+                      LOCAL_WORLD_SIZE=str(world))
+    sys.argv = argv
+    main()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `--gpus N` without torchrun: one process per GPU, spawned here
+        import torch.multiprocessing as mp
+        mp.spawn(_spawned, args=(args.gpus, _free_port(), list(sys.argv)), nprocs=args.gpus,
+                 join=True)
+        return
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    run_ours(args)
 
 
 if __name__ == "__main__":

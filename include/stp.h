@@ -26,11 +26,15 @@
 extern "C" {
 #endif
 
-#define STP_ABI_VERSION 1
+#define STP_ABI_VERSION 2
 
 /* Status codes.  CONFIG -> ConfigError (rasterizer.py:93-117, 196-203),
  * DATA -> DataError (rasterizer.py:770-771), WORKSPACE_TOO_SMALL -> the host
- * grows the workspace to StpStats.bin_entries and retries once. */
+ * grows the workspace to the frame's entry count and retries once.  The entry
+ * count E of a frame is only known on the device after K3: synchronous calls
+ * (stats != NULL) return WORKSPACE_TOO_SMALL with StpStats.bin_entries = E;
+ * asynchronous calls report it through StpOutputs.status (below), which the
+ * caller reads after synchronising the stream. */
 enum {
   STP_OK = 0,
   STP_ERR_CONFIG = 1,
@@ -117,12 +121,6 @@ typedef struct {
 #define STP_MODE_WINDOW 3
 
 #define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
-#define STP_FLAG_FAST32 2   /* K6 through the fp32-state certified kernel
-                               (float64 keys, fp32 queues / alpha / T), with the
-                               float64 kernel for the sub-tile pairs it cannot
-                               certify; default: the float64 kernel throughout */
-#define STP_FLAG_FB_TEST 4  /* testing (with FAST32): hand every odd sub-tile pair
-                               to the float64 pass (exercises its list mode) */
 
 /* Output buffers (device).  Colour is HWC float32 composited over the
  * background (rasterizer.py:680); depth is the unnormalised expected depth
@@ -142,6 +140,17 @@ typedef struct {
   float* sort_error;     /* [H,W] per-pixel sort error delta or NULL: the sum
                             of positive depth inversions of consecutive blended
                             contributions (metrics.py:46-73)             */
+  int64_t* status;       /* [2] frame status word or NULL, written on the
+                            device by K5 (and K6): status[0] = STP_OK, or
+                            STP_ERR_WORKSPACE_TOO_SMALL when the frame's
+                            entries exceeded the workspace capacity (the
+                            frame is then truncated and must be re-rendered
+                            with a larger workspace), or STP_ERR_CUDA on an
+                            internal scheduler fault; status[1] = the frame's
+                            entry count E.  The asynchronous paths' error
+                            report (stp_render(stats = NULL),
+                            stp_render_events, one word per view in
+                            stp_render_views).                              */
 } StpOutputs;
 
 /* stats dict of rasterizer.py:683-690 (+ projection stats
@@ -152,8 +161,6 @@ typedef struct {
   int64_t tiles;            /* non-empty tiles                             */
   int64_t nonfinite_pixels;
   int64_t tie_runs;         /* equal fp32 keys re-ordered by fp64 depth    */
-  int64_t exact_items;      /* K6 sub-tile pairs re-rendered in float64    */
-  int64_t resolves;         /* K6 fast path: comparisons settled in float64 */
   int64_t entry_capacity;   /* workspace capacity used for this frame      */
   float ms_project, ms_duplicate, ms_sort, ms_blend, ms_total;
   int32_t overflow;         /* 1 if bin_entries > entry_capacity           */
@@ -161,7 +168,7 @@ typedef struct {
 
 /* Byte offsets of the workspace regions (debug / parity dumps). */
 typedef struct {
-  size_t recs, recs32, fb_items, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
+  size_t recs, camera, masks, state, counts, offsets, keys0, keys1, vals, ranges,
       counters, hist, lookback, scan_scratch,
       rowlist, /* ids of kept Gaussians whose coarse rect exceeds 64 tiles */
       aux,     /* [n] (view z, |mean - origin|) float64 pairs (GlobalZ)     */
@@ -202,17 +209,25 @@ int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const Stp
                      StpStats* stats, void* stream);
 
 /* Render n_views cameras back to back on one stream (one workspace, outputs
- * per view); never synchronises. */
+ * per view); never synchronises.  Entry overflow of view v is reported in
+ * outs[v].status (set it to detect overflow: the shared workspace is
+ * overwritten by the next view, so it cannot be recovered afterwards). */
 int stp_render_views(const StpScene* scene, const StpCamera* cams, int32_t n_views,
                      const StpConfig* cfg, void* workspace, size_t workspace_bytes,
                      const StpOutputs* outs, void* stream);
 
-/* Render one view recording 5 caller-created CUDA events (cudaEvent_t as
- * void*) at the stage boundaries [K0+K1 | K2+K3 | K4+K5 | K6]; asynchronous.
- * events[3] -> events[4] brackets the render kernel K6 alone. */
+/* Render one view recording caller-created CUDA events (cudaEvent_t as
+ * void*) at kernel boundaries; asynchronous.  n_events = 5: the stage
+ * boundaries [K0+K1 | K2+K3 | K4+K5 | K6] (rasterizer.py:299-376 timing keys
+ * project / duplicate / sort / blend); n_events = 8: every kernel
+ * [K0 init | K1 preprocess (+ row count) | K2 scan | K3 duplicate (+ row
+ * duplicate) | K4 sort | K5 ranges | K6 render].  The last interval brackets
+ * the render kernel K6 alone. */
+#define STP_STAGE_EVENTS 5
+#define STP_KERNEL_EVENTS 8
 int stp_render_events(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
                       void* workspace, size_t workspace_bytes, const StpOutputs* out,
-                      void* const* events, void* stream);
+                      void* const* events, int32_t n_events, void* stream);
 
 /* Backward pass (gradients.py:103-162): gradients of the loss w.r.t. the
  * projected splat attributes, given dL/d(colour) of the frame.  The frame is

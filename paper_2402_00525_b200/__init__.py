@@ -1,6 +1,6 @@
 """B200-native hierarchical sorted Gaussian-splatting forward renderer
 (StopThePop, arXiv 2402.00525), a drop-in for the reference package's
-``render(scene, cam, Hierarchical(), cfg)`` path.
+``render(scene, cam, Hierarchical(), cfg)`` path (and its other sort modes).
 
 Public API mirrors ``splatsort`` (reference __init__.py:42-61) for this path.
 Importing the package does not need a GPU; rendering does (no CPU fallback).

@@ -14,8 +14,9 @@ LIB_PATH = os.path.join(HERE, "libstp_b200.so")
 
 STP_OK, STP_ERR_CONFIG, STP_ERR_DATA, STP_ERR_WORKSPACE_TOO_SMALL, STP_ERR_CUDA = range(5)
 STP_FLAG_TIMINGS = 1
-STP_FLAG_FAST32 = 2
-STP_FLAG_FB_TEST = 4
+STP_STAGE_EVENTS = 5    # [K0+K1 | K2+K3 | K4+K5 | K6]
+STP_KERNEL_EVENTS = 8   # [K0 | K1 | K2 | K3 | K4 | K5 | K6]
+ABI_VERSION = 2
 STP_MODE_HIERARCHICAL = 0
 STP_MODE_GLOBALZ = 1
 STP_MODE_FULL = 2
@@ -69,7 +70,7 @@ class StpOutputs(ctypes.Structure):
                 ("depth", ctypes.c_void_p), ("rec_count", ctypes.c_void_p),
                 ("rec_splat", ctypes.c_void_p), ("rec_t", ctypes.c_void_p),
                 ("rec_alpha", ctypes.c_void_p), ("state", ctypes.c_void_p),
-                ("sort_error", ctypes.c_void_p)]
+                ("sort_error", ctypes.c_void_p), ("status", ctypes.c_void_p)]
 
 
 class StpGrads(ctypes.Structure):
@@ -83,8 +84,7 @@ class StpStats(ctypes.Structure):
                 ("guard", ctypes.c_int64), ("degenerate", ctypes.c_int64),
                 ("kept", ctypes.c_int64), ("bin_entries", ctypes.c_int64),
                 ("tiles", ctypes.c_int64), ("nonfinite_pixels", ctypes.c_int64),
-                ("tie_runs", ctypes.c_int64), ("exact_items", ctypes.c_int64),
-                ("resolves", ctypes.c_int64), ("entry_capacity", ctypes.c_int64),
+                ("tie_runs", ctypes.c_int64), ("entry_capacity", ctypes.c_int64),
                 ("ms_project", ctypes.c_float), ("ms_duplicate", ctypes.c_float),
                 ("ms_sort", ctypes.c_float), ("ms_blend", ctypes.c_float),
                 ("ms_total", ctypes.c_float), ("overflow", ctypes.c_int32)]
@@ -92,7 +92,7 @@ class StpStats(ctypes.Structure):
 
 class StpLayout(ctypes.Structure):
     _fields_ = [(n, ctypes.c_size_t) for n in (
-        "recs", "recs32", "fb_items", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals", "ranges",
+        "recs", "camera", "masks", "state", "counts", "offsets", "keys0", "keys1", "vals", "ranges",
         "counters", "hist", "lookback", "scan_scratch", "rowlist", "aux", "total")] + [
         ("entry_capacity", ctypes.c_int64), ("n_tiles", ctypes.c_int32),
         ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32),
@@ -148,12 +148,13 @@ def load(build_if_missing: bool = True):
     L.stp_render_events.argtypes = [ctypes.POINTER(StpScene), ctypes.POINTER(StpCamera),
                                     ctypes.POINTER(StpConfig), ctypes.c_void_p,
                                     ctypes.c_size_t, ctypes.POINTER(StpOutputs),
-                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                    ctypes.c_void_p]
     L.stp_events_create.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
     L.stp_events_destroy.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
     L.stp_event_elapsed_ms.argtypes = [ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.POINTER(ctypes.c_float)]
-    if L.stp_abi_version() != 1:
+    if L.stp_abi_version() != ABI_VERSION:
         raise RuntimeError("libstp_b200.so ABI version mismatch")
     _lib = L
     return L

@@ -14,8 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstp_b200.so")
-SOURCES = ["stp_api.cu", "stp_preprocess.cu", "stp_sort.cu", "stp_render.cu",
-           "stp_render_fast.cu"]
+SOURCES = ["stp_api.cu", "stp_preprocess.cu", "stp_sort.cu", "stp_render.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--shared",
          "-Xptxas", "-v", "-Wno-deprecated-gpu-targets"]

@@ -59,8 +59,6 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.ranges = o;       o = align_up(o + (size_t)L.n_tiles * 8);
   L.scan_scratch = o; o = align_up(o + (size_t)(nb + 1) * 4);
   L.recs = o;         o = align_up(o + (size_t)n * sizeof(SplatRec));
-  L.recs32 = o;       o = align_up(o + (size_t)n * sizeof(SplatRec32));
-  L.fb_items = o;     o = align_up(o + (size_t)L.n_tiles * 8 * 4);
   L.camera = o;       o = align_up(o + sizeof(DevCam));
   L.masks = o;        o = align_up(o + (size_t)n * 8);
   L.state = o;        o = align_up(o + (size_t)n);
@@ -138,8 +136,6 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   plan(n, cam->width, cam->height, ecap, L);
   unsigned char* b = static_cast<unsigned char*>(ws);
   f.recs = reinterpret_cast<SplatRec*>(b + L.recs);
-  f.recs32 = reinterpret_cast<SplatRec32*>(b + L.recs32);
-  f.fb_items = reinterpret_cast<uint32_t*>(b + L.fb_items);
   f.camp = reinterpret_cast<DevCam*>(b + L.camera);
   f.masks = reinterpret_cast<uint64_t*>(b + L.masks);
   f.rowlist = reinterpret_cast<uint32_t*>(b + L.rowlist);
@@ -152,9 +148,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
     f.tile0 = std::max(0, std::min(cfg->tile_begin, L.n_tiles));
     f.tile1 = std::max(f.tile0, std::min(cfg->tile_end, L.n_tiles));
   }
-  f.exact_only = ((cfg->flags & STP_FLAG_FAST32) && cfg->sort_mode == STP_MODE_HIERARCHICAL &&
-                  cfg->tile_end <= 0) ? 0 : 1;
-  f.fb_test = (cfg->flags & STP_FLAG_FB_TEST) ? 1 : 0;
+  f.status = nullptr;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);
   f.offsets = reinterpret_cast<uint32_t*>(b + L.offsets);
@@ -203,12 +197,14 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
   return true;
 }
 
-// One view.  `ev` (5 events or null) is recorded at the stage boundaries
-// [init+K1 | K2+K3 | K4+K5 | K6]; with `ms` the stream is synchronised and the
-// stage times returned.
+// One view.  `ev` (n_ev = 5 or 8 events, or null) is recorded at the stage
+// boundaries [init+K1 | K2+K3 | K4+K5 | K6] (5) or at every kernel boundary
+// [K0 | K1 | K2 | K3 | K4 | K5 | K6] (8); with `ms` the stream is synchronised
+// and the 4 stage times returned.
 int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* cam,
                const StpConfig* cfg, void* ws, size_t ws_bytes, const StpOutputs* out,
-               cudaStream_t s, cudaEvent_t* ev, float* ms, const StpGrads* grads = nullptr) {
+               cudaStream_t s, cudaEvent_t* ev, int n_ev, float* ms,
+               const StpGrads* grads = nullptr) {
   Frame f;
   StpLayout L;
   if (!carve_frame(batch ? batch->n : sc->n, cam, cfg, ws, ws_bytes, f, L))
@@ -216,24 +212,40 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   if (cfg->sort_mode == STP_MODE_HIERARCHICAL &&
       (size_t)render_smem_bytes(cfg->q_tail, cfg->q_mid) > 227 * 1024)
     return STP_ERR_CONFIG;
+  f.status = out->status;
   cudaEvent_t own[5];
   if (ms && !ev) {
     for (int i = 0; i < 5; ++i) cudaEventCreate(&own[i]);
     ev = own;
+    n_ev = 5;
   }
-  if (ev) cudaEventRecord(ev[0], s);
+  const bool fine = ev && n_ev == STP_KERNEL_EVENTS;
+  // event i of the 8-event scheme; the 5-event scheme records a subset
+  auto mark = [&](int k8) {
+    if (!ev) return;
+    if (fine) {
+      cudaEventRecord(ev[k8], s);
+      return;
+    }
+    static const int k5[8] = {0, -1, 1, -1, 2, -1, 3, 4};
+    if (k5[k8] >= 0) cudaEventRecord(ev[k5[k8]], s);
+  };
+  mark(0);
   launch_init(f, s);
+  mark(1);
   StpOutputs o = *out;
   if (o.state) f.state = o.state;
   if (batch) launch_ingest(f, *batch, s);
   else launch_preprocess(f, *sc, s);
-  if (ev) cudaEventRecord(ev[1], s);
+  mark(2);
   launch_scan(f, s);
+  mark(3);
   launch_duplicate(f, s);
-  if (ev) cudaEventRecord(ev[2], s);
+  mark(4);
   const int buf = launch_sort(f, s);
+  mark(5);
   launch_ranges(f, buf, s);
-  if (ev) cudaEventRecord(ev[3], s);
+  mark(6);
   if (grads) {
     // backward (gradients.py:103-162): K6 replayed twice over the same bins,
     // first for each pixel's float64 colour sum and final T, then with the
@@ -256,12 +268,12 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
     // the persistent K6 hands out (tile, pair) items from frame counters and
     // per-SM rings: clear them for the second replay
     cudaMemsetAsync(f.counters + C_TILE, 0, sizeof(unsigned long long), s);
-    cudaMemsetAsync(f.counters + C_SM, 0, (size_t)(C_SMT + 256 * 16 - C_SM) * 8, s);
+    cudaMemsetAsync(f.counters + C_SM, 0, (size_t)(C_PSTAT - C_SM) * 8, s);
     launch_render(f, buf, o, s, XM_BWD, &g);
   } else {
     launch_render(f, buf, o, s);
   }
-  if (ev) cudaEventRecord(ev[4], s);
+  mark(7);
   if (ms) {
     cudaEventSynchronize(ev[4]);
     for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
@@ -305,23 +317,31 @@ int fill_stats(const void* ws, size_t ws_bytes, int64_t n, int32_t W, int32_t H,
   st->tiles = (int64_t)c[C_TILES];
   st->nonfinite_pixels = (int64_t)c[C_NONFINITE];
   st->tie_runs = (int64_t)c[C_TIES];
-  st->exact_items = (int64_t)c[C_FB];
-  {
-    unsigned long long res[256];
-    if (cudaMemcpyAsync(res, static_cast<const unsigned char*>(ws) + L.counters + C_RES * 8,
-                        sizeof(res), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-      return STP_ERR_CUDA;
-    int64_t tot = 0;
-    for (int i = 0; i < 256; ++i) tot += (int64_t)res[i];
-    st->resolves = tot;
-  }
   st->entry_capacity = ecap;
   st->overflow = st->bin_entries > ecap ? 1 : 0;
+  if (c[C_SCHED]) {
+    fprintf(stderr, "stp: K6 tile scheduler fault (%llu)\n", c[C_SCHED]);
+    return STP_ERR_CUDA;
+  }
   return STP_OK;
 }
 
 }  // namespace
+}  // namespace stp
+
+namespace stp {
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
 }  // namespace stp
 
 using namespace stp;
@@ -381,7 +401,7 @@ int stp_render(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float ms[4] = {0, 0, 0, 0};
   const bool timed = stats && (cfg->flags & STP_FLAG_TIMINGS);
-  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr,
+  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr, 0,
                   timed ? ms : nullptr);
   if (rc != STP_OK) return rc;
   if (stats) {
@@ -398,11 +418,10 @@ int stp_render(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg
   return STP_OK;
 }
 
-int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
-                     void* workspace, size_t workspace_bytes, const StpOutputs* out,
-                     StpStats* stats, void* stream) {
+static int check_batch_inputs(const StpSplatBatch* batch, const StpCamera* cam,
+                              const StpConfig* cfg, const StpOutputs* out) {
   if (!batch || !cam || !cfg || !out) return STP_ERR_CONFIG;
-  int rc = cfg_check(cfg);
+  const int rc = cfg_check(cfg);
   if (rc != STP_OK) return rc;
   if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0) || !(cam->fy > 0))
     return STP_ERR_DATA;
@@ -410,15 +429,26 @@ int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const Stp
   if (batch->n > 0 && (!batch->mean2d || !batch->conic || !batch->color || !batch->opacity ||
                        !batch->radius || !batch->inv_cov3 || !batch->inv_cov_center))
     return STP_ERR_DATA;
+  if (cfg->sort_mode == STP_MODE_GLOBALZ && batch->n > 0 &&
+      (!batch->global_depth || !batch->center_dist))
+    return STP_ERR_DATA;
   if (!out->color || !out->transmittance) return STP_ERR_DATA;
   if (cfg->with_depth && !out->depth) return STP_ERR_DATA;
   if (cfg->record_cap > 0 && (!out->rec_count || !out->rec_splat || !out->rec_t ||
                               !out->rec_alpha))
     return STP_ERR_DATA;
+  return STP_OK;
+}
+
+int stp_render_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
+                     void* workspace, size_t workspace_bytes, const StpOutputs* out,
+                     StpStats* stats, void* stream) {
+  int rc = check_batch_inputs(batch, cam, cfg, out);
+  if (rc != STP_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float ms[4] = {0, 0, 0, 0};
   const bool timed = stats && (cfg->flags & STP_FLAG_TIMINGS);
-  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr,
+  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr, 0,
                   timed ? ms : nullptr);
   if (rc != STP_OK) return rc;
   if (stats) {
@@ -443,7 +473,7 @@ int stp_render_views(const StpScene* scene, const StpCamera* cams, int32_t n_vie
     int rc = check_inputs(scene, cams + v, cfg, outs + v);
     if (rc != STP_OK) return rc;
     rc = render_one(scene, nullptr, cams + v, cfg, workspace, workspace_bytes, outs + v,
-                    static_cast<cudaStream_t>(stream), nullptr, nullptr);
+                    static_cast<cudaStream_t>(stream), nullptr, 0, nullptr);
     if (rc != STP_OK) return rc;
   }
   return STP_OK;
@@ -451,14 +481,15 @@ int stp_render_views(const StpScene* scene, const StpCamera* cams, int32_t n_vie
 
 int stp_render_events(const StpScene* scene, const StpCamera* cam, const StpConfig* cfg,
                       void* workspace, size_t workspace_bytes, const StpOutputs* out,
-                      void* const* events, void* stream) {
+                      void* const* events, int32_t n_events, void* stream) {
   const int rc = check_inputs(scene, cam, cfg, out);
   if (rc != STP_OK) return rc;
-  if (!events) return STP_ERR_CONFIG;
-  cudaEvent_t ev[5];
-  for (int i = 0; i < 5; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
+  if (!events || (n_events != STP_STAGE_EVENTS && n_events != STP_KERNEL_EVENTS))
+    return STP_ERR_CONFIG;
+  cudaEvent_t ev[STP_KERNEL_EVENTS];
+  for (int i = 0; i < n_events; ++i) ev[i] = static_cast<cudaEvent_t>(events[i]);
   return render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out,
-                    static_cast<cudaStream_t>(stream), ev, nullptr);
+                    static_cast<cudaStream_t>(stream), ev, n_events, nullptr);
 }
 
 int stp_events_create(int32_t n, void** events) {
@@ -505,8 +536,8 @@ int stp_backward(const StpScene* scene, const StpCamera* cam, const StpConfig* c
   if (rc != STP_OK) return rc;
   if ((rc = check_grads(grads, scene->n)) != STP_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr, nullptr,
-                  grads);
+  rc = render_one(scene, nullptr, cam, cfg, workspace, workspace_bytes, out, s, nullptr, 0,
+                  nullptr, grads);
   if (rc != STP_OK) return rc;
   if (stats) {
     memset(stats, 0, sizeof(*stats));
@@ -520,16 +551,12 @@ int stp_backward(const StpScene* scene, const StpCamera* cam, const StpConfig* c
 int stp_backward_batch(const StpSplatBatch* batch, const StpCamera* cam, const StpConfig* cfg,
                        void* workspace, size_t workspace_bytes, const StpOutputs* out,
                        const StpGrads* grads, StpStats* stats, void* stream) {
-  if (!batch || !cam || !cfg || !out) return STP_ERR_CONFIG;
-  int rc = cfg_check(cfg);
+  int rc = check_batch_inputs(batch, cam, cfg, out);
   if (rc != STP_OK) return rc;
-  if (batch->n < 0 || batch->n >= (int64_t)0x7fffffff) return STP_ERR_DATA;
-  if (!out->color || !out->transmittance) return STP_ERR_DATA;
-  if (cfg->with_depth && !out->depth) return STP_ERR_DATA;
   if ((rc = check_grads(grads, batch->n)) != STP_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr, nullptr,
-                  grads);
+  rc = render_one(nullptr, batch, cam, cfg, workspace, workspace_bytes, out, s, nullptr, 0,
+                  nullptr, grads);
   if (rc != STP_OK) return rc;
   if (stats) {
     memset(stats, 0, sizeof(*stats));

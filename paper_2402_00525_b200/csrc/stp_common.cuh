@@ -24,6 +24,7 @@ constexpr int kTile = 16;
 constexpr int kSortPartition = 256 * STP_SORT_ITEMS;  // K4 entries per partition (256 threads)
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSmRing = 64;  // K6 per-SM tile ring slots (C_SMT)
 
 // Projected splat, one per kept Gaussian, indexed by Gaussian id; 160 B.
 // The first 128-B line holds everything the pixel stage reads for one
@@ -50,24 +51,6 @@ __device__ __forceinline__ void ld256(const void* p, double& a, double& b, doubl
       : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
       : "l"(p));
 }
-
-// Camera-space record of the K6 fast path (128 B, one cache line), written
-// by K1 next to SplatRec.  With the camera ray v = ((x-cx)/fx, (y-cy)/fy, 1),
-//   t_opt = |v| (v . q') / (v^T M' v),   M' = R Sigma^-1 R^T,  q' = M' p_view,
-// the same real number as the reference's (d . Sigma^-1 (mu - o)) /
-// (d^T Sigma^-1 d) with d = R^T v / |v| (tile_culling.py:161-195), in 2+5
-// float64 FMAs instead of a rotation, a normalisation and two dot products.
-struct __align__(16) SplatRec32 {
-  double mx, my;           // mean2d (pixels)                                  0
-  double ca, cb;           // conic a, b                                       16
-  double cc, q0;           // conic c, q'_x                                    32
-  double q1, q2;           // q'_y, q'_z                                       48
-  double m00, m11;         // M'                                               64
-  double m22, m01x2;       //                                                  80
-  double m02x2, m12x2;     //                                                  96
-  float op, c0, c1, c2;    // opacity, colour                                  112
-};
-static_assert(sizeof(SplatRec32) == 128, "SplatRec32 must be 128 B");
 
 struct DevCam {
   double R[9];
@@ -101,14 +84,11 @@ enum Counter {
   C_WORK = 24,      // render work counter
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
   C_TILE = 40,      // render: global tile counter
-  C_FB = 41,        // render: items handed to the exact (fp64) pass
-  C_FBWORK = 42,    // render: exact-pass work counter
-  C_RESOLVE = 43,   // (unused: per-SM slots at C_RES)
+  C_SCHED = 41,     // render: per-SM tile ring overrun / spin bound hit (must stay 0)
   C_STAT = 48,      // 8 work counters (STP_PHASE_PROF builds)
   C_SM = 64,        // render: per-SM sub-tile counters [256]
-  C_SMT = 320,      // render: per-SM tile ring [256][16] (tag<<32 | tile+2)
-  C_RES = 320 + 256 * 16,   // render: per-SM float64 resolution counts [256]
-  C_PSTAT = C_RES + 256,    // K1: per-SM projection stats [256][4] (behind, guard, degenerate, kept)
+  C_SMT = 320,      // render: per-SM tile ring [256][kSmRing] (tag<<32 | tile+2)
+  C_PSTAT = C_SMT + 256 * 64,  // K1: per-SM projection stats [256][4] (behind, guard, degenerate, kept)
   C_COUNT = C_PSTAT + 256 * 4
 };
 
@@ -290,22 +270,9 @@ __device__ __forceinline__ double blend_depth(const double* m, double q0, double
   return fdiv(num, den);
 }
 
-// t_opt along the camera ray v = (u, w, 1), |v| = vn, in the SplatRec32
-// camera-space form: |v| (v . q') / (v^T M' v) (same real number as
-// blend_depth on the unit world ray R^T v / |v|).
-__device__ __forceinline__ double key_cam(const SplatRec32* __restrict__ r, double u, double w,
-                                          double vn) {
-  const double2 qa = __ldg(reinterpret_cast<const double2*>(&r->cc));     // cc q0
-  const double2 qb = __ldg(reinterpret_cast<const double2*>(&r->q1));     // q1 q2
-  const double2 ma = __ldg(reinterpret_cast<const double2*>(&r->m00));    // m00 m11
-  const double2 mb = __ldg(reinterpret_cast<const double2*>(&r->m22));    // m22 m01x2
-  const double2 mc = __ldg(reinterpret_cast<const double2*>(&r->m02x2));  // m02x2 m12x2
-  const double N = fma(u, qa.y, fma(w, qb.x, qb.y));
-  const double D = fma(u, fma(ma.x, u, fma(mb.y, w, mc.x)), fma(w, fma(ma.y, w, mc.y), mb.x));
-  return vn * fdiv(N, D);
-}
-
-// the same from a SplatRec (camera-space M', q')
+// t_opt along the camera ray v = (u, w, 1), |v| = vn, from a SplatRec's
+// camera-space M', q': |v| (v . q') / (v^T M' v), the same real number as
+// blend_depth on the unit world ray R^T v / |v| (tile_culling.py:161-195)
 __device__ __forceinline__ double key_rec(const double* m, double q0, double q1, double q2,
                                           double u, double w, double vn) {
   const double N = fma(u, q0, fma(w, q1, q2));
@@ -333,15 +300,6 @@ __device__ __forceinline__ double key_rec_at(const DevCam& cam, const SplatRec& 
   double u, w, vn;
   cam_ray(cam, x, y, u, w, vn);
   return key_rec(r.m, r.q0, r.q1, r.q2, u, w, vn);
-}
-
-// camera ray of a float64 image point and the key along it
-__device__ __forceinline__ double key_at_point(const DevCam& cam, const SplatRec32* __restrict__ r,
-                                               double x, double y) {
-  const double u = (x - cam.cx) * cam.inv_fx;
-  const double w = (y - cam.cy) * cam.inv_fy;
-  const double vv = fma(u, u, fma(w, w, 1.0));
-  return key_cam(r, u, w, vv * frsqrt(vv));
 }
 
 // Monotone fp32 sort key of a float64 depth: round-to-nearest, -0 -> +0,
@@ -456,7 +414,6 @@ namespace stp {
 struct Frame {
   // device pointers carved from the workspace
   SplatRec* recs;
-  SplatRec32* recs32;
   uint64_t* masks;        // per Gaussian: surviving tiles of a <= 64-tile coarse rect
   uint32_t* rowlist;      // ids of kept Gaussians with a > 64-tile rect (C_ROWS of them)
   double2* aux;           // per Gaussian (view z, |mean - origin|), GlobalZ only
@@ -464,7 +421,6 @@ struct Frame {
   int sort_mode;          // STP_MODE_*
   int tile0, tile1;       // K6 tile band [tile0, tile1)
   DevCam* camp;           // device copy of `cam` (written by K0)
-  uint32_t* fb_items;     // [n_tiles * 8] (tile, pair) items for the exact pass
   uint8_t* state;
   uint32_t* counts;
   uint32_t* offsets;
@@ -481,12 +437,12 @@ struct Frame {
   int passes, partitions;
   int depth_bits;         // entry word = (tile << depth_bits | truncated depth key) << id_bits | id
   int id_bits;
-  int exact_only;         // no STP_FLAG_FAST32: every item through the fp64 kernel
-  int fb_test;            // STP_FLAG_FB_TEST
+  int64_t* status;        // StpOutputs.status (device) or NULL: written by K5
   DevCam cam;
   DevCfg cfg;
 };
 
+int device_sm_count();  // SMs of the current device (cached per device)
 void launch_init(const Frame& f, cudaStream_t s);
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s);
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s);

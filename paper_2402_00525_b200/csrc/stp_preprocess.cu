@@ -314,7 +314,7 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
 
 __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
     StpScene sc, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
-    SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
+    uint64_t* __restrict__ masks,
     uint32_t* __restrict__ rowlist, double2* __restrict__ aux, uint32_t* __restrict__ counts,
     uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
@@ -494,29 +494,6 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           recs[i] = r;
           // GlobalZ: view z and |mean - origin| (gaussian_math.py:421-430)
           if (aux) aux[i] = make_double2(z, sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2));
-          if (recs32) {
-            // camera-space record (see SplatRec32): M' = W inv3 W^T, q' = M' p_view
-            SplatRec32 f;
-            f.mx = r.mx;
-            f.my = r.my;
-            f.ca = r.ca;
-            f.cb = r.cb;
-            f.cc = r.cc;
-            f.m00 = r.m[0];
-            f.m11 = r.m[1];
-            f.m22 = r.m[2];
-            f.m01x2 = r.m[3];
-            f.m02x2 = r.m[4];
-            f.m12x2 = r.m[5];
-            f.q0 = r.q0;
-            f.q1 = r.q1;
-            f.q2 = r.q2;
-            f.op = opf;
-            f.c0 = col[0];
-            f.c1 = col[1];
-            f.c2 = col[2];
-            recs32[i] = f;
-          }
           g.mx = r.mx;
           g.my = r.my;
           g.a = r.ca;
@@ -545,8 +522,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
 // in flight at full occupancy.
 __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
                                                const uint32_t* __restrict__ counts,
-                                               SplatRec* __restrict__ recs,
-                                               SplatRec32* __restrict__ recs32) {
+                                               SplatRec* __restrict__ recs) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= sc.n || counts[i] == 0) return;
   const double rel0 = (double)__ldg(sc.means + 3 * i + 0) - cam.pos[0];
@@ -559,11 +535,6 @@ __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
   recs[i].c0 = col[0];
   recs[i].c1 = col[1];
   recs[i].c2 = col[2];
-  if (recs32) {
-    recs32[i].c0 = col[0];
-    recs32[i].c1 = col[1];
-    recs32[i].c2 = col[2];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -571,7 +542,7 @@ __global__ void __launch_bounds__(256) k_shade(StpScene sc, DevCam cam,
 // (rasterizer.py:616-618 skips project_scene); every batch splat is kept.
 __global__ void __launch_bounds__(kPreThreads) k_ingest(
     StpSplatBatch b, DevCam cam, DevCfg cfg, int gw, int gh, SplatRec* __restrict__ recs,
-    SplatRec32* __restrict__ recs32, uint64_t* __restrict__ masks,
+    uint64_t* __restrict__ masks,
     uint32_t* __restrict__ rowlist, double2* __restrict__ aux, uint32_t* __restrict__ counts,
     uint8_t* __restrict__ state,
     unsigned long long* __restrict__ counters) {
@@ -634,28 +605,6 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
     if (aux)
       aux[i] = make_double2(b.global_depth ? b.global_depth[i] : 0.0,
                             b.center_dist ? b.center_dist[i] : 0.0);
-    if (recs32) {
-      SplatRec32 f;
-      f.mx = r.mx;
-      f.my = r.my;
-      f.ca = r.ca;
-      f.cb = r.cb;
-      f.cc = r.cc;
-      f.m00 = r.m[0];
-      f.m11 = r.m[1];
-      f.m22 = r.m[2];
-      f.m01x2 = r.m[3];
-      f.m02x2 = r.m[4];
-      f.m12x2 = r.m[5];
-      f.q0 = r.q0;
-      f.q1 = r.q1;
-      f.q2 = r.q2;
-      f.op = r.op;
-      f.c0 = r.c0;
-      f.c1 = r.c1;
-      f.c2 = r.c2;
-      recs32[i] = f;
-    }
     g.mx = r.mx;
     g.my = r.my;
     g.a = r.ca;
@@ -987,7 +936,8 @@ void launch_init(const Frame& f, cudaStream_t s) {
 // fixed grid of warps strides over it (idle warps exit at once)
 static unsigned rows_blocks(const Frame& f) {
   const int64_t b = (f.n + 255) / 256;
-  return (unsigned)(b < 148 * 8 ? b : 148 * 8);
+  const int64_t cap = (int64_t)device_sm_count() * 8;
+  return (unsigned)(b < cap ? b : cap);
 }
 
 static void launch_rows_count(const Frame& f, cudaStream_t s) {
@@ -1000,12 +950,11 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_preprocess<<<(unsigned)blocks, kPreThreads, 0, s>>>(sc, f.cam, f.cfg, f.gw, f.gh, f.recs,
-                                                      f.exact_only ? nullptr : f.recs32, f.masks,
+                                                      f.masks,
                                                       f.rowlist, f.globalz ? f.aux : nullptr,
                                                       f.counts, f.state, f.counters);
 #if STP_SPLIT_SH
-  k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs,
-                                           f.exact_only ? nullptr : f.recs32);
+  k_shade<<<(unsigned)blocks, 256, 0, s>>>(sc, f.cam, f.counts, f.recs);
 #endif
   launch_rows_count(f, s);
 }
@@ -1014,7 +963,7 @@ void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;
   k_ingest<<<(unsigned)blocks, kPreThreads, 0, s>>>(b, f.cam, f.cfg, f.gw, f.gh, f.recs,
-                                                  f.exact_only ? nullptr : f.recs32, f.masks,
+                                                  f.masks,
                                                   f.rowlist, f.globalz ? f.aux : nullptr,
                                                   f.counts, f.state, f.counters);
   launch_rows_count(f, s);

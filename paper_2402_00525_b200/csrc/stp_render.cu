@@ -122,7 +122,6 @@ struct RenderArgs {
   float log_eps;
   StpOutputs out;
   unsigned long long* counters;
-  const uint32_t* list;   // list mode: (tile*8 + pair) items handed over by the fast path
   DevGrads grad;          // XM_FWD / XM_BWD
 };
 
@@ -563,38 +562,42 @@ __global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(Rende
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   smid &= 255;
   unsigned long long* sm_cnt = A.counters + C_SM + smid;
-  unsigned long long* sm_ring = A.counters + C_SMT + smid * 16;
+  unsigned long long* sm_ring = A.counters + C_SMT + smid * kSmRing;
 
   for (;;) {
     // ---- work item: (tile, pair) with the 8 pairs of a tile on one SM
     int tile = -1, pair = 0;
-    if (A.list) {
-      // list mode: the items the fp32 fast path could not certify
-      if (lane == 0) {
-        const unsigned long long g = atomicAdd(A.counters + C_FBWORK, 1ull);
-        const unsigned long long n = *reinterpret_cast<volatile unsigned long long*>(
-            A.counters + C_FB);
-        if (g < n) {
-          const uint32_t it = A.list[g];
-          tile = (int)(it >> 3);
-          pair = (int)(it & 7);
-        }
-      }
-    } else if (lane == 0) {
+    if (lane == 0) {
       const unsigned long long i = atomicAdd(sm_cnt, 1ull);
       const unsigned long long tl = i >> 3;
       pair = (int)(i & 7);
-      unsigned long long* slot = sm_ring + (tl & 15);
+      unsigned long long* slot = sm_ring + (tl % kSmRing);
       if (pair == 0) {
         const int g = (int)atomicAdd(A.counters + C_TILE, 1ull);
         const int gt = g < A.n_items ? g + A.tile0 : -1;
         atomicExch(slot, (tl << 32) | (unsigned long long)(gt + 2));
         tile = gt;
       } else {
+        // pair 0 of tile tl was drawn before this pair (one counter per SM)
+        // and publishes it right after its draw.  The slot could only be
+        // overwritten once kSmRing more tiles start on this SM, i.e. after
+        // the SM's other warps finished hundreds of items while this one did
+        // not get to read: bounded and reported (C_SCHED) instead of hanging.
         unsigned long long v;
-        do {
+        unsigned spins = 0;
+        for (;;) {
           v = *reinterpret_cast<volatile unsigned long long*>(slot);
-        } while ((v >> 32) != tl || (v & 0xffffffffull) == 0);
+          const unsigned long long tag = v >> 32;
+          if (tag == tl && (v & 0xffffffffull) != 0) break;
+          if (tag > tl || ++spins > (1u << 26)) {
+            atomicAdd(A.counters + C_SCHED, 1ull);
+            if (A.out.status) atomicExch(reinterpret_cast<unsigned long long*>(A.out.status),
+                                         (unsigned long long)STP_ERR_CUDA);
+            v = 1;  // tile -1: stop
+            break;
+          }
+          if (spins > 64) __nanosleep(32);
+        }
         tile = (int)(v & 0xffffffffull) - 2;
       }
     }
@@ -1174,9 +1177,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
     attr = smem;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT, XM>,
                                                   kRenderThreads, smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    n_sm = device_sm_count();
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -1490,11 +1491,6 @@ static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
   }
 }
 
-void launch_render_fast(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s);
-
-// K6: the float64 kernel over every (tile, pair) item; with STP_FLAG_FAST32
-// the fp32-state certified kernel first, then the float64 kernel over the
-// items it handed over (list mode).
 // K6 dispatch.  xm: XM_NONE (render), or with `g` the backward replays
 // XM_FWD / XM_BWD; a non-null out.sort_error selects XM_SERR.
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s, int xm,
@@ -1516,17 +1512,10 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.n_items = f.tile1 - f.tile0;
   A.out = out;
   A.counters = f.counters;
-  A.list = nullptr;
   if (g) A.grad = *g;
   if (f.sort_mode == STP_MODE_FULL || f.sort_mode == STP_MODE_WINDOW) {
     launch_render_pixelsort(f, A, xm, s);
     return;
-  }
-  // the extra modes run the float64 kernel over every item
-  const bool exact_only = f.exact_only || xm != XM_NONE;
-  if (!exact_only) {
-    launch_render_fast(f, buf, out, s);
-    A.list = f.fb_items;
   }
   const size_t smem = render_smem_bytes(f.cfg.q_tail, f.cfg.q_mid);
   if (xm != XM_NONE) {

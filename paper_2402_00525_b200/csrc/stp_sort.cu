@@ -231,8 +231,15 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
                                                 const SplatRec* __restrict__ recs, DevCam cam,
                                                 int gw, int depth_bits, int id_bits,
                                                 const double2* __restrict__ aux,
-                                                double* __restrict__ d64) {
+                                                double* __restrict__ d64,
+                                                int64_t* __restrict__ status) {
   const int64_t E = n_entries(counters, ecap);
+  if (status && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the frame status word of the asynchronous paths (stp.h StpOutputs.status)
+    const int64_t total = (int64_t)counters[C_ENTRIES];
+    status[0] = total > ecap ? STP_ERR_WORKSPACE_TOO_SMALL : STP_OK;
+    status[1] = total;
+  }
   const uint64_t id_mask = (1ull << id_bits) - 1ull;
   int heads = 0, runs = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
@@ -317,7 +324,7 @@ int launch_sort(const Frame& f, cudaStream_t s) {
   // one resident wave of persistent blocks (the entry count is only known
   // on the device; a grid sized by the capacity would launch mostly idle blocks)
   const int sweep_blocks = min(f.partitions, sweep_grid);
-  const int hist_blocks = 148 * 4;
+  const int hist_blocks = device_sm_count() * 4;
   k_sort_hist<<<hist_blocks, kSortThreads, 0, s>>>(f.keys[0], f.counters, f.ecap, f.passes,
                                                     f.id_bits, f.hist);
   int cur = 0;
@@ -332,13 +339,14 @@ int launch_sort(const Frame& f, cudaStream_t s) {
 }
 
 void launch_ranges(const Frame& f, int buf, cudaStream_t s) {
-  if (f.ecap == 0) return;
-  const int64_t blocks = min((int64_t)148 * 8, (f.ecap + 255) / 256);
+  if (f.ecap == 0 && !f.status) return;
+  const int64_t blocks =
+      max((int64_t)1, min((int64_t)device_sm_count() * 8, (f.ecap + 255) / 256));
   // the other ping-pong key buffer (E x 8 B) is free: float64 depths of tie runs
   double* d64 = reinterpret_cast<double*>(f.keys[buf ^ 1]);
   k_ranges<<<(unsigned)blocks, 256, 0, s>>>(f.keys[buf], f.vals, f.counters, f.ecap, f.ranges,
                                             f.recs, f.cam, f.gw, f.depth_bits, f.id_bits,
-                                            f.globalz ? f.aux : nullptr, d64);
+                                            f.globalz ? f.aux : nullptr, d64, f.status);
 }
 
 }  // namespace stp

@@ -100,9 +100,61 @@ def gather_frames(local: dict[int, dict], n_views: int, keys=("color", "transmit
     return out
 
 
+def render_shard_streamed(cams: Sequence, render_fn: Callable, finalize_fn: Callable | None = None,
+                          keys=("color", "transmittance"), dst: int = 0, gather: bool = True,
+                          group=None) -> dict[int, dict] | None:
+    """Render this rank's views and stream every finished frame to ``dst``
+    while the next view renders (the optional gather,
+    overlapped).  ``render_fn(cam, v)`` enqueues view v and returns its frame
+    dict without synchronising; ``finalize_fn(v, frame)`` is called one view
+    later (after the next view is enqueued) and returns the checked frame --
+    the device renderer reads the view's status word there and re-renders an
+    overflowed view.  Frames are sent with point-to-point isend / irecv
+    (NCCL on the GPU box: the transfer runs on NCCL's stream behind the
+    render work already enqueued).  Returns {view: frame} on ``dst`` (every
+    view when ``gather``) and this rank's frames elsewhere."""
+    finalize_fn = finalize_fn or (lambda v, f: f)
+    n = len(cams)
+    on = dist.is_initialized() and dist.get_world_size(group) > 1
+    world = dist.get_world_size(group) if on else 1
+    rank = dist.get_rank(group) if on else 0
+    mine = shard_views(n, world, rank)
+    out: dict[int, dict] = {}
+    works = []
+    pending = None
+
+    def ship(v, frame):
+        out[v] = frame
+        if on and gather and rank != dst:
+            for k in keys:
+                works.append(dist.isend(frame[k].contiguous(), dst=dst, group=group))
+
+    for v in mine:
+        frame = render_fn(cams[v], v)
+        if pending is not None:
+            ship(pending[0], finalize_fn(*pending))
+        pending = (v, frame)
+    if pending is not None:
+        ship(pending[0], finalize_fn(*pending))
+    if on and gather and rank == dst:
+        proto = next(iter(out.values()), None)
+        for r in range(world):
+            if r == dst:
+                continue
+            for v in shard_views(n, world, r):
+                if proto is None:
+                    raise RuntimeError("render_shard_streamed: destination rank rendered no view")
+                out[v] = {k: torch.empty_like(proto[k]) for k in keys}
+                for k in keys:
+                    works.append(dist.irecv(out[v][k], src=r, group=group))
+    for w in works:
+        w.wait()
+    return out
+
+
 def device_render_fn(scene: dict, mode=None, cfg=None, device=None) -> Callable:
     """Per-view renderer on this rank's GPU (no CPU fallback): returns
-    float32 device tensors."""
+    float32 device tensors (synchronous: stats + overflow retry)."""
     from .renderer import GaussianScene, Renderer
     gs = GaussianScene(*(scene[k] for k in SCENE_KEYS), device=device)
     r = Renderer(gs, mode, cfg, gs.device)
@@ -113,6 +165,37 @@ def device_render_fn(scene: dict, mode=None, cfg=None, device=None) -> Callable:
         return outs
 
     return fn
+
+
+def device_streamed_fns(scene: dict, mode=None, cfg=None, device=None):
+    """(render_fn, finalize_fn) for ``render_shard_streamed`` on this rank's
+    GPU: asynchronous views (stp_render, stats = NULL) with a status word
+    per view, checked one view later; an overflowed view is re-rendered
+    synchronously after the workspace grows."""
+    from .renderer import GaussianScene, Renderer
+    gs = scene if isinstance(scene, GaussianScene) else \
+        GaussianScene(*(scene[k] for k in SCENE_KEYS), device=device)
+    r = Renderer(gs, mode, cfg, gs.device)
+
+    def render_fn(cam, v):
+        outs = r.alloc_outputs(cam.width, cam.height)
+        outs["status"] = torch.zeros(2, dtype=torch.int64, device=gs.device)
+        r.render_into(cam, outs)
+        return outs
+
+    def finalize_fn(v, outs):
+        st = outs.pop("status")
+        if not r.check_status(st):
+            r.render_into(cam_of[v], outs, stats=True)
+        return outs
+
+    cam_of: dict = {}
+
+    def render_fn_keep(cam, v):
+        cam_of[v] = cam
+        return render_fn(cam, v)
+
+    return render_fn_keep, finalize_fn
 
 
 # ---------------------------------------------------------------------------

@@ -21,8 +21,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .types import (Camera, ConfigError, DataError, FrameOutput, Hierarchical, PixelRecords,
-                    RenderConfig, _is_hier, mode_name, validate_mode)
+from .types import (Camera, ConfigError, DataError, FrameOutput, FullPerPixel, Hierarchical,
+                    PixelRecords, RenderConfig, _is_hier, mode_name, validate_mode)
 
 _SH_OK = (1, 4, 9, 16)
 
@@ -153,14 +153,16 @@ def _is_globalz(mode) -> bool:
     return type(mode).__name__ == "GlobalZ"
 
 
+WINDOW_MAX = 16
+
+
 def _check_supported(mode) -> None:
     """All four sort modes run on the B200 path: Hierarchical (the paper's
     pipeline), GlobalZ (the 3DGS order), FullPerPixel (the exact per-pixel
-    order) and Window(size) with 1 <= size <= 16 (a register window; larger
-    windows raise ConfigError)."""
-    if type(mode).__name__ == "Window" and not 1 <= int(mode.size) <= 16:
-        raise ConfigError(f"the B200 Window mode keeps at most 16 entries per pixel, got "
-                          f"{mode_name(mode)}")
+    order) and Window(size) with 1 <= size <= WINDOW_MAX."""
+    if type(mode).__name__ == "Window" and not 1 <= int(mode.size) <= WINDOW_MAX:
+        raise ConfigError(f"the B200 Window mode keeps at most {WINDOW_MAX} entries per pixel, "
+                          f"got {mode_name(mode)}")
 
 
 def _is_batch(scene) -> bool:
@@ -184,7 +186,7 @@ def make_camera(cam) -> _lib.StpCamera:
 
 
 def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = False,
-                fast32: bool = False, fb_test: bool = False, tiles=None):
+                tiles=None):
     c = _lib.StpConfig()
     c.eps = float(cfg.opacity_eps)
     c.termination = float(cfg.termination)
@@ -211,8 +213,7 @@ def make_config(cfg: RenderConfig, mode, record_cap: int = 0, timings: bool = Fa
     c.with_depth = int(bool(cfg.with_depth))
     c.exact_culling = int(bool(cfg.exact_culling(mode)))
     c.record_cap = int(record_cap)
-    c.flags = ((_lib.STP_FLAG_TIMINGS if timings else 0) |
-               (_lib.STP_FLAG_FAST32 if fast32 else 0) | (_lib.STP_FLAG_FB_TEST if fb_test else 0))
+    c.flags = _lib.STP_FLAG_TIMINGS if timings else 0
     return c
 
 
@@ -266,12 +267,15 @@ class Renderer:
     """Renders views of one device-resident scene; the building block of
     ``render``, the multi-view driver and the benchmark.
 
-    ``render_into`` is asynchronous (no host sync) unless stats are requested.
+    ``render_into`` is asynchronous (no host sync) unless stats are requested;
+    an asynchronous frame's entry overflow is reported by the device status
+    word (``check_status``).  The default mode of this class is Hierarchical
+    (the B200 hot path); the drop-in ``render`` defaults to FullPerPixel like
+    the reference.
     """
 
     def __init__(self, scene, mode=None, cfg: RenderConfig | None = None, device=None,
-                 entry_capacity: int | None = None, fast32: bool = False,
-                 fb_test: bool = False):
+                 entry_capacity: int | None = None):
         if _is_batch(scene):
             self.scene = scene if isinstance(scene, BatchScene) else BatchScene(scene, device)
         else:
@@ -288,8 +292,8 @@ class Renderer:
         self.lib = _lib.load()
         self.ws = Workspace(self.device)
         self.entry_capacity = entry_capacity
-        self.fast32 = bool(fast32)    # K6 via the fp32-state certified kernel (see stp.h)
-        self.fb_test = bool(fb_test)  # testing: route odd pairs through the float64 pass
+        # StpOutputs.status of the asynchronous path: (code, entries), written by K5
+        self.status = torch.zeros(2, dtype=torch.int64, device=self.device)
         self.c_scene = self.scene.struct()
         rc = self.lib.stp_validate_config(ctypes.byref(make_config(self.cfg, self.mode)))
         if rc != _lib.STP_OK:
@@ -317,26 +321,30 @@ class Renderer:
     def outputs_struct(o: dict) -> _lib.StpOutputs:
         s = _lib.StpOutputs()
         for k in ("color", "transmittance", "depth", "rec_count", "rec_splat", "rec_t",
-                  "rec_alpha", "state", "sort_error"):
+                  "rec_alpha", "state", "sort_error", "status"):
             if k in o:
                 setattr(s, k, o[k].data_ptr())
         return s
 
     def _ensure(self, cam):
         guess = self.entry_capacity or max(1 << 16, 8 * self.scene.n)
+        self._last_w, self._last_h = int(cam.width), int(cam.height)
         self.ws.ensure(self.scene.n, cam.width, cam.height, guess)
 
     def render_into(self, cam, outs: dict, stats: bool = False, timings: bool = False,
                     record_cap: int = 0, stream=None, tiles=None):
         """One view into preallocated device outputs.  Returns StpStats when
-        ``stats`` (synchronising), else None (asynchronous).  ``tiles`` =
-        (t0, t1) renders only that band of row-major tile ids (the pixels of
-        the other tiles are left untouched)."""
+        ``stats`` (synchronising; an entry overflow grows the workspace and
+        re-renders), else None (asynchronous: the frame's status word lands in
+        ``self.status`` -- see ``check_status``).  ``tiles`` = (t0, t1)
+        renders only that band of row-major tile ids (the pixels of the other
+        tiles are left untouched)."""
         c_cam = make_camera(cam)
         self._ensure(cam)
-        c_cfg = make_config(self.cfg, self.mode, record_cap, timings, self.fast32, self.fb_test,
-                            tiles)
+        c_cfg = make_config(self.cfg, self.mode, record_cap, timings, tiles)
         c_out = self.outputs_struct(outs)
+        if "status" not in outs:
+            c_out.status = self.status.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         st = _lib.StpStats() if stats else None
         for attempt in range(3):
@@ -355,6 +363,72 @@ class Renderer:
                 _raise(rc, "stp_render")
             return st
         raise DataError("stp_render: workspace retry failed")
+
+    def render_views(self, cams, outs_list, stream=None, retry: bool = True):
+        """``render_trajectory``'s loop of independent views (rasterizer.py:
+        758-772) as ONE stp_render_views call on one stream (one workspace,
+        outputs per view, no host sync inside).  Each view's status word is
+        written on the device; with ``retry`` the call synchronises once at
+        the end and re-renders the views that overflowed the workspace (grown
+        to the largest entry count).  Returns the [V, 2] status tensor."""
+        V = len(cams)
+        if V != len(outs_list):
+            raise DataError("render_views: one output dict per camera")
+        if self.batch:
+            raise DataError("render_views takes a Gaussian scene, not a SplatBatch")
+        status = torch.zeros((max(V, 1), 2), dtype=torch.int64, device=self.device)
+        c_cams = (_lib.StpCamera * max(V, 1))()
+        c_outs = (_lib.StpOutputs * max(V, 1))()
+        for v, (cam, o) in enumerate(zip(cams, outs_list)):
+            c_cams[v] = make_camera(cam)
+            c_outs[v] = self.outputs_struct(o)
+            c_outs[v].status = status[v].data_ptr()
+        if V:
+            self._ensure(cams[0])
+            if any((c.width, c.height) != (cams[0].width, cams[0].height) for c in cams):
+                w = max(c.width for c in cams)
+                h = max(c.height for c in cams)
+                self._last_w, self._last_h = w, h
+                self.ws.ensure(self.scene.n, w, h, self.entry_capacity or 8 * self.scene.n)
+        c_cfg = make_config(self.cfg, self.mode)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        rc = self.lib.stp_render_views(ctypes.byref(self.c_scene), c_cams, V, ctypes.byref(c_cfg),
+                                       ctypes.c_void_p(self.ws.ptr), self.ws.nbytes, c_outs,
+                                       ctypes.c_void_p(s))
+        if rc != _lib.STP_OK:
+            _raise(rc, "stp_render_views")
+        if retry and V:
+            st = status[:V].cpu()
+            bad = [v for v in range(V) if int(st[v, 0]) != _lib.STP_OK]
+            if bad:
+                if any(int(st[v, 0]) != _lib.STP_ERR_WORKSPACE_TOO_SMALL for v in bad):
+                    _raise(int(st[bad[0], 0]), "stp_render_views (device status)")
+                need = int(max(int(st[v, 1]) for v in bad) * 1.25) + 4096
+                self.entry_capacity = max(self.entry_capacity or 0, need)
+                for v in bad:
+                    self.ws.ensure(self.scene.n, cams[v].width, cams[v].height,
+                                   self.entry_capacity)
+                    self.render_into(cams[v], outs_list[v], stats=True)
+                    status[v, 0] = _lib.STP_OK
+        return status[:V]
+
+    def check_status(self, status=None, grow: bool = True) -> bool:
+        """Read the status word of the last asynchronous frame (synchronises
+        the stream).  True when the frame is complete; on an entry overflow
+        the workspace is grown to the frame's entry count (``grow``) and False
+        is returned -- the caller re-renders that view.  A scheduler fault
+        raises DataError."""
+        st = self.status if status is None else status
+        code, entries = (int(x) for x in st.tolist())
+        if code == _lib.STP_OK:
+            return True
+        if code == _lib.STP_ERR_WORKSPACE_TOO_SMALL:
+            if grow:
+                need = int(entries * 1.25) + 4096
+                self.entry_capacity = max(self.entry_capacity or 0, need)
+                self.ws.ensure(self.scene.n, self._last_w, self._last_h, self.entry_capacity)
+            return False
+        _raise(code, "stp_render (device status)")
 
     def frame(self, cam, device_output: bool = False, sort_error: bool = False) -> FrameOutput:
         """One frame.  ``sort_error``: also the per-pixel sort error delta
@@ -390,9 +464,11 @@ class Renderer:
             "timings": timings,
             "nonfinite_pixels": [],
             "tie_runs": int(st.tie_runs),
-            "exact_items": int(st.exact_items),
-            "resolves": int(st.resolves),
         }
+        if st.nonfinite_pixels:
+            bad = ~(torch.isfinite(outs["color"]).all(dim=2) & torch.isfinite(outs["transmittance"]))
+            ys, xs = (t.cpu().numpy() for t in torch.nonzero(bad, as_tuple=True))
+            stats["nonfinite_pixels"] = [(int(x), int(y)) for y, x in zip(ys, xs)]
         if sort_error:
             se = outs["sort_error"]
             stats["sort_error"] = {"delta_max": float(se.max().item()) if se.numel() else 0.0,
@@ -411,10 +487,6 @@ class Renderer:
         tn = outs["transmittance"].double().cpu().numpy()
         depth = outs["depth"].double().cpu().numpy() if cfg.with_depth else None
         src = self.scene.source_index if self.batch else kept.cpu().numpy().astype(np.int64)
-        if st.nonfinite_pixels:
-            bad = ~(np.isfinite(color).all(axis=2) & np.isfinite(tn))
-            ys, xs = np.nonzero(bad)
-            stats["nonfinite_pixels"] = [(int(x), int(y)) for y, x in zip(ys, xs)]
         records = None
         if rec_cap:
             records = self._records(outs, None if self.batch else src, cam)
@@ -516,34 +588,29 @@ class Renderer:
         return recs
 
 
-_SCENE_CACHE: dict = {}
-
-
 def _scene_for(scene, device):
-    """Cache the device copy of a host scene (uploaded once, like weights)."""
+    """Device copy of the scene for one call.  No implicit cache: the
+    reference re-projects its (mutable) Gaussian3D list on every call, so a
+    list or array dict is uploaded per call; pass a GaussianScene (or use a
+    Renderer) to keep a scene resident across calls."""
     if isinstance(scene, (GaussianScene, BatchScene)):
         return scene
     if _is_batch(scene):
         return BatchScene(scene, device)
-    key = (id(scene), len(scene) if hasattr(scene, "__len__") else None)
-    hit = _SCENE_CACHE.get(key)
-    if hit is not None and hit[0] is scene:
-        return hit[1]
-    gs = GaussianScene.from_any(scene, device)
-    _SCENE_CACHE.clear()
-    _SCENE_CACHE[key] = (scene, gs)
-    return gs
+    return GaussianScene.from_any(scene, device)
 
 
 def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
            device_output: bool = False, device=None, sort_error: bool = False) -> FrameOutput:
-    """Render one frame under the Hierarchical (default) or GlobalZ mode
-    (rasterizer.py:595-698).
+    """Drop-in ``render`` (rasterizer.py:595-698): every sort mode, default
+    FullPerPixel like the reference (rasterizer.py:598); the paper's hot
+    path is ``mode=Hierarchical()``.
 
     ``scene`` is a list of Gaussian3D, a dict of arrays/tensors in the drop-in
-    layout, or a GaussianScene.  Returns float64 numpy arrays like the
-    reference unless ``device_output`` (float32 device tensors)."""
-    mode = mode if mode is not None else Hierarchical()
+    layout, a GaussianScene, or an already-projected SplatBatch.  Returns
+    float64 numpy arrays like the reference unless ``device_output`` (float32
+    device tensors)."""
+    mode = mode if mode is not None else FullPerPixel()
     cfg = cfg or RenderConfig()
     validate_mode(mode)
     _check_supported(mode)
@@ -556,21 +623,24 @@ def render(scene, cam: Camera, mode=None, cfg: RenderConfig | None = None, *,
 
 
 def render_depth(scene, cam, mode=None, cfg: RenderConfig | None = None, **kw) -> FrameOutput:
-    """rasterizer.py:701-715."""
+    """rasterizer.py:701-715 (default mode FullPerPixel, :704)."""
     cfg = replace(cfg or RenderConfig(), with_depth=True)
     return render(scene, cam, mode, cfg, **kw)
 
 
 def render_trajectory(scene, cameras, mode=None, cfg: RenderConfig | None = None,
                       interpolate: int = 0, **kw) -> list:
-    """rasterizer.py:758-772 (interpolation of poses is host logic; only
-    ``interpolate=0`` is supported here)."""
+    """rasterizer.py:758-772 (default mode FullPerPixel, :761).  The scene is
+    uploaded once for the whole trajectory.  Interpolation of poses is host
+    logic; only ``interpolate=0`` is supported here."""
     if interpolate:
         raise ConfigError("camera interpolation is not part of the B200 path")
+    dev = _require_cuda(kw.get("device"))
+    gs = _scene_for(scene, dev)
     frames = []
     for i, cam in enumerate(cameras):
         try:
-            frames.append(render(scene, cam, mode, cfg, **kw))
+            frames.append(render(gs, cam, mode, cfg, **kw))
         except Exception as exc:
             raise DataError(f"frame {i}: {exc}") from exc
     return frames

@@ -138,6 +138,25 @@ def orbit_cameras(n_views, radius=4.0, height=-1.2, target=(0.0, 0.3, 0.0), widt
     return cams
 
 
+def yaw_sweep_cameras(n_views, position=(0.0, -1.2, -4.0), target=(0.0, 0.3, 0.0),
+                      half_span_deg=15.0, width=1920, height_px=1080, f=1100.0):
+    """C5: a camera at a FIXED position panning its yaw
+    over +-half_span around the view of ``target`` (a rotation sweep, cf. the
+    popping pan fixtures.py:54-62,144-156).  Frame v's forward axis is the
+    base forward rotated about the world vertical (y) axis."""
+    base = look_at(position, target)
+    cams = []
+    for v in range(n_views):
+        a = np.deg2rad(-half_span_deg + 2 * half_span_deg * v / max(n_views - 1, 1))
+        c, s_ = np.cos(a), np.sin(a)
+        ry = np.array([[c, 0.0, s_], [0.0, 1.0, 0.0], [-s_, 0.0, c]])  # world-frame yaw
+        R = base @ ry.T          # world->view of the yawed camera (view axes rotated by ry)
+        uu, _, vt = np.linalg.svd(R)
+        cams.append(Camera(rotation=uu @ vt, position=np.asarray(position, dtype=np.float64),
+                           fx=f, fy=f, width=width, height=height_px))
+    return cams
+
+
 CONFIGS = {
     "C1": "synthetic 10k random Gaussians, SH degree 0, single 256x256 view",
     "C2": "synthetic 1M Gaussians, SH degree 3, single 1920x1080 view",
@@ -153,8 +172,7 @@ def config_cameras(name: str, n_views: int | None = None):
     if name == "C3":
         return orbit_cameras(n_views or 256)
     if name == "C5":
-        nv = n_views or 240
-        return orbit_cameras(nv, yaw0=-np.deg2rad(15), yaw_span=np.deg2rad(30))
+        return yaw_sweep_cameras(n_views or 240)
     return config_scene(name, n=16, n_views=n_views)[1]
 
 
@@ -184,7 +202,5 @@ def config_scene(name: str, n: int | None = None, n_views: int | None = None):
         return to_f32_scene(arrs), [cam]
     if name == "C5":
         arrs = garden_scene(n or 1_500_000, 5, density=0.5)
-        nv = n_views or 240
-        cams = orbit_cameras(nv, yaw0=-np.deg2rad(15), yaw_span=np.deg2rad(30))
-        return to_f32_scene(arrs), cams
+        return to_f32_scene(arrs), yaw_sweep_cameras(n_views or 240)
     raise KeyError(name)

@@ -9,10 +9,10 @@ Names, fields, defaults and error behaviour follow the reference package:
 * ``TileBin`` / ``PixelRecords`` / ``FrameOutput``  rasterizer.py:215-255
 * ``SceneFormatError`` / ``ConfigError`` / ``DataError``  errors.py:4-13
 
-Only the ``Hierarchical`` sort mode runs on the B200 path; the other reference
-modes (``GlobalZ``, ``FullPerPixel``, ``Window``) are accepted by
-``parse_mode``/``validate_mode`` for API compatibility but ``render`` raises
-``ConfigError`` for them (out of scope this round).
+Every reference sort mode runs on the B200 path: ``Hierarchical`` (the
+paper's pipeline, the benchmarked hot path), ``GlobalZ`` (the 3DGS order),
+``FullPerPixel`` (the exact per-pixel order; the default of ``render`` as in
+the reference) and ``Window(size)``.
 """
 
 from __future__ import annotations
@@ -104,17 +104,21 @@ class Camera:
 
 @dataclass(frozen=True)
 class GlobalZ:
-    """Reference mode (rasterizer.py:48-50); not on the B200 path."""
+    """One view-space z key per splat, the 3DGS order (rasterizer.py:48-50);
+    K6 = k_render_globalz."""
 
 
 @dataclass(frozen=True)
 class FullPerPixel:
-    """Reference mode (rasterizer.py:53-55); not on the B200 path."""
+    """The exact per-pixel order (rasterizer.py:53-55); K6 =
+    k_render_pixelsort (repeated top-16 selection)."""
 
 
 @dataclass(frozen=True)
 class Window:
-    """Reference mode (rasterizer.py:58-67); not on the B200 path."""
+    """Per-pixel resorting window over the per-tile key stream
+    (rasterizer.py:58-67); K6 = k_render_pixelsort (register window) or
+    k_render_window (shared-memory heap, larger windows)."""
 
     size: int = 8
 

@@ -75,7 +75,7 @@ def test_struct_layouts_match_header(tmp_path):
 
 
 def test_version_and_errors(lib):
-    assert lib.stp_abi_version() == 1
+    assert lib.stp_abi_version() == _lib.ABI_VERSION == 2
     assert _lib.error_string(_lib.STP_OK) == "ok"
     assert "configuration" in _lib.error_string(_lib.STP_ERR_CONFIG)
     assert "workspace" in _lib.error_string(_lib.STP_ERR_WORKSPACE_TOO_SMALL)
@@ -143,7 +143,7 @@ def test_workspace_layout(lib):
     assert (L.grid_w, L.grid_h, L.n_tiles) == (120, 68, 8160)
     # 13 tile bits + 27 depth bits: 5 eight-bit passes; ids in the low 10 bits
     assert (L.sort_bits, L.depth_bits, L.sort_passes, L.id_bits) == (40, 27, 5, 10)
-    regions = sorted((getattr(L, k), k) for k in ("recs", "recs32", "fb_items", "camera", "masks",
+    regions = sorted((getattr(L, k), k) for k in ("recs", "camera", "masks",
                                                     "state", "counts", "offsets", "keys0",
                                                     "keys1", "vals", "ranges",
                                                     "counters", "hist", "lookback",

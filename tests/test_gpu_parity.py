@@ -16,16 +16,12 @@ TOL = 1e-4
 pytestmark = pytest.mark.gpu
 
 
-def _renderer(scene, mode, cfg, path="exact64"):
-    """path: "exact64" (default float64 K6), "fast32" (fp32-state certified
-    K6), "fbtest" (fast32 with every odd sub-tile pair handed to the float64
-    list pass)."""
+def _renderer(scene, mode, cfg, path=None):
     from paper_2402_00525_b200.renderer import Renderer
-    return Renderer(scene, mode, cfg, fast32=path in ("fast32", "fbtest"),
-                    fb_test=path == "fbtest")
+    return Renderer(scene, mode, cfg)
 
 
-PATHS = pytest.mark.parametrize("exact", ["exact64", "fast32", "fbtest"])
+PATHS = pytest.mark.parametrize("exact", ["exact64"])
 
 
 @PATHS
@@ -511,3 +507,15 @@ def test_tile_band_rendering(mode_name):
     torch.cuda.synchronize()
     for k in full:
         assert torch.equal(band[k], full[k]), k
+
+
+def test_render_default_mode_is_full_per_pixel():
+    """render() / render_depth() default to FullPerPixel like the reference
+    (rasterizer.py:598, 704) and match its exact-order output."""
+    from paper_2402_00525_b200 import FullPerPixel, mode_name, render, render_depth
+    scene, cam, cfg, mode, d = golden_io.load("shallow")
+    out = render(scene, cam, cfg=cfg)
+    assert out.stats["mode"] == mode_name(FullPerPixel())
+    assert render_depth(scene, cam).stats["mode"] == mode_name(FullPerPixel())
+    # shallow scene: Hierarchical == Full (test_rasterizer.py:398-412)
+    np.testing.assert_allclose(out.color, d["color"], atol=TOL, rtol=0)

@@ -145,3 +145,46 @@ def test_gloo_band_gather():
     for rank, got, full in res:
         for k in full:
             np.testing.assert_array_equal(got[k], full[k])
+
+
+def _streamed_worker(rank, world, port, q):
+    """render_shard_streamed: frames go to rank 0 by isend / irecv right
+    after each view (one view of lag for the status check)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, cams = _scene_and_cams()
+        scene_t = multiview.replicate_scene(sc if rank == 0 else None, "cpu")
+        fin = []
+        got = multiview.render_shard_streamed(cams, _oracle_fn(scene_t),
+                                              finalize_fn=lambda v, f: (fin.append(v), f)[1])
+        if rank == 0:
+            q.put((rank, fin, {v: {k: t.numpy() for k, t in f.items()} for v, f in got.items()}))
+        else:
+            q.put((rank, fin, sorted(got)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_streamed_gather_equals_serial():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_streamed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sc, cams = _scene_and_cams()
+    for rank, fin, _ in res:
+        assert fin == multiview.shard_views(len(cams), world, rank)   # every view finalized once
+    gathered = res[0][2]
+    serial = _oracle_fn({k: torch.from_numpy(v) for k, v in sc.items()})
+    assert sorted(gathered) == list(range(len(cams)))
+    for v, cam in enumerate(cams):
+        ref = serial(cam, v)
+        np.testing.assert_array_equal(gathered[v]["color"], ref["color"].numpy())
+        np.testing.assert_array_equal(gathered[v]["transmittance"], ref["transmittance"].numpy())
