@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define STP_ABI_VERSION 2
+#define STP_ABI_VERSION 3
 
 /* Status codes.  CONFIG -> ConfigError (rasterizer.py:93-117, 196-203),
  * DATA -> DataError (rasterizer.py:770-771), WORKSPACE_TOO_SMALL -> the host
@@ -113,12 +113,14 @@ typedef struct {
  * order for every pixel (rasterizer.py:472-485, the 3DGS baseline);
  * FULL: the exact per-pixel order (rasterizer.py:488-501); WINDOW: a
  * per-pixel resorting window of q_head entries over the per-tile-key stream
- * (rasterizer.py:504-588, Window.size -> q_head, 1..16).  Queue fields other
- * than q_head (WINDOW) are ignored outside HIERARCHICAL. */
+ * (rasterizer.py:504-588, Window.size -> q_head, 1..STP_WINDOW_MAX: a
+ * register window up to 16, a per-pixel shared-memory heap above).  Queue
+ * fields other than q_head (WINDOW) are ignored outside HIERARCHICAL. */
 #define STP_MODE_HIERARCHICAL 0
 #define STP_MODE_GLOBALZ 1
 #define STP_MODE_FULL 2
 #define STP_MODE_WINDOW 3
+#define STP_WINDOW_MAX 512
 
 #define STP_FLAG_TIMINGS 1  /* record per-stage CUDA-event timings (syncs) */
 
@@ -151,6 +153,16 @@ typedef struct {
                             report (stp_render(stats = NULL),
                             stp_render_events, one word per view in
                             stp_render_views).                              */
+  /* float64 outputs (the reference's FrameOutput precision, rasterizer.py:
+   * 246-255), all optional.  With color64 set, K6 also accumulates each
+   * pixel's colour and depth in float64 and composites the background in
+   * float64 (the float32 buffers above are still written); rec_t64 /
+   * rec_alpha64 receive the blend records' t and alpha in float64. */
+  double* color64;          /* [H,W,3] or NULL                              */
+  double* transmittance64;  /* [H,W]   (with color64)                       */
+  double* depth64;          /* [H,W]   or NULL (with color64)               */
+  double* rec_t64;          /* [H,W,record_cap] or NULL                     */
+  double* rec_alpha64;      /* [H,W,record_cap] or NULL                     */
 } StpOutputs;
 
 /* stats dict of rasterizer.py:683-690 (+ projection stats

@@ -16,7 +16,7 @@ STP_OK, STP_ERR_CONFIG, STP_ERR_DATA, STP_ERR_WORKSPACE_TOO_SMALL, STP_ERR_CUDA 
 STP_FLAG_TIMINGS = 1
 STP_STAGE_EVENTS = 5    # [K0+K1 | K2+K3 | K4+K5 | K6]
 STP_KERNEL_EVENTS = 8   # [K0 | K1 | K2 | K3 | K4 | K5 | K6]
-ABI_VERSION = 2
+ABI_VERSION = 3
 STP_MODE_HIERARCHICAL = 0
 STP_MODE_GLOBALZ = 1
 STP_MODE_FULL = 2
@@ -70,7 +70,10 @@ class StpOutputs(ctypes.Structure):
                 ("depth", ctypes.c_void_p), ("rec_count", ctypes.c_void_p),
                 ("rec_splat", ctypes.c_void_p), ("rec_t", ctypes.c_void_p),
                 ("rec_alpha", ctypes.c_void_p), ("state", ctypes.c_void_p),
-                ("sort_error", ctypes.c_void_p), ("status", ctypes.c_void_p)]
+                ("sort_error", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("color64", ctypes.c_void_p), ("transmittance64", ctypes.c_void_p),
+                ("depth64", ctypes.c_void_p), ("rec_t64", ctypes.c_void_p),
+                ("rec_alpha64", ctypes.c_void_p)]
 
 
 class StpGrads(ctypes.Structure):

@@ -110,9 +110,10 @@ int cfg_check(const StpConfig* c) {
   if (c->tile_end > 0 && (c->tile_begin < 0 || c->tile_begin >= c->tile_end))
     return STP_ERR_CONFIG;
   if (c->sort_mode == STP_MODE_GLOBALZ || c->sort_mode == STP_MODE_FULL) return STP_OK;
-  // Window(size): validate_mode (rasterizer.py:96-98) + the register window
-  if (c->sort_mode == STP_MODE_WINDOW) return (c->q_head >= 1 && c->q_head <= 16) ? STP_OK
-                                                                                 : STP_ERR_CONFIG;
+  // Window(size): validate_mode (rasterizer.py:96-98); a register window up
+  // to 16, a shared-memory heap up to STP_WINDOW_MAX
+  if (c->sort_mode == STP_MODE_WINDOW)
+    return (c->q_head >= 1 && c->q_head <= STP_WINDOW_MAX) ? STP_OK : STP_ERR_CONFIG;
   // validate_mode (rasterizer.py:98-115)
   if (c->q_tail < 64 || c->q_tail % 32 != 0) return STP_ERR_CONFIG;
   if (c->q_mid < 4 || c->q_mid % 4 != 0) return STP_ERR_CONFIG;

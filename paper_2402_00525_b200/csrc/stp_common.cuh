@@ -451,7 +451,9 @@ void launch_duplicate(const Frame& f, cudaStream_t s);
 int launch_sort(const Frame& f, cudaStream_t s);  // returns the buffer holding the result
 void launch_ranges(const Frame& f, int buf, cudaStream_t s);
 // K6 extra modes (stp_render.cu) and the backward pass's buffers
-constexpr int XM_NONE = 0, XM_SERR = 1, XM_FWD = 2, XM_BWD = 3;
+// XM_F64: the forward render with float64 colour / depth accumulation and
+// float64 outputs (StpOutputs.color64 ...), plus the sort error when asked
+constexpr int XM_NONE = 0, XM_SERR = 1, XM_FWD = 2, XM_BWD = 3, XM_F64 = 4;
 struct DevGrads {
   const double* upstream;  // [H,W,3] dL/d colour
   double* pix;             // [H,W,4]: float64 blended colour sum (3) + final T

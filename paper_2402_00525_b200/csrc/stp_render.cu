@@ -29,6 +29,8 @@
 // its 16 pixels have T < 1e-4 (blends of terminated pixels are no-ops, so
 // stopping is output-identical).  Rects stay full size at image borders
 // (hierarchy.py:124-142); pixels outside the image run as terminated.
+#include <algorithm>
+
 #include "stp_common.cuh"
 
 namespace stp {
@@ -95,6 +97,9 @@ struct Head {
 //            backward pass's first replay)
 //   XM_BWD   the backward replay (gradients.py:103-162): the same blend order
 //            recomputed, each contribution's gradients scattered
+//   XM_F64   + float64 colour / depth sums, float64 outputs composited over
+//            the background in float64 (the reference's output precision),
+//            and the sort error when StpOutputs.sort_error is set
 
 struct Pixel {
   double px, py;
@@ -109,6 +114,7 @@ struct Pixel {
   double a0, a1, a2;  // XM_BWD: running sum (acc)
   double g0, g1, g2;  // XM_BWD: upstream dL/dcolour of the pixel
   double tn;          // XM_BWD: the pixel's final T
+  double dd;          // XM_F64: float64 depth sum
 };
 
 struct RenderArgs {
@@ -134,6 +140,7 @@ __device__ __forceinline__ void xm_init(Pixel& P, const RenderArgs& A) {
   P.a0 = P.a1 = P.a2 = 0.0;
   P.g0 = P.g1 = P.g2 = 0.0;
   P.tn = 0.0;
+  P.dd = 0.0;
   if (XM == XM_BWD && P.pix >= 0) {
     const double* g = A.grad.upstream + P.pix * 3;
     P.g0 = g[0];
@@ -181,10 +188,11 @@ __device__ __noinline__ void bwd_step(Pixel& P, const RenderArgs& A, double al, 
 template <int XM>
 __device__ __forceinline__ void xm_step(Pixel& P, const RenderArgs& A, double t, double al,
                                         uint32_t id, float4 oc) {
-  if (XM == XM_SERR) {
+  if (XM == XM_SERR || XM == XM_F64) {
     P.serr += fmax(P.tprev - t, 0.0);
     P.tprev = t;
-  } else if (XM == XM_FWD) {
+  }
+  if (XM == XM_FWD || XM == XM_F64) {
     const double w = al * P.T;
     P.f0 += (double)oc.y * w;
     P.f1 += (double)oc.z * w;
@@ -199,6 +207,15 @@ template <int XM>
 __device__ __forceinline__ void xm_done(const Pixel& P, const RenderArgs& A) {
   if (P.pix < 0) return;
   if (XM == XM_SERR) A.out.sort_error[P.pix] = (float)P.serr;
+  if (XM == XM_F64) {
+    if (A.out.sort_error) A.out.sort_error[P.pix] = (float)P.serr;
+    double* c = A.out.color64 + P.pix * 3;
+    c[0] = P.f0 + P.T * A.cfg.bg[0];
+    c[1] = P.f1 + P.T * A.cfg.bg[1];
+    c[2] = P.f2 + P.T * A.cfg.bg[2];
+    if (A.out.transmittance64) A.out.transmittance64[P.pix] = P.T;
+    if (A.out.depth64) A.out.depth64[P.pix] = P.dd;
+  }
   if (XM == XM_FWD) {
     double* q = A.grad.pix + P.pix * 4;
     q[0] = P.f0;
@@ -216,6 +233,8 @@ __device__ __noinline__ void write_record(StpOutputs out, int cap, int64_t pix, 
     out.rec_splat[o] = (int32_t)id;
     out.rec_t[o] = (float)t;
     out.rec_alpha[o] = (float)al;
+    if (out.rec_t64) out.rec_t64[o] = t;
+    if (out.rec_alpha64) out.rec_alpha64[o] = al;
   }
 }
 
@@ -231,6 +250,7 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
   P.C1 += oc.z * wf;
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
+  if (XM == XM_F64) P.dd += t * w;
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
   xm_step<XM>(P, A, t, al, id, oc);
   P.T = P.T * (1.0 - al);
@@ -247,6 +267,7 @@ __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double
   P.C1 += oc.z * wf;
   P.C2 += oc.w * wf;
   P.D += (float)(t * w);
+  if (XM == XM_F64) P.dd += t * w;
   if (A.cfg.rec_cap > 0) write_record(A.out, A.cfg.rec_cap, P.pix, P.rc++, t, al, id);
   xm_step<XM>(P, A, t, al, id, oc);
   P.T = P.T * (1.0 - al);
@@ -1228,7 +1249,8 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
   R.out = A.out;
   R.counters = A.counters;
   R.grad = A.grad;
-  const bool need_t = A.cfg.rec_cap > 0 || A.xm == XM_SERR;
+  const bool need_t = A.cfg.rec_cap > 0 || A.xm == XM_SERR ||
+                      (A.xm == XM_F64 && A.out.sort_error != nullptr);
   for (int band = blockIdx.x; band < A.n_tiles; band += gridDim.x) {
     const int tile = band + A.tile0;
     const int tx = tile % A.gw, ty = tile / A.gw;
@@ -1281,6 +1303,7 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
         P.C1 += oc.z * wf;
         P.C2 += oc.w * wf;
         P.D += (float)(s_dist[k] * wt);
+        if (A.xm == XM_F64) P.dd += s_dist[k] * wt;
         double t = 0.0;
         if (need_t) {
           const SplatRec* r = A.recs + s_id[k];
@@ -1291,6 +1314,7 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
           case XM_SERR: xm_step<XM_SERR>(P, R, t, al, s_id[k], oc); break;
           case XM_FWD: xm_step<XM_FWD>(P, R, t, al, s_id[k], oc); break;
           case XM_BWD: xm_step<XM_BWD>(P, R, t, al, s_id[k], oc); break;
+          case XM_F64: xm_step<XM_F64>(P, R, t, al, s_id[k], oc); break;
           default: break;
         }
         P.T = P.T * (1.0 - al);
@@ -1300,6 +1324,7 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
     switch (A.xm) {
       case XM_SERR: xm_done<XM_SERR>(P, R); break;
       case XM_FWD: xm_done<XM_FWD>(P, R); break;
+      case XM_F64: xm_done<XM_F64>(P, R); break;
       default: break;
     }
     if (P.pix >= 0 && A.xm != XM_BWD) {
@@ -1471,14 +1496,173 @@ static void launch_pixelsort_t(const RenderArgs& A, int xm, cudaStream_t s) {
     case XM_SERR: k_render_pixelsort<QH, EXACT, FULL, XM_SERR><<<A.n_items, 256, 0, s>>>(A); break;
     case XM_FWD: k_render_pixelsort<QH, EXACT, FULL, XM_FWD><<<A.n_items, 256, 0, s>>>(A); break;
     case XM_BWD: k_render_pixelsort<QH, EXACT, FULL, XM_BWD><<<A.n_items, 256, 0, s>>>(A); break;
+    case XM_F64: k_render_pixelsort<QH, EXACT, FULL, XM_F64><<<A.n_items, 256, 0, s>>>(A); break;
     default: k_render_pixelsort<QH, EXACT, FULL, XM_NONE><<<A.n_items, 256, 0, s>>>(A); break;
   }
+}
+
+// ---------------------------------------------------------------------------
+// K6 under Window(size > 16) (rasterizer.py:504-588): the window is a
+// per-pixel binary min-heap of (t, rank) in shared memory, laid out
+// [slot][lane] so every heap access of a warp is bank-conflict free.  The
+// reference's window is a set with "emit the smaller of (incoming, window
+// minimum) on overflow, drain in (t, rank) order" -- exactly a bounded
+// min-heap (ranks are unique, so the order is total).  A slot stores (t,
+// rank) only; alpha of a popped entry is re-evaluated (emit_eval_bf is
+// deterministic: the same t and alpha as at insertion), which keeps 12 B per
+// slot: up to kWindowMax entries per pixel for a 32-pixel warp (one warp per
+// block: 16 x 2 pixels, 8 warps per tile).
+constexpr int kWindowMax = STP_WINDOW_MAX;
+constexpr int kWinPix = 32;
+
+__host__ __device__ inline size_t window_smem_bytes(int cap) {
+  return (size_t)cap * kWinPix * (sizeof(double) + sizeof(uint32_t));
+}
+
+template <int XM>
+__global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double s_tab[64];
+  for (int i = threadIdx.x; i < 64; i += kWinPix) s_tab[i] = kExp2Tab[i];
+  __syncwarp();
+  const int lane = threadIdx.x;
+  double* hd = reinterpret_cast<double*>(smem_raw) + lane;                    // [slot][lane]
+  uint32_t* hid = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem_raw) +
+                                              (size_t)cap * kWinPix) + lane;
+  const double term = A.cfg.term;
+  for (int item = blockIdx.x; item < A.n_items * 8; item += gridDim.x) {
+    const int tile = item / 8 + A.tile0, strip = item % 8;
+    const int tx = tile % A.gw, ty = tile / A.gw;
+    Pixel P;
+    {
+      const int gx = tx * kTile + (lane & 15), gy = ty * kTile + 2 * strip + (lane >> 4);
+      const bool in_img = gx < A.cam.W && gy < A.cam.H;
+      P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
+      P.px = (double)gx + 0.5;
+      P.py = (double)gy + 0.5;
+      cam_ray(A.cam, P.px, P.py, P.u, P.w, P.vn);
+      P.T = in_img ? 1.0 : 0.0;
+      P.C0 = P.C1 = P.C2 = P.D = 0.f;
+      P.rc = 0;
+      xm_init<XM>(P, A);
+    }
+    // place (xd, xi) in the root's hole and sift it down over n elements
+    auto sift_down = [&](double xd, uint32_t xi, int n) {
+      int p = 0;
+      for (;;) {
+        int c = 2 * p + 1;
+        if (c >= n) break;
+        double cd = hd[(size_t)c * kWinPix];
+        uint32_t ci = hid[(size_t)c * kWinPix];
+        if (c + 1 < n) {
+          const double rd = hd[(size_t)(c + 1) * kWinPix];
+          const uint32_t ri = hid[(size_t)(c + 1) * kWinPix];
+          if (lt(rd, ri, cd, ci)) {
+            ++c;
+            cd = rd;
+            ci = ri;
+          }
+        }
+        if (!lt(cd, ci, xd, xi)) break;
+        hd[(size_t)p * kWinPix] = cd;
+        hid[(size_t)p * kWinPix] = ci;
+        p = c;
+      }
+      hd[(size_t)p * kWinPix] = xd;
+      hid[(size_t)p * kWinPix] = xi;
+    };
+    // blend the popped minimum (t0, i0): alpha re-evaluated
+    auto blend_min = [&](double t0, uint32_t i0) {
+      double t, al;
+      emit_eval_bf(P, A, i0, s_tab, t, al);
+      blend<XM>(P, A, t0, al, i0);
+    };
+    const uint2 rg = A.ranges[tile];
+    int n = 0;
+    for (uint32_t j = rg.x; j < rg.y; ++j) {
+      if (!__any_sync(kFull, P.T >= term)) break;
+      const uint32_t id = A.vals[j];
+      double t, al;
+      const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
+      if (!(pass && P.T >= term)) continue;
+      if (n < cap) {
+        // sift up
+        int c = n++;
+        while (c > 0) {
+          const int p = (c - 1) >> 1;
+          const double pd = hd[(size_t)p * kWinPix];
+          const uint32_t pi = hid[(size_t)p * kWinPix];
+          if (!lt(t, id, pd, pi)) break;
+          hd[(size_t)c * kWinPix] = pd;
+          hid[(size_t)c * kWinPix] = pi;
+          c = p;
+        }
+        hd[(size_t)c * kWinPix] = t;
+        hid[(size_t)c * kWinPix] = id;
+      } else if (lt(t, id, hd[0], hid[0])) {
+        blend<XM>(P, A, t, al, id);  // the incoming entry is the smallest: emitted
+      } else {
+        // emit the minimum; the incoming entry takes its place
+        const double t0 = hd[0];
+        const uint32_t i0 = hid[0];
+        sift_down(t, id, n);
+        blend_min(t0, i0);
+      }
+    }
+    // drain in ascending (t, rank) (rasterizer.py:565-573); no-ops once terminated
+    while (n > 0 && P.T >= term) {
+      const double t0 = hd[0];
+      const uint32_t i0 = hid[0];
+      --n;
+      sift_down(hd[(size_t)n * kWinPix], hid[(size_t)n * kWinPix], n);
+      blend_min(t0, i0);
+    }
+    xm_done<XM>(P, A);
+    if (P.pix >= 0 && XM != XM_BWD) {
+      const float T = (float)P.T;
+      const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
+      const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
+      const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
+      A.out.color[P.pix * 3 + 0] = c0;
+      A.out.color[P.pix * 3 + 1] = c1;
+      A.out.color[P.pix * 3 + 2] = c2;
+      A.out.transmittance[P.pix] = T;
+      if (A.out.depth) A.out.depth[P.pix] = P.D;
+      if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
+      if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
+        atomicAdd(A.counters + C_NONFINITE, 1ull);
+    }
+  }
+}
+
+template <int XM>
+static void launch_window_t(const RenderArgs& A, int cap, cudaStream_t s) {
+  const size_t smem = window_smem_bytes(cap);
+  cudaFuncSetAttribute(k_render_window<XM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_window<XM>, kWinPix, smem);
+  const long long items = (long long)A.n_items * 8;
+  const long long grid = std::min<long long>(items, (long long)device_sm_count() *
+                                                        std::max(per_sm, 1));
+  k_render_window<XM><<<(int)grid, kWinPix, smem, s>>>(A, cap);
 }
 
 static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
                                     cudaStream_t s) {
   if (f.sort_mode == STP_MODE_FULL) {
     launch_pixelsort_t<16, true, true>(A, xm, s);
+    return;
+  }
+  if (f.cfg.q_head > 16) {
+    if (A.n_items <= 0) return;
+    switch (xm) {
+      case XM_SERR: launch_window_t<XM_SERR>(A, f.cfg.q_head, s); break;
+      case XM_FWD: launch_window_t<XM_FWD>(A, f.cfg.q_head, s); break;
+      case XM_BWD: launch_window_t<XM_BWD>(A, f.cfg.q_head, s); break;
+      case XM_F64: launch_window_t<XM_F64>(A, f.cfg.q_head, s); break;
+      default: launch_window_t<XM_NONE>(A, f.cfg.q_head, s); break;
+    }
     return;
   }
   switch (f.cfg.q_head) {  // the window size
@@ -1495,6 +1679,7 @@ static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
 // XM_FWD / XM_BWD; a non-null out.sort_error selects XM_SERR.
 void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t s, int xm,
                    const DevGrads* g) {
+  if (xm == XM_NONE && out.color64) xm = XM_F64;
   if (xm == XM_NONE && out.sort_error) xm = XM_SERR;
   if (f.globalz) {
     launch_render_globalz(f, out, s, xm, g);
@@ -1529,6 +1714,10 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
       case XM_FWD:
         if (dflt) launch_render_t<4, true, 8, 64, XM_FWD>(A, smem, s);
         else launch_render_t<16, false, 0, 0, XM_FWD>(A, smem, s);
+        break;
+      case XM_F64:
+        if (dflt) launch_render_t<4, true, 8, 64, XM_F64>(A, smem, s);
+        else launch_render_t<16, false, 0, 0, XM_F64>(A, smem, s);
         break;
       default:
         if (dflt) launch_render_t<4, true, 8, 64, XM_BWD>(A, smem, s);

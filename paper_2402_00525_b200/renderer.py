@@ -153,7 +153,7 @@ def _is_globalz(mode) -> bool:
     return type(mode).__name__ == "GlobalZ"
 
 
-WINDOW_MAX = 16
+WINDOW_MAX = 512   # stp.h STP_WINDOW_MAX: register window <= 16, shared-memory heap above
 
 
 def _check_supported(mode) -> None:
@@ -300,7 +300,11 @@ class Renderer:
             _raise(rc, "configuration")
 
     def alloc_outputs(self, width, height, record_cap: int = 0, with_state: bool = False,
-                      sort_error: bool = False):
+                      sort_error: bool = False, f64: bool = False):
+        """Device output buffers for render_into.  ``f64``: also the float64
+        outputs (StpOutputs.color64 ...: colour / depth accumulated and the
+        background composited in float64, records' t and alpha in float64 --
+        the reference's FrameOutput precision)."""
         d = self.device
         o = {"color": torch.empty((height, width, 3), dtype=torch.float32, device=d),
              "transmittance": torch.empty((height, width), dtype=torch.float32, device=d)}
@@ -315,13 +319,23 @@ class Renderer:
             o["state"] = torch.empty(max(1, self.scene.n), dtype=torch.uint8, device=d)
         if sort_error:
             o["sort_error"] = torch.empty((height, width), dtype=torch.float32, device=d)
+        if f64:
+            f = torch.float64
+            o["color64"] = torch.empty((height, width, 3), dtype=f, device=d)
+            o["transmittance64"] = torch.empty((height, width), dtype=f, device=d)
+            if self.cfg.with_depth:
+                o["depth64"] = torch.empty((height, width), dtype=f, device=d)
+            if record_cap > 0:
+                o["rec_t64"] = torch.empty((height, width, record_cap), dtype=f, device=d)
+                o["rec_alpha64"] = torch.empty((height, width, record_cap), dtype=f, device=d)
         return o
 
     @staticmethod
     def outputs_struct(o: dict) -> _lib.StpOutputs:
         s = _lib.StpOutputs()
         for k in ("color", "transmittance", "depth", "rec_count", "rec_splat", "rec_t",
-                  "rec_alpha", "state", "sort_error", "status"):
+                  "rec_alpha", "state", "sort_error", "status", "color64", "transmittance64",
+                  "depth64", "rec_t64", "rec_alpha64"):
             if k in o:
                 setattr(s, k, o[k].data_ptr())
         return s
@@ -341,6 +355,10 @@ class Renderer:
         tiles are left untouched)."""
         c_cam = make_camera(cam)
         self._ensure(cam)
+        if not record_cap and "rec_splat" in outs:
+            record_cap = int(outs["rec_splat"].shape[2])   # the buffers' capacity
+        if record_cap and "rec_splat" not in outs:
+            raise DataError("record_cap > 0 needs record buffers (alloc_outputs(record_cap=...))")
         c_cfg = make_config(self.cfg, self.mode, record_cap, timings, tiles)
         c_out = self.outputs_struct(outs)
         if "status" not in outs:
@@ -438,8 +456,10 @@ class Renderer:
         t0 = time.perf_counter()
         rec_cap = 64 if cfg.capture_records else 0
         while True:
+            # the float64 FrameOutput of the reference (rasterizer.py:246-255):
+            # float64 colour / depth sums and records; device tensors stay fp32
             outs = self.alloc_outputs(cam.width, cam.height, rec_cap, with_state=True,
-                                      sort_error=sort_error)
+                                      sort_error=sort_error, f64=not device_output)
             st = self.render_into(cam, outs, stats=True, timings=True, record_cap=rec_cap)
             if rec_cap and int(outs["rec_count"].max().item()) > rec_cap:
                 rec_cap = int(outs["rec_count"].max().item())
@@ -483,9 +503,9 @@ class Renderer:
                                                     "rec_alpha")}
             timings["total"] = time.perf_counter() - t0
             return out
-        color = outs["color"].double().cpu().numpy()
-        tn = outs["transmittance"].double().cpu().numpy()
-        depth = outs["depth"].double().cpu().numpy() if cfg.with_depth else None
+        color = outs["color64"].cpu().numpy()
+        tn = outs["transmittance64"].cpu().numpy()
+        depth = outs["depth64"].cpu().numpy() if cfg.with_depth else None
         src = self.scene.source_index if self.batch else kept.cpu().numpy().astype(np.int64)
         records = None
         if rec_cap:
@@ -572,8 +592,8 @@ class Renderer:
     def _records(outs, src, cam):
         cnt = outs["rec_count"].cpu().numpy()
         spl = outs["rec_splat"].cpu().numpy()
-        tt = outs["rec_t"].double().cpu().numpy()
-        aa = outs["rec_alpha"].double().cpu().numpy()
+        tt = outs["rec_t64" if "rec_t64" in outs else "rec_t"].double().cpu().numpy()
+        aa = outs["rec_alpha64" if "rec_alpha64" in outs else "rec_alpha"].double().cpu().numpy()
         # Gaussian id -> batch rank (projection preserves source order);
         # a SplatBatch input is indexed by rank already
         rank = spl if src is None else np.searchsorted(src, spl)

@@ -145,7 +145,7 @@ def save(name, arrs, cam, mode, cfg, sh_coeffs=16, rec_pixels=None, store_batch=
           f"ref={dt:.2f}s -> {os.path.getsize(path) / 1e6:.2f} MB", flush=True)
 
 
-def main(only=None):
+def main(only=None, only_grads=None):
     H = S.Hierarchical()
     jobs = {}
 
@@ -263,12 +263,28 @@ def main(only=None):
              S.RenderConfig(with_depth=True))
     jobs["pixelsort"] = pixelsort
 
+    # 10b. Window(k) beyond the register window (k > 16): the paper's Table-1
+    #      window 24 and a 64-entry window whose overflow
+    #      path still triggers on the deep border fixture
+    def windows():
+        gs, cams, _ = random_cloud(300, seed=5)
+        a = from_gaussians(gs)
+        save("win24_cloud300", a, cams[0], S.Window(24), S.RenderConfig(with_depth=True))
+        arrs = scenes.frustum_cloud(1500, 21, 203, 117, 150.0, z_lo=1.0, z_hi=5.0)
+        arrs["scales"] = arrs["scales"] * 4.0
+        pos = np.array([0.1, -0.05, -0.2])
+        R = scenes.look_at(pos, np.array([0.15, 0.0, 3.0]))
+        cam = axis_cam(203, 117, f=150.0, R=R, pos=pos, cx=97.3, cy=61.9)
+        save("win64_sh3_border", scenes.to_f32_scene(arrs), cam, S.Window(64),
+             S.RenderConfig(with_depth=True))
+    jobs["windows"] = windows
+
     # 11. backward pass (gradients.py:84-162): reference gradients w.r.t. the
     #     projected batch for a seeded upstream dL/dcolour, per fixture/mode
     def grads():
         from splatsort import gradients as SG
-        for fx in ("cloud300", "shallow", "sh3_border", "gz_cloud300", "win8_cloud300",
-                   "edges"):
+        for fx in (only_grads or ("cloud300", "shallow", "sh3_border", "gz_cloud300",
+                                  "win8_cloud300", "edges", "win24_cloud300")):
             z = np.load(os.path.join(HERE, f"{fx}.npz"))
             d = {k: z[k] for k in z.files}
             arrs = {k: d[k] for k in ("means", "quats", "scales", "opacity", "sh")}
@@ -365,4 +381,10 @@ def main(only=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or None)
+    # make_golden.py [job ...] [--grads fixture ...]
+    argv = sys.argv[1:]
+    grads_only = None
+    if "--grads" in argv:
+        i = argv.index("--grads")
+        grads_only, argv = tuple(argv[i + 1:]), argv[:i]
+    main(argv or None, grads_only)

@@ -75,7 +75,7 @@ def test_struct_layouts_match_header(tmp_path):
 
 
 def test_version_and_errors(lib):
-    assert lib.stp_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.stp_abi_version() == _lib.ABI_VERSION == 3
     assert _lib.error_string(_lib.STP_OK) == "ok"
     assert "configuration" in _lib.error_string(_lib.STP_ERR_CONFIG)
     assert "workspace" in _lib.error_string(_lib.STP_ERR_WORKSPACE_TOO_SMALL)
@@ -106,14 +106,14 @@ def test_validate_config_rejects(lib, field, value):
 
 
 def test_validate_config_modes_and_bands(lib):
-    """Sort modes (GlobalZ / FullPerPixel / Window <= 16) and K6 tile bands
+    """Sort modes (GlobalZ / FullPerPixel / Window <= 512) and K6 tile bands
     through the host-side config check (no device work)."""
     from paper_2402_00525_b200 import FullPerPixel, GlobalZ, Window
     from paper_2402_00525_b200.renderer import make_config
-    for m in (GlobalZ(), FullPerPixel(), Window(1), Window(8), Window(16)):
+    for m in (GlobalZ(), FullPerPixel(), Window(1), Window(8), Window(16), Window(17), Window(512)):
         c = make_config(RenderConfig(), m)
         assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_OK, m
-    c = make_config(RenderConfig(), Window(17))
+    c = make_config(RenderConfig(), Window(513))
     assert lib.stp_validate_config(ctypes.byref(c)) == _lib.STP_ERR_CONFIG
     c = _cfg()
     c.sort_mode = 7

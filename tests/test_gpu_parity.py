@@ -134,7 +134,7 @@ def test_config_errors_raise():
     with pytest.raises(ConfigError):
         render(scene, cam, Window(0), RenderConfig())      # validate_mode
     with pytest.raises(ConfigError):
-        render(scene, cam, Window(17), RenderConfig())     # B200 register window
+        render(scene, cam, Window(513), RenderConfig())    # B200 window envelope (stp.h)
     with pytest.raises(ConfigError):
         render(scene, cam, Hierarchical(queue_tail=48), RenderConfig())
     with pytest.raises(ConfigError):
@@ -310,11 +310,12 @@ def test_sort_error_scaled_globalz_vs_hierarchical():
     assert avg["Hierarchical"] < avg["GlobalZ"]
 
 
-@pytest.mark.parametrize("mode_name", ["full", "window:8", "window:3"])
+@pytest.mark.parametrize("mode_name", ["full", "window:8", "window:3", "window:24", "window:100"])
 def test_oracle_parity_pixelsort_modes(mode_name):
     """FullPerPixel (exact per-pixel order by repeated top-16 selection) and
-    Window(k) on the C3 layout at 60k Gaussians vs the oracle: tile lists,
-    order, blend sequences, pixels; FullPerPixel has zero sort error."""
+    Window(k) (register window k <= 16, shared-memory heap above) on the C3
+    layout at 60k Gaussians vs the oracle: tile lists, order, blend
+    sequences, pixels; FullPerPixel has zero sort error."""
     from paper_2402_00525_b200 import RenderConfig, parse_mode, scenes, sort_error
     from paper_2402_00525_b200.renderer import Renderer
     arrs = scenes.to_f32_scene(scenes.garden_scene(60_000, 3))
@@ -324,6 +325,22 @@ def test_oracle_parity_pixelsort_modes(mode_name):
     if mode_name == "full":
         out = Renderer(arrs, mode, RenderConfig()).frame(cam, sort_error=True)
         assert sort_error(out).delta_max == 0.0
+
+
+def test_large_window_equals_full():
+    """test_rasterizer.py:377-383: a window that can hold a whole bin never
+    overflows, so it blends in the exact per-pixel order -- bit-equal to
+    FullPerPixel (300-splat cloud: every bin holds <= 300 entries)."""
+    from paper_2402_00525_b200 import FullPerPixel, Window
+    scene, cam, cfg, _, d = golden_io.load("full_cloud300")
+    full = _renderer(scene, FullPerPixel(), cfg, "exact64").frame(cam)
+    np.testing.assert_allclose(full.color, d["color"], atol=TOL, rtol=0)
+    assert np.bincount(d["bin_tile"]).max() <= 300
+    for k in (300, 512):
+        wide = _renderer(scene, Window(k), cfg, "exact64").frame(cam)
+        np.testing.assert_array_equal(wide.color, full.color)
+        np.testing.assert_array_equal(wide.transmittance, full.transmittance)
+        np.testing.assert_array_equal(wide.depth, full.depth)
 
 
 def _grad_close(got, ref, name):
