@@ -163,6 +163,11 @@ typedef struct {
   double* depth64;          /* [H,W]   or NULL (with color64)               */
   double* rec_t64;          /* [H,W,record_cap] or NULL                     */
   double* rec_alpha64;      /* [H,W,record_cap] or NULL                     */
+  double* splat_color64;    /* [n,3] scratch or NULL (with color64, Gaussian
+                               input): the SH colour in float64
+                               (gaussian_math.py:415-419), blended instead of
+                               the float32 record colour.  A SplatBatch input
+                               blends its own float64 colour.               */
 } StpOutputs;
 
 /* stats dict of rasterizer.py:683-690 (+ projection stats

@@ -73,7 +73,7 @@ class StpOutputs(ctypes.Structure):
                 ("sort_error", ctypes.c_void_p), ("status", ctypes.c_void_p),
                 ("color64", ctypes.c_void_p), ("transmittance64", ctypes.c_void_p),
                 ("depth64", ctypes.c_void_p), ("rec_t64", ctypes.c_void_p),
-                ("rec_alpha64", ctypes.c_void_p)]
+                ("rec_alpha64", ctypes.c_void_p), ("splat_color64", ctypes.c_void_p)]
 
 
 class StpGrads(ctypes.Structure):

@@ -150,6 +150,7 @@ bool carve_frame(int64_t n, const StpCamera* cam, const StpConfig* cfg, void* ws
     f.tile1 = std::max(f.tile0, std::min(cfg->tile_end, L.n_tiles));
   }
   f.status = nullptr;
+  f.col64 = nullptr;
   f.state = b + L.state;
   f.counts = reinterpret_cast<uint32_t*>(b + L.counts);
   f.offsets = reinterpret_cast<uint32_t*>(b + L.offsets);
@@ -238,6 +239,15 @@ int render_one(const StpScene* sc, const StpSplatBatch* batch, const StpCamera* 
   if (o.state) f.state = o.state;
   if (batch) launch_ingest(f, *batch, s);
   else launch_preprocess(f, *sc, s);
+  if (o.color64) {
+    // float64 outputs: blend the float64 colour (a SplatBatch's own, or the
+    // SH colour re-evaluated in float64 for the kept Gaussians)
+    if (batch) f.col64 = batch->color;
+    else if (o.splat_color64) {
+      launch_shade64(f, *sc, o.splat_color64, s);
+      f.col64 = o.splat_color64;
+    }
+  }
   mark(2);
   launch_scan(f, s);
   mark(3);

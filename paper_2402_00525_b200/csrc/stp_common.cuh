@@ -438,6 +438,7 @@ struct Frame {
   int depth_bits;         // entry word = (tile << depth_bits | truncated depth key) << id_bits | id
   int id_bits;
   int64_t* status;        // StpOutputs.status (device) or NULL: written by K5
+  const double* col64;    // float64 splat colour [n,3] (XM_F64) or NULL
   DevCam cam;
   DevCfg cfg;
 };
@@ -445,6 +446,7 @@ struct Frame {
 int device_sm_count();  // SMs of the current device (cached per device)
 void launch_init(const Frame& f, cudaStream_t s);
 void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s);
+void launch_shade64(const Frame& f, const StpScene& sc, double* col64, cudaStream_t s);
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s);
 void launch_scan(const Frame& f, cudaStream_t s);
 void launch_duplicate(const Frame& f, cudaStream_t s);

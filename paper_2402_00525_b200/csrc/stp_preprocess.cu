@@ -959,6 +959,49 @@ void launch_preprocess(const Frame& f, const StpScene& sc, cudaStream_t s) {
   launch_rows_count(f, s);
 }
 
+// K1c (float64 outputs only): the SH colour of every kept Gaussian in
+// float64, sh_basis (gaussian_math.py:152-175) and the clipped einsum
+// (:415-419) as the reference evaluates them; blended by the XM_F64 K6
+// instead of the float32 record colour.
+__global__ void __launch_bounds__(256) k_shade64(StpScene sc, DevCam cam,
+                                                 const uint8_t* __restrict__ state,
+                                                 double* __restrict__ col) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= sc.n || state[i] != 0) return;
+  const double r0 = (double)sc.means[3 * i + 0] - cam.pos[0];
+  const double r1 = (double)sc.means[3 * i + 1] - cam.pos[1];
+  const double r2 = (double)sc.means[3 * i + 2] - cam.pos[2];
+  const double dist = sqrt(r0 * r0 + r1 * r1 + r2 * r2);
+  const double x = r0 / dist, y = r1 / dist, z = r2 / dist;
+  const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  const double b[16] = {c_SH_C0,
+                        -c_SH_C1 * y,
+                        c_SH_C1 * z,
+                        -c_SH_C1 * x,
+                        c_SH_C2[0] * xy,
+                        c_SH_C2[1] * yz,
+                        c_SH_C2[2] * (2.0 * zz - xx - yy),
+                        c_SH_C2[3] * xz,
+                        c_SH_C2[4] * (xx - yy),
+                        c_SH_C3[0] * y * (3.0 * xx - yy),
+                        c_SH_C3[1] * xy * z,
+                        c_SH_C3[2] * y * (4.0 * zz - xx - yy),
+                        c_SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy),
+                        c_SH_C3[4] * x * (4.0 * zz - xx - yy),
+                        c_SH_C3[5] * z * (xx - yy),
+                        c_SH_C3[6] * x * (xx - 3.0 * yy)};
+  const float* sh = sc.sh + i * sc.sh_coeffs * 3;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < sc.sh_coeffs; ++k)
+    for (int c = 0; c < 3; ++c) acc[c] += b[k] * (double)sh[3 * k + c];
+  for (int c = 0; c < 3; ++c) col[3 * i + c] = fmax(acc[c] + 0.5, 0.0);
+}
+
+void launch_shade64(const Frame& f, const StpScene& sc, double* col64, cudaStream_t s) {
+  if (f.n == 0) return;
+  k_shade64<<<(unsigned)((f.n + 255) / 256), 256, 0, s>>>(sc, f.cam, f.state, col64);
+}
+
 void launch_ingest(const Frame& f, const StpSplatBatch& b, cudaStream_t s) {
   if (f.n == 0) return;
   const int64_t blocks = (f.n + kPreThreads - 1) / kPreThreads;

@@ -129,6 +129,7 @@ struct RenderArgs {
   StpOutputs out;
   unsigned long long* counters;
   DevGrads grad;          // XM_FWD / XM_BWD
+  const double* col64;    // XM_F64: float64 splat colour [n,3] or NULL
 };
 
 // per-pixel state of the extra modes at the start of a pixel
@@ -192,7 +193,13 @@ __device__ __forceinline__ void xm_step(Pixel& P, const RenderArgs& A, double t,
     P.serr += fmax(P.tprev - t, 0.0);
     P.tprev = t;
   }
-  if (XM == XM_FWD || XM == XM_F64) {
+  if (XM == XM_F64 && A.col64) {
+    const double w = al * P.T;
+    const double* c = A.col64 + (size_t)id * 3;
+    P.f0 += c[0] * w;
+    P.f1 += c[1] * w;
+    P.f2 += c[2] * w;
+  } else if (XM == XM_FWD || XM == XM_F64) {
     const double w = al * P.T;
     P.f0 += (double)oc.y * w;
     P.f1 += (double)oc.z * w;
@@ -1231,6 +1238,7 @@ struct GzArgs {
   int gw, n_tiles;
   StpOutputs out;
   unsigned long long* counters;
+  const double* col64;
 };
 
 __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
@@ -1249,6 +1257,7 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
   R.out = A.out;
   R.counters = A.counters;
   R.grad = A.grad;
+  R.col64 = A.col64;
   const bool need_t = A.cfg.rec_cap > 0 || A.xm == XM_SERR ||
                       (A.xm == XM_F64 && A.out.sort_error != nullptr);
   for (int band = blockIdx.x; band < A.n_tiles; band += gridDim.x) {
@@ -1361,6 +1370,7 @@ static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStr
   A.n_tiles = f.tile1 - f.tile0;
   A.out = out;
   A.counters = f.counters;
+  A.col64 = f.col64;
   if (A.n_tiles > 0) k_render_globalz<<<A.n_tiles, kGzThreads, 0, s>>>(A);
 }
 
@@ -1697,6 +1707,7 @@ void launch_render(const Frame& f, int buf, const StpOutputs& out, cudaStream_t 
   A.n_items = f.tile1 - f.tile0;
   A.out = out;
   A.counters = f.counters;
+  A.col64 = f.col64;
   if (g) A.grad = *g;
   if (f.sort_mode == STP_MODE_FULL || f.sort_mode == STP_MODE_WINDOW) {
     launch_render_pixelsort(f, A, xm, s);

@@ -322,6 +322,8 @@ class Renderer:
         if f64:
             f = torch.float64
             o["color64"] = torch.empty((height, width, 3), dtype=f, device=d)
+            if not self.batch:
+                o["splat_color64"] = torch.empty((max(1, self.scene.n), 3), dtype=f, device=d)
             o["transmittance64"] = torch.empty((height, width), dtype=f, device=d)
             if self.cfg.with_depth:
                 o["depth64"] = torch.empty((height, width), dtype=f, device=d)
@@ -335,7 +337,7 @@ class Renderer:
         s = _lib.StpOutputs()
         for k in ("color", "transmittance", "depth", "rec_count", "rec_splat", "rec_t",
                   "rec_alpha", "state", "sort_error", "status", "color64", "transmittance64",
-                  "depth64", "rec_t64", "rec_alpha64"):
+                  "depth64", "rec_t64", "rec_alpha64", "splat_color64"):
             if k in o:
                 setattr(s, k, o[k].data_ptr())
         return s

@@ -66,7 +66,8 @@ def base(name):
 
 
 def to_us(v, u):
-    return v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+    return v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                "msecond": 1e3, "s": 1e6, "second": 1e6}.get(u, 1.0)
 
 
 def to_bytes(v, u):
@@ -75,7 +76,9 @@ def to_bytes(v, u):
 
 STALL = re.compile(r"smsp__average_warps_issue_stalled_(.+)_per_issue_active\.ratio$")
 stall_cols = [(m.group(1), h) for h in hdr for m in [STALL.match(h)] if m]
-fp64_cols = [h for h in hdr if "fp64" in h and "pct_of_peak_sustained_active" in h]
+fp64_cols = [h for h in ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+                         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+             if h in col]
 launches = collections.OrderedDict()
 for r in data:
     k = base(r[col["Kernel Name"]])
@@ -144,7 +147,7 @@ for g, names in GROUP:
     us = sum(p["us"] for p in parts)
     by = sum(p["dram_bytes"] for p in parts)
     main = max(parts, key=lambda p: p["us"])
-    fp = max(main["fp64_pct"].values()) if main["fp64_pct"] else None
+    fp = main["fp64_pct"].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
     summary["kernels"][g] = {
         "us_ncu": us, "dram_bytes_per_view": by, "dram_gbs_ncu": by / (us * 1e-6) / 1e9,
         "dram_frac_of_peak_ncu": by / (us * 1e-6) / 1e9 / PEAK,
