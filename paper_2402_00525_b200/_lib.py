@@ -114,12 +114,15 @@ def load(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     from . import build as _build
-    if build_if_missing and _build.needs_build():
+    # A/B experiments (scripts/ab.sh): an alternative in-tree build of the
+    # same sources with different compile-time knobs
+    path = os.environ.get("STP_LIB_VARIANT") or LIB_PATH
+    if path == LIB_PATH and build_if_missing and _build.needs_build():
         _build.build()
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"{LIB_PATH} is missing: run paper_2402_00525_b200/build.py "
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run paper_2402_00525_b200/build.py "
                            "(no CPU fallback exists)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     L.stp_abi_version.restype = ctypes.c_int
     L.stp_error_string.restype = ctypes.c_char_p
     L.stp_error_string.argtypes = [ctypes.c_int]

@@ -36,24 +36,34 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
+    """Build LIB (or ``out``: an A/B variant, e.g. variants/libstp_<tag>.so,
+    with extra -D knobs)."""
+    lib = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     extra = list(extra) + os.environ.get("STP_NVCC_EXTRA", "").split()
-    cmd = [nvcc(), *ARCH, *FLAGS, *[e for e in extra if e], *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    cmd = [nvcc(), *ARCH, *FLAGS, *[e for e in extra if e], *[os.path.join(CSRC, s) for s in SOURCES], "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(CSRC, "ptxas.log")
+    log = os.path.join(CSRC, "ptxas.log" if out is None else "ptxas_variant.log")
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libstp_b200.so")
-    os.replace(LIB + ".tmp", LIB)
-    os.utime(LIB, None)
+    os.replace(lib + ".tmp", lib)
+    os.utime(lib, None)
     if verbose:
         sys.stdout.write(r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # build.py [--force] | build.py --variant TAG -DKNOB=1 ...
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        tag, knobs = sys.argv[i + 1], sys.argv[i + 2:]
+        print(build(force=True, extra=knobs, out=os.path.join(HERE, "variants", f"libstp_{tag}.so")))
+    else:
+        build(force="--force" in sys.argv, verbose=True)

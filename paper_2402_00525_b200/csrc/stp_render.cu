@@ -1195,6 +1195,10 @@ size_t render_smem_bytes(int qt, int qm) {
   return kWarpsPerBlock * warp_smem_bytes(qt, qm) + STP_SMEM_PAD;
 }
 
+#ifndef STP_K6_BPS
+#define STP_K6_BPS 0  // cap on resident K6 blocks per SM (0: the occupancy maximum)
+#endif
+
 template <int QH, bool EXACT, int QMX, int QT = 0, int XM = XM_NONE>
 static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
   static size_t attr = 0;
@@ -1206,6 +1210,7 @@ static void launch_render_t(const RenderArgs& A, size_t smem, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_render<QH, EXACT, QMX, QT, XM>,
                                                   kRenderThreads, smem);
     n_sm = device_sm_count();
+    if (STP_K6_BPS > 0 && blocks_per_sm > STP_K6_BPS) blocks_per_sm = STP_K6_BPS;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int want = (A.n_items * 8 + kWarpsPerBlock - 1) / kWarpsPerBlock;

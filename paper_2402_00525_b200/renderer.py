@@ -234,7 +234,7 @@ class Workspace:
     def ensure(self, n: int, width: int, height: int, entries: int) -> None:
         need = int(_lib.load().stp_workspace_bytes(n, width, height, int(entries)))
         if self.buf.numel() < need:
-            self.buf = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self.buf = torch.zeros(need, dtype=torch.uint8, device=self.device)  # zeroed once: the sort look-back words are epoch-tagged, never cleared per frame
 
     @property
     def ptr(self) -> int:

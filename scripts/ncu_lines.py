@@ -1,9 +1,11 @@
 """Aggregate an ncu source page (cuda,sass view) by CUDA source line:
-stall samples and executed instructions.  usage: ncu_lines.py report.ncu-rep [top]"""
+stall samples and executed instructions.
+usage: ncu_lines.py report.ncu-rep [top] [kernel filter, e.g. regex:k_render]"""
 import csv, subprocess, sys, io
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+kfilt = ["-k", sys.argv[3]] if len(sys.argv) > 3 else []   # e.g. regex:k_render
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+                     + kfilt, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 data = []; f = "?"; hdr = None
 for r in rows:
