@@ -546,6 +546,21 @@ def run_ours(args):
                                           f"project + bin_and_sort + {mode_name(mode)} render "
                                           "of all tiles by the float64 C++ restatement "
                                           "(oracle/stp_oracle.cpp)"}
+        # the unmodified reference (baseline/_ref) itself, measured on this
+        # box's host by scripts/reference_cpu_point.py (SURVEY.md 8(d)
+        # protocol: projection and bin_and_sort in full, render_tile on a
+        # stratified tile sample, extrapolated by entries) -- too slow to
+        # re-run inside every bench (minutes per view)
+        refpt = _profile_json(f"reference_python_{args.config.upper()}.json")
+        if refpt and type(mode).__name__ == "Hierarchical":
+            line["cpu_baseline"]["reference_python"] = {
+                "value": refpt["views_per_s"], "unit": UNIT, "cores": refpt["workers"],
+                "kind": "reference", "s_per_view": refpt["s_per_view"],
+                "sample": f"view {refpt['view']}: project_scene + bin_and_sort in full, "
+                          f"hierarchy.render_tile on {refpt['tiles_sampled']} stratified tiles "
+                          f"({refpt['entries_sampled']} of {refpt['bin_entries']} entries), "
+                          "extrapolated by entries; 1 worker (GIL-bound pool)",
+                "source": f"profiles/reference_python_{args.config.upper()}.json"}
         pouts = r.alloc_outputs(W, H)
         r.render_into(cams[v0], pouts)
         torch.cuda.synchronize()

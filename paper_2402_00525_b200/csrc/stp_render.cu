@@ -557,7 +557,13 @@ struct SubQ {
 // shared-memory offset is an immediate (the default 64/8/4 configuration;
 // otherwise the compiler re-derives the offsets inside the hot loops).
 template <int QH, bool EXACT, int QMX, int QT, int XM>
-__global__ void __launch_bounds__(kRenderThreads, STP_EXACT_MINB) k_render(RenderArgs A) {
+#ifdef STP_K6_MAXNREG
+// experiments: a register cap instead of a min-blocks bound
+#define STP_K6_BOUNDS __maxnreg__(STP_K6_MAXNREG)
+#else
+#define STP_K6_BOUNDS __launch_bounds__(kRenderThreads, STP_EXACT_MINB)
+#endif
+__global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
   const int qt = QT ? QT : A.cfg.q_tail, qm = (QT && QMX) ? QMX : A.cfg.q_mid;
