@@ -4,7 +4,8 @@ the blend) and the render time relative to GlobalZ, on full C3 orbit views
 and C5 yaw-sweep views (1080p).  Modes: GlobalZ (the 3DGS order),
 Hierarchical 64/8/4, Window 4 / 8 / 16 / 24 and FullPerPixel (the exact
 per-pixel order, delta = 0).  Times are per-stage CUDA events (one view at a
-time, after a warm-up view).
+time, after a warm-up view) of the plain render (no sort-error map: the
+instrumented K6 computes t on every blend, which GlobalZ otherwise skips).
 usage: python scripts/sort_error_table.py [out.json]"""
 import json
 import os
@@ -25,10 +26,12 @@ for cfgname, views in (("C3", (0, 64, 128, 192)), ("C5", (0, 120))):
         r = Renderer(sc, mode, RenderConfig())
         cam0 = cams[views[0]]
         outs = r.alloc_outputs(cam0.width, cam0.height, sort_error=True)
-        r.render_into(cam0, outs, stats=True, timings=True)          # warm-up
+        plain = r.alloc_outputs(cam0.width, cam0.height)   # timing: the plain render
+        r.render_into(cam0, plain, stats=True, timings=True)         # warm-up
         for v in views:
-            st = r.render_into(cams[v], outs, stats=True, timings=True)
+            r.render_into(cams[v], outs, stats=True)                 # delta map (XM_SERR)
             pp = outs["sort_error"].double().cpu().numpy()
+            st = r.render_into(cams[v], plain, stats=True, timings=True)
             rows.append({"config": cfgname, "view": v, "mode": type(mode).__name__ +
                          (f"({mode.size})" if isinstance(mode, Window) else ""),
                          "delta_max": float(pp.max()), "delta_avg": float(pp.mean()),
@@ -38,7 +41,7 @@ for cfgname, views in (("C3", (0, 64, 128, 192)), ("C5", (0, 120))):
                          "ms_view": float(st.ms_project + st.ms_duplicate + st.ms_sort +
                                           st.ms_blend)})
             print(json.dumps(rows[-1]), flush=True)
-        del r, outs
+        del r, outs, plain
 summ = {}
 for r_ in rows:
     summ.setdefault((r_["config"], r_["mode"]), []).append(r_)
