@@ -1675,7 +1675,12 @@ static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
     launch_pixelsort_t<16, true, true>(A, xm, s);
     return;
   }
-  if (f.cfg.q_head > 16) {
+#ifndef STP_WINDOW_HEAP_MIN
+#define STP_WINDOW_HEAP_MIN 9  // Window(k >= this): the shared-memory heap kernel
+#endif
+  // measured (profiles/r2g/table1.json): the register window's 16-slot state
+  // (80 registers) makes Window(16) 2x slower than the heap kernel at 24
+  if (f.cfg.q_head >= STP_WINDOW_HEAP_MIN) {
     if (A.n_items <= 0) return;
     switch (xm) {
       case XM_SERR: launch_window_t<XM_SERR>(A, f.cfg.q_head, s); break;
@@ -1691,8 +1696,10 @@ static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
     case 2: launch_pixelsort_t<2, true, false>(A, xm, s); break;
     case 4: launch_pixelsort_t<4, true, false>(A, xm, s); break;
     case 8: launch_pixelsort_t<8, true, false>(A, xm, s); break;
-    case 16: launch_pixelsort_t<16, true, false>(A, xm, s); break;
-    default: launch_pixelsort_t<16, false, false>(A, xm, s); break;
+    default:
+      if (f.cfg.q_head <= 8) launch_pixelsort_t<8, false, false>(A, xm, s);
+      else launch_pixelsort_t<16, false, false>(A, xm, s);  // (STP_WINDOW_HEAP_MIN > 16 only)
+      break;
   }
 }
 
