@@ -1540,7 +1540,18 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
   return (size_t)cap * kWinPix * (sizeof(double) + sizeof(uint32_t));
 }
 
-template <int XM>
+// FullPerPixel (rasterizer.py:488-501) on the same kernel (FULL): the exact
+// per-pixel order by repeated top-K selection with a K-slot MAX-heap -- a
+// pass over the bin keeps the K smallest valid (t, rank) above the last
+// blended one, heap-sorts them ascending and blends them; the next pass
+// continues above the K-th.  A pixel is done when a pass keeps fewer than K
+// or it terminates.  With K = STP_FULL_HEAP (64) most pixels terminate
+// within the first pass (the register kernel's K = 16 needed ~4 passes).
+#ifndef STP_FULL_HEAP
+#define STP_FULL_HEAP 64
+#endif
+
+template <int XM, bool FULL>
 __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_tab[64];
@@ -1551,6 +1562,11 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
   uint32_t* hid = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(smem_raw) +
                                               (size_t)cap * kWinPix) + lane;
   const double term = A.cfg.term;
+  // heap order: "a belongs nearer the root than b" -- min-heap (Window) or
+  // max-heap (FULL's top-K selection)
+  auto before = [](double ad, uint32_t ai, double bd, uint32_t bi) {
+    return FULL ? lt(bd, bi, ad, ai) : lt(ad, ai, bd, bi);
+  };
   for (int item = blockIdx.x; item < A.n_items * 8; item += gridDim.x) {
     const int tile = item / 8 + A.tile0, strip = item % 8;
     const int tx = tile % A.gw, ty = tile / A.gw;
@@ -1578,13 +1594,13 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
         if (c + 1 < n) {
           const double rd = hd[(size_t)(c + 1) * kWinPix];
           const uint32_t ri = hid[(size_t)(c + 1) * kWinPix];
-          if (lt(rd, ri, cd, ci)) {
+          if (before(rd, ri, cd, ci)) {
             ++c;
             cd = rd;
             ci = ri;
           }
         }
-        if (!lt(cd, ci, xd, xi)) break;
+        if (!before(cd, ci, xd, xi)) break;
         hd[(size_t)p * kWinPix] = cd;
         hid[(size_t)p * kWinPix] = ci;
         p = c;
@@ -1592,51 +1608,86 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
       hd[(size_t)p * kWinPix] = xd;
       hid[(size_t)p * kWinPix] = xi;
     };
-    // blend the popped minimum (t0, i0): alpha re-evaluated
-    auto blend_min = [&](double t0, uint32_t i0) {
+    auto sift_up = [&](double xd, uint32_t xi, int c) {
+      while (c > 0) {
+        const int p = (c - 1) >> 1;
+        const double pd = hd[(size_t)p * kWinPix];
+        const uint32_t pi = hid[(size_t)p * kWinPix];
+        if (!before(xd, xi, pd, pi)) break;
+        hd[(size_t)c * kWinPix] = pd;
+        hid[(size_t)c * kWinPix] = pi;
+        c = p;
+      }
+      hd[(size_t)c * kWinPix] = xd;
+      hid[(size_t)c * kWinPix] = xi;
+    };
+    // blend (t0, i0): alpha re-evaluated (deterministic: the value at insertion)
+    auto blend_at = [&](double t0, uint32_t i0) {
       double t, al;
       emit_eval_bf(P, A, i0, s_tab, t, al);
       blend<XM>(P, A, t0, al, i0);
     };
     const uint2 rg = A.ranges[tile];
-    int n = 0;
-    for (uint32_t j = rg.x; j < rg.y; ++j) {
-      if (!__any_sync(kFull, P.T >= term)) break;
-      const uint32_t id = A.vals[j];
-      double t, al;
-      const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
-      if (!(pass && P.T >= term)) continue;
-      if (n < cap) {
-        // sift up
-        int c = n++;
-        while (c > 0) {
-          const int p = (c - 1) >> 1;
-          const double pd = hd[(size_t)p * kWinPix];
-          const uint32_t pi = hid[(size_t)p * kWinPix];
-          if (!lt(t, id, pd, pi)) break;
-          hd[(size_t)c * kWinPix] = pd;
-          hid[(size_t)c * kWinPix] = pi;
-          c = p;
+    if (!FULL) {
+      int n = 0;
+      for (uint32_t j = rg.x; j < rg.y; ++j) {
+        if (!__any_sync(kFull, P.T >= term)) break;
+        const uint32_t id = A.vals[j];
+        double t, al;
+        const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
+        if (!(pass && P.T >= term)) continue;
+        if (n < cap) {
+          sift_up(t, id, n++);
+        } else if (lt(t, id, hd[0], hid[0])) {
+          blend<XM>(P, A, t, al, id);  // the incoming entry is the smallest: emitted
+        } else {
+          // emit the minimum; the incoming entry takes its place
+          const double t0 = hd[0];
+          const uint32_t i0 = hid[0];
+          sift_down(t, id, n);
+          blend_at(t0, i0);
         }
-        hd[(size_t)c * kWinPix] = t;
-        hid[(size_t)c * kWinPix] = id;
-      } else if (lt(t, id, hd[0], hid[0])) {
-        blend<XM>(P, A, t, al, id);  // the incoming entry is the smallest: emitted
-      } else {
-        // emit the minimum; the incoming entry takes its place
+      }
+      // drain in ascending (t, rank) (rasterizer.py:565-573); no-ops once terminated
+      while (n > 0 && P.T >= term) {
         const double t0 = hd[0];
         const uint32_t i0 = hid[0];
-        sift_down(t, id, n);
-        blend_min(t0, i0);
+        --n;
+        sift_down(hd[(size_t)n * kWinPix], hid[(size_t)n * kWinPix], n);
+        blend_at(t0, i0);
       }
-    }
-    // drain in ascending (t, rank) (rasterizer.py:565-573); no-ops once terminated
-    while (n > 0 && P.T >= term) {
-      const double t0 = hd[0];
-      const uint32_t i0 = hid[0];
-      --n;
-      sift_down(hd[(size_t)n * kWinPix], hid[(size_t)n * kWinPix], n);
-      blend_min(t0, i0);
+    } else {
+      double lo_t = -INFINITY;
+      uint32_t lo_id = 0;
+      bool first = true, more = true;
+      while (__any_sync(kFull, more && P.T >= term)) {
+        if (!(more && P.T >= term)) continue;
+        int n = 0;
+        for (uint32_t j = rg.x; j < rg.y; ++j) {
+          const uint32_t id = A.vals[j];
+          double t, al;
+          if (!emit_eval_bf(P, A, id, s_tab, t, al)) continue;
+          if (!first && !lt(lo_t, lo_id, t, id)) continue;  // blended by an earlier pass
+          if (n < cap) sift_up(t, id, n++);
+          else if (lt(t, id, hd[0], hid[0])) sift_down(t, id, n);  // replaces the maximum
+        }
+        // heap-sort ascending in place, then blend in order
+        for (int m = n - 1; m > 0; --m) {
+          const double xd = hd[(size_t)m * kWinPix];
+          const uint32_t xi = hid[(size_t)m * kWinPix];
+          hd[(size_t)m * kWinPix] = hd[0];
+          hid[(size_t)m * kWinPix] = hid[0];
+          sift_down(xd, xi, m);
+        }
+        for (int i = 0; i < n && P.T >= term; ++i)
+          blend_at(hd[(size_t)i * kWinPix], hid[(size_t)i * kWinPix]);
+        if (n < cap) more = false;
+        else {
+          lo_t = hd[(size_t)(n - 1) * kWinPix];
+          lo_id = hid[(size_t)(n - 1) * kWinPix];
+        }
+        first = false;
+      }
     }
     xm_done<XM>(P, A);
     if (P.pix >= 0 && XM != XM_BWD) {
@@ -1656,39 +1707,50 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
   }
 }
 
-template <int XM>
+template <int XM, bool FULL>
 static void launch_window_t(const RenderArgs& A, int cap, cudaStream_t s) {
   const size_t smem = window_smem_bytes(cap);
-  cudaFuncSetAttribute(k_render_window<XM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_render_window<XM, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_window<XM>, kWinPix, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_window<XM, FULL>, kWinPix,
+                                                smem);
   const long long items = (long long)A.n_items * 8;
   const long long grid = std::min<long long>(items, (long long)device_sm_count() *
                                                         std::max(per_sm, 1));
-  k_render_window<XM><<<(int)grid, kWinPix, smem, s>>>(A, cap);
+  k_render_window<XM, FULL><<<(int)grid, kWinPix, smem, s>>>(A, cap);
+}
+
+template <bool FULL>
+static void launch_window_xm(const RenderArgs& A, int cap, int xm, cudaStream_t s) {
+  switch (xm) {
+    case XM_SERR: launch_window_t<XM_SERR, FULL>(A, cap, s); break;
+    case XM_FWD: launch_window_t<XM_FWD, FULL>(A, cap, s); break;
+    case XM_BWD: launch_window_t<XM_BWD, FULL>(A, cap, s); break;
+    case XM_F64: launch_window_t<XM_F64, FULL>(A, cap, s); break;
+    default: launch_window_t<XM_NONE, FULL>(A, cap, s); break;
+  }
 }
 
 static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
                                     cudaStream_t s) {
   if (f.sort_mode == STP_MODE_FULL) {
-    launch_pixelsort_t<16, true, true>(A, xm, s);
+    if (STP_FULL_HEAP > 0) {
+      if (A.n_items > 0) launch_window_xm<true>(A, STP_FULL_HEAP, xm, s);
+    } else {
+      launch_pixelsort_t<16, true, true>(A, xm, s);
+    }
     return;
   }
 #ifndef STP_WINDOW_HEAP_MIN
-#define STP_WINDOW_HEAP_MIN 9  // Window(k >= this): the shared-memory heap kernel
+#define STP_WINDOW_HEAP_MIN 1  // Window(k >= this): the shared-memory heap kernel
 #endif
-  // measured (profiles/r2g/table1.json): the register window's 16-slot state
-  // (80 registers) makes Window(16) 2x slower than the heap kernel at 24
+  // measured (profiles/r2h): the heap kernel beats the register window at
+  // every size (C3 K6: Window(3) 3.9 vs 5.4 ms, (8) 4.8 vs 5.4, (16) 5.6 vs
+  // 14.8 -- the register window's state costs occupancy)
   if (f.cfg.q_head >= STP_WINDOW_HEAP_MIN) {
     if (A.n_items <= 0) return;
-    switch (xm) {
-      case XM_SERR: launch_window_t<XM_SERR>(A, f.cfg.q_head, s); break;
-      case XM_FWD: launch_window_t<XM_FWD>(A, f.cfg.q_head, s); break;
-      case XM_BWD: launch_window_t<XM_BWD>(A, f.cfg.q_head, s); break;
-      case XM_F64: launch_window_t<XM_F64>(A, f.cfg.q_head, s); break;
-      default: launch_window_t<XM_NONE>(A, f.cfg.q_head, s); break;
-    }
+    launch_window_xm<false>(A, f.cfg.q_head, xm, s);
     return;
   }
   switch (f.cfg.q_head) {  // the window size

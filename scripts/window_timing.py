@@ -8,13 +8,13 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
-from paper_2402_00525_b200 import RenderConfig, Window, scenes  # noqa: E402
+from paper_2402_00525_b200 import FullPerPixel, RenderConfig, Window, scenes  # noqa: E402
 from paper_2402_00525_b200.renderer import Renderer  # noqa: E402
 
-ks = [int(a) for a in sys.argv[1:]] or [3, 4, 8, 12, 16, 24]
+ks = [int(a) for a in sys.argv[1:]] or [3, 4, 8, 12, 16, 24]   # 0 = FullPerPixel
 sc, cams = scenes.config_scene("C3")
 for k in ks:
-    r = Renderer(sc, Window(k), RenderConfig())
+    r = Renderer(sc, Window(k) if k else FullPerPixel(), RenderConfig())
     outs = r.alloc_outputs(cams[0].width, cams[0].height)
     r.render_into(cams[0], outs, stats=True, timings=True)
     ms = [r.render_into(cams[v], outs, stats=True, timings=True).ms_blend for v in (0, 64, 128)]
