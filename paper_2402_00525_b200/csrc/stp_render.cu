@@ -1545,10 +1545,10 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
 // pass over the bin keeps the K smallest valid (t, rank) above the last
 // blended one, heap-sorts them ascending and blends them; the next pass
 // continues above the K-th.  A pixel is done when a pass keeps fewer than K
-// or it terminates.  With K = STP_FULL_HEAP (64) most pixels terminate
-// within the first pass (the register kernel's K = 16 needed ~4 passes).
+// or it terminates.  C3 K6 (profiles/r2i): K = 16 in registers 112.9 ms,
+// heap K = 32 47.9 ms, 64 53.1 ms, 128 64.4 ms (fewer passes vs occupancy).
 #ifndef STP_FULL_HEAP
-#define STP_FULL_HEAP 64
+#define STP_FULL_HEAP 32
 #endif
 
 template <int XM, bool FULL>
