@@ -991,6 +991,16 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
             d = INFINITY;
             id = kNoId;
           }
+#ifdef STP_WORK_STATS
+          {  // sortedness of each half's candidates in bin order
+            const double pd = __shfl_up_sync(kFull, d, 1, 16);
+            const uint32_t pi = __shfl_up_sync(kFull, id, 1, 16);
+            const bool ok = L == 0 || L >= nk || lt(pd, pi, d, id);
+            const unsigned bo = __ballot_sync(kFull, ok);
+            STAT_ADD(12, L == 0 && nk > 1);
+            STAT_ADD(13, L == 0 && nk > 1 && ((bo >> (lane & 16)) & 0xffffu) == 0xffffu);
+          }
+#endif
 #if STP_RANK16
           // position of (d, id) among its half's candidates: 16 independent
           // shuffle + compare rounds instead of a 10-stage bitonic network
@@ -1048,6 +1058,21 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
             Q.bi()[xS1] = iS1;
           }
           __syncwarp();
+#ifdef STP_WORK_STATS
+          {  // merges that are appends (every batch element after the tail)
+            const int sl = lane & 1;
+            const int nks = sl ? nkB : nkA, nts = sl ? nt1 : nt0, ths = sl ? th1 : th0;
+            const SubQ Qs = subq(sl);
+            const bool both = nks > 0 && nts > 0;
+            bool app = false;
+            if (lane < 2 && both) {
+              const int cs = sl ? cur1 : cur0;
+              app = lt(Qs.td(cs)[ths + nts - 1], Qs.ti(cs)[ths + nts - 1], Qs.bd()[0], Qs.bi()[0]);
+            }
+            STAT_ADD(14, lane < 2 && both);
+            STAT_ADD(15, lane < 2 && app);
+          }
+#endif
           if (tail_inplace(qt)) {
             // qt == 64: tails hold <= 32 here, so every lane reads and ranks
             // at most one new element per sub-tile and two tail elements,
@@ -1546,9 +1571,10 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
 // blended one, heap-sorts them ascending and blends them; the next pass
 // continues above the K-th.  A pixel is done when a pass keeps fewer than K
 // or it terminates.  C3 K6 (profiles/r2i): K = 16 in registers 112.9 ms,
-// heap K = 32 47.9 ms, 64 53.1 ms, 128 64.4 ms (fewer passes vs occupancy).
+// heap K = 16 61.1 ms, 24 52.0, 32 47.9, 48 46.8, 64 53.1, 128 64.4 (fewer
+// passes vs occupancy).
 #ifndef STP_FULL_HEAP
-#define STP_FULL_HEAP 32
+#define STP_FULL_HEAP 48
 #endif
 
 template <int XM, bool FULL>
