@@ -1077,15 +1077,33 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
             // qt == 64: tails hold <= 32 here, so every lane reads and ranks
             // at most one new element per sub-tile and two tail elements,
             // then all lanes write (single buffer)
+            // Append fast path (65% of C3's merges, profiles/r2k): when the
+            // batch's first element sorts after the tail's last, every new
+            // element lands at nt + its batch index and the tail elements
+            // keep their order -- no rank searches, and no moves at all if
+            // the tail already starts at slot 0
+            bool app0 = true, app1 = true;
+            if (nkA && nt0) {
+              const SubQ Q = subq(0);
+              app0 = lt(Q.td(0)[th0 + nt0 - 1], Q.ti(0)[th0 + nt0 - 1], Q.bd()[0], Q.bi()[0]);
+            }
+            if (nkB && nt1) {
+              const SubQ Q = subq(1);
+              app1 = lt(Q.td(0)[th1 + nt1 - 1], Q.ti(0)[th1 + nt1 - 1], Q.bd()[0], Q.bi()[0]);
+            }
             int rk1 = 0, rk2 = 0;
             if (v1)
-              rk1 = count_below(Q1.td(0) + (s1 ? th1 : th0), Q1.ti(0) + (s1 ? th1 : th0),
-                                s1 ? nt1 : nt0, d1, i1);
+              rk1 = (s1 ? app1 : app0)
+                        ? (s1 ? nt1 : nt0)
+                        : count_below(Q1.td(0) + (s1 ? th1 : th0), Q1.ti(0) + (s1 ? th1 : th0),
+                                      s1 ? nt1 : nt0, d1, i1);
             if (!cpt && vS1) {
               const SubQ Q = subq(1);
-              rk2 = count_below(Q.td(0) + th1, Q.ti(0) + th1, nt1, dS1, iS1);
+              rk2 = app1 ? nt1 : count_below(Q.td(0) + th1, Q.ti(0) + th1, nt1, dS1, iS1);
             }
-            const int n0 = nkA ? nt0 : 0, n1 = nkB ? nt1 : 0;
+            // tail elements to (re)place: none for an append onto a tail at slot 0
+            const int n0 = (nkA && !(app0 && th0 == 0)) ? nt0 : 0;
+            const int n1 = (nkB && !(app1 && th1 == 0)) ? nt1 : 0;
             double tv[2];
             uint32_t tiv[2];
             int trk[2], tpos[2], tst[2];
@@ -1101,7 +1119,9 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
                 const int th = st ? th1 : th0;
                 tv[k] = Q.td(0)[th + t];
                 tiv[k] = Q.ti(0)[th + t];
-                trk[k] = count_below(Q.bd(), Q.bi(), st ? nkB : nkA, tv[k], tiv[k]);
+                trk[k] = (st ? app1 : app0) ? 0
+                                            : count_below(Q.bd(), Q.bi(), st ? nkB : nkA, tv[k],
+                                                          tiv[k]);
                 tpos[k] = t;
               }
             }
@@ -1413,142 +1433,10 @@ static void launch_render_globalz(const Frame& f, const StpOutputs& out, cudaStr
 // ---------------------------------------------------------------------------
 // K6 under Window(size) (rasterizer.py:504-588) and FullPerPixel (:488-501).
 // The bins are the hierarchical ones (per-tile t_opt keys, exact culling).
-// One thread per pixel, warps independent (a warp stops when its 32 pixels
-// have terminated); every entry is evaluated exactly as the hierarchical
-// pixel stage does (alpha, eps test, cap, pixel-ray t_opt).
-//  Window: the valid entries of the bin stream through a per-pixel sorted
-//   window of `size` in registers; on overflow the smaller by (t, rank) of the
-//   incoming entry and the window minimum is blended -- head_push -- and the
-//   window drains in order at the end of the bin.
-//  FullPerPixel: the exact per-pixel order by repeated top-QH selection: a
-//   pass over the bin keeps the QH smallest (t, rank) above the last blended
-//   one in a sorted register buffer, blends them in order, and the next pass
-//   continues above the last; a pixel is done when a pass selects fewer than
-//   QH or it terminates.  Exact for any bin length, QH registers per pixel.
-template <int QH>
-__device__ __forceinline__ void topk_push(Head<QH>& H, double t, double al, uint32_t id) {
-  // bubble (t, id) into the sorted buffer; when full the largest falls off
-  double xt = t, xa = al;
-  uint32_t xi = id;
-#pragma unroll
-  for (int i = 0; i < QH; ++i) {
-    const bool sw = lt(xt, xi, H.t[i], H.id[i]);
-    const double ht = H.t[i], ha = H.a[i];
-    const uint32_t hi = H.id[i];
-    H.t[i] = sw ? xt : ht;
-    H.a[i] = sw ? xa : ha;
-    H.id[i] = sw ? xi : hi;
-    xt = sw ? ht : xt;
-    xa = sw ? ha : xa;
-    xi = sw ? hi : xi;
-  }
-  H.n = min(H.n + 1, QH);
-}
-
-template <int QH, bool EXACT, bool FULL, int XM>
-__global__ void __launch_bounds__(256) k_render_pixelsort(RenderArgs A) {
-  __shared__ double s_tab[64];
-  if (threadIdx.x < 64) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];
-  __syncthreads();
-  const int qh_rt = A.cfg.q_head;  // Window: the window size
-  const double term = A.cfg.term;
-  const int lane = threadIdx.x & 31;
-  for (int band = blockIdx.x; band < A.n_items; band += gridDim.x) {
-    const int tile = band + A.tile0;
-    const int tx = tile % A.gw, ty = tile / A.gw;
-    Pixel P;
-    {
-      const int gx = tx * kTile + (threadIdx.x & 15), gy = ty * kTile + (threadIdx.x >> 4);
-      const bool in_img = gx < A.cam.W && gy < A.cam.H;
-      P.pix = in_img ? (int64_t)gy * A.cam.W + gx : -1;
-      P.px = (double)gx + 0.5;
-      P.py = (double)gy + 0.5;
-      cam_ray(A.cam, P.px, P.py, P.u, P.w, P.vn);
-      P.T = in_img ? 1.0 : 0.0;
-      P.C0 = P.C1 = P.C2 = P.D = 0.f;
-      P.rc = 0;
-      xm_init<XM>(P, A);
-    }
-    Head<QH> H;
-    const uint2 rg = A.ranges[tile];
-    auto reset = [&]() {
-      H.n = 0;
-#pragma unroll
-      for (int i = 0; i < QH; ++i) {
-        H.t[i] = INFINITY;
-        H.a[i] = 0.0;
-        H.id[i] = kNoId;
-      }
-    };
-    reset();
-    if (!FULL) {
-      for (uint32_t j = rg.x; j < rg.y; ++j) {
-        if (!__any_sync(kFull, P.T >= term)) break;
-        const uint32_t id = A.vals[j];
-        double t, al;
-        const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
-        if (pass && P.T >= term) head_push<QH, EXACT, XM>(P, H, A, qh_rt, t, al, id);
-      }
-#pragma unroll
-      for (int i = 0; i < QH; ++i)
-        if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
-    } else {
-      double lo_t = -INFINITY;
-      uint32_t lo_id = 0;
-      bool first = true, more = true;
-      while (__any_sync(kFull, more && P.T >= term)) {
-        reset();
-        if (more && P.T >= term) {
-          for (uint32_t j = rg.x; j < rg.y; ++j) {
-            const uint32_t id = A.vals[j];
-            double t, al;
-            const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
-            // entries already blended: (t, rank) <= the last one
-            if (pass && (first || lt(lo_t, lo_id, t, id))) topk_push<QH>(H, t, al, id);
-          }
-#pragma unroll
-          for (int i = 0; i < QH; ++i)
-            if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
-          if (H.n < QH) more = false;
-          lo_t = H.t[QH - 1];
-          lo_id = H.id[QH - 1];
-          first = false;
-        }
-      }
-    }
-    (void)lane;
-    xm_done<XM>(P, A);
-    if (P.pix >= 0 && XM != XM_BWD) {
-      const float T = (float)P.T;
-      const float c0 = P.C0 + (float)(P.T * A.cfg.bg[0]);
-      const float c1 = P.C1 + (float)(P.T * A.cfg.bg[1]);
-      const float c2 = P.C2 + (float)(P.T * A.cfg.bg[2]);
-      A.out.color[P.pix * 3 + 0] = c0;
-      A.out.color[P.pix * 3 + 1] = c1;
-      A.out.color[P.pix * 3 + 2] = c2;
-      A.out.transmittance[P.pix] = T;
-      if (A.out.depth) A.out.depth[P.pix] = P.D;
-      if (A.cfg.rec_cap > 0) A.out.rec_count[P.pix] = P.rc;
-      if (!(isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(T)))
-        atomicAdd(A.counters + C_NONFINITE, 1ull);
-    }
-  }
-}
-
-template <int QH, bool EXACT, bool FULL>
-static void launch_pixelsort_t(const RenderArgs& A, int xm, cudaStream_t s) {
-  if (A.n_items <= 0) return;
-  switch (xm) {
-    case XM_SERR: k_render_pixelsort<QH, EXACT, FULL, XM_SERR><<<A.n_items, 256, 0, s>>>(A); break;
-    case XM_FWD: k_render_pixelsort<QH, EXACT, FULL, XM_FWD><<<A.n_items, 256, 0, s>>>(A); break;
-    case XM_BWD: k_render_pixelsort<QH, EXACT, FULL, XM_BWD><<<A.n_items, 256, 0, s>>>(A); break;
-    case XM_F64: k_render_pixelsort<QH, EXACT, FULL, XM_F64><<<A.n_items, 256, 0, s>>>(A); break;
-    default: k_render_pixelsort<QH, EXACT, FULL, XM_NONE><<<A.n_items, 256, 0, s>>>(A); break;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K6 under Window(size > 16) (rasterizer.py:504-588): the window is a
+// One warp per block = 32 pixels (a 16 x 2 strip of a tile, 8 warps per
+// tile, warps independent: a warp stops when its pixels have terminated);
+// every entry is evaluated exactly as the hierarchical pixel stage does
+// (alpha, eps test, cap, pixel-ray t_opt).  Window: the window is a
 // per-pixel binary min-heap of (t, rank) in shared memory, laid out
 // [slot][lane] so every heap access of a warp is bank-conflict free.  The
 // reference's window is a set with "emit the smaller of (incoming, window
@@ -1556,8 +1444,10 @@ static void launch_pixelsort_t(const RenderArgs& A, int xm, cudaStream_t s) {
 // min-heap (ranks are unique, so the order is total).  A slot stores (t,
 // rank) only; alpha of a popped entry is re-evaluated (emit_eval_bf is
 // deterministic: the same t and alpha as at insertion), which keeps 12 B per
-// slot: up to kWindowMax entries per pixel for a 32-pixel warp (one warp per
-// block: 16 x 2 pixels, 8 warps per tile).
+// slot: up to kWindowMax entries per pixel.  (Round 1 kept windows up to 16
+// in registers, one thread per pixel in 256-thread tile blocks: measured
+// slower at every size, C3 K6 Window(3) 5.4 vs 3.9 ms, (8) 5.4 vs 4.8,
+// (16) 14.8 vs 5.6 -- profiles/r2i -- and removed.)
 constexpr int kWindowMax = STP_WINDOW_MAX;
 constexpr int kWinPix = 32;
 
@@ -1574,7 +1464,7 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
 // heap K = 16 61.1 ms, 24 52.0, 32 47.9, 48 46.8, 64 53.1, 128 64.4 (fewer
 // passes vs occupancy).
 #ifndef STP_FULL_HEAP
-#define STP_FULL_HEAP 48
+#define STP_FULL_HEAP 48  // K (round 1: K = 16 selection in registers, 112.9 ms)
 #endif
 
 template <int XM, bool FULL>
@@ -1760,35 +1650,9 @@ static void launch_window_xm(const RenderArgs& A, int cap, int xm, cudaStream_t 
 
 static void launch_render_pixelsort(const Frame& f, const RenderArgs& A, int xm,
                                     cudaStream_t s) {
-  if (f.sort_mode == STP_MODE_FULL) {
-    if (STP_FULL_HEAP > 0) {
-      if (A.n_items > 0) launch_window_xm<true>(A, STP_FULL_HEAP, xm, s);
-    } else {
-      launch_pixelsort_t<16, true, true>(A, xm, s);
-    }
-    return;
-  }
-#ifndef STP_WINDOW_HEAP_MIN
-#define STP_WINDOW_HEAP_MIN 1  // Window(k >= this): the shared-memory heap kernel
-#endif
-  // measured (profiles/r2h): the heap kernel beats the register window at
-  // every size (C3 K6: Window(3) 3.9 vs 5.4 ms, (8) 4.8 vs 5.4, (16) 5.6 vs
-  // 14.8 -- the register window's state costs occupancy)
-  if (f.cfg.q_head >= STP_WINDOW_HEAP_MIN) {
-    if (A.n_items <= 0) return;
-    launch_window_xm<false>(A, f.cfg.q_head, xm, s);
-    return;
-  }
-  switch (f.cfg.q_head) {  // the window size
-    case 1: launch_pixelsort_t<1, true, false>(A, xm, s); break;
-    case 2: launch_pixelsort_t<2, true, false>(A, xm, s); break;
-    case 4: launch_pixelsort_t<4, true, false>(A, xm, s); break;
-    case 8: launch_pixelsort_t<8, true, false>(A, xm, s); break;
-    default:
-      if (f.cfg.q_head <= 8) launch_pixelsort_t<8, false, false>(A, xm, s);
-      else launch_pixelsort_t<16, false, false>(A, xm, s);  // (STP_WINDOW_HEAP_MIN > 16 only)
-      break;
-  }
+  if (A.n_items <= 0) return;
+  if (f.sort_mode == STP_MODE_FULL) launch_window_xm<true>(A, STP_FULL_HEAP, xm, s);
+  else launch_window_xm<false>(A, f.cfg.q_head, xm, s);
 }
 
 // K6 dispatch.  xm: XM_NONE (render), or with `g` the backward replays

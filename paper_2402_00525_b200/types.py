@@ -111,14 +111,14 @@ class GlobalZ:
 @dataclass(frozen=True)
 class FullPerPixel:
     """The exact per-pixel order (rasterizer.py:53-55); K6 =
-    k_render_pixelsort (repeated top-16 selection)."""
+    k_render_window (repeated top-48 selection with a shared-memory heap)."""
 
 
 @dataclass(frozen=True)
 class Window:
     """Per-pixel resorting window over the per-tile key stream
-    (rasterizer.py:58-67); K6 = k_render_pixelsort (register window) or
-    k_render_window (shared-memory heap, larger windows)."""
+    (rasterizer.py:58-67); K6 = k_render_window (a per-pixel shared-memory
+    min-heap, sizes up to 512)."""
 
     size: int = 8
 
