@@ -245,7 +245,7 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
   }
   __syncwarp();
   const int wbase = threadIdx.x & ~31;
-#ifdef STP_WORK_STATS
+#ifdef STP_WORK_STATS_K1  // K1 pair counts (slots 10/11 are K6's mid stats otherwise)
   {
     const unsigned tot = __reduce_add_sync(kFull, (unsigned)full);
     const unsigned big = __reduce_add_sync(kFull, full > 64 ? (unsigned)full : 0u);

@@ -750,6 +750,8 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         const int ng = min(4, c - 4 * gg);
         const double* g_d = gdp + 4 * gg;
         const uint32_t* g_i = gip + 4 * gg;
+        STAT_ADD(10, (lane & 7) == 0);                                        // mid merges
+        STAT_ADD(11, (lane & 7) == 0 && QMX == 8 && qm == 8 && nm == 4 && ng == 4);  // steady
         if (QMX == 8 && qm == 8 && nm == 4 && ng == 4) {
           // steady state: mid holds 4, a full group of 4 arrives, the merged 8
           // emit their first 4 and keep the last 4.  Lane slot sl owns one

@@ -19,7 +19,7 @@ names = ["load(+cull+d4)", "sort+merge", "push_mid", "pixel", "item_epilogue", "
 tot = prof.sum()
 stat = c[48:64].astype(np.int64)
 snames = ["load_evals(entry,subtile)", "kept_4x4", "batches", "batches_nonempty",
-          "pixel_slots(lane,entry)", "pixel_evals(T>=term)", "alpha_pass", "evals_in_all_fail_quads", "pixel_warp_steps", "consume_calls", "K1_coarse_pairs", "K1_pairs_in_rects_gt64",
+          "pixel_slots(lane,entry)", "pixel_evals(T>=term)", "alpha_pass", "evals_in_all_fail_quads", "pixel_warp_steps", "consume_calls", "mid_merges", "mid_merges_steady",
           "compact_halves_nk_gt1", "compact_halves_sorted", "tail_merges", "tail_merges_append"]
 print(json.dumps({"K6_ms": st.ms_blend, "entries": int(st.bin_entries),
                   "stats": {n: int(v) for n, v in zip(snames, stat)},
