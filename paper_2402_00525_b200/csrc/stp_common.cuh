@@ -85,9 +85,9 @@ enum Counter {
   C_PROF = 32,      // 8 phase-profile accumulators (STP_PHASE_PROF builds)
   C_TILE = 40,      // render: global tile counter
   C_SCHED = 41,     // render: per-SM tile ring overrun / spin bound hit (must stay 0)
-  C_STAT = 48,      // 8 work counters (STP_PHASE_PROF builds)
-  C_SM = 64,        // render: per-SM sub-tile counters [256]
-  C_SMT = 320,      // render: per-SM tile ring [256][kSmRing] (tag<<32 | tile+2)
+  C_STAT = 48,      // 32 work counters (STP_WORK_STATS builds)
+  C_SM = 80,        // render: per-SM sub-tile counters [256]
+  C_SMT = 336,      // render: per-SM tile ring [256][kSmRing] (tag<<32 | tile+2)
   C_PSTAT = C_SMT + 256 * 64,  // K1: per-SM projection stats [256][4] (behind, guard, degenerate, kept)
   C_COUNT = C_PSTAT + 256 * 4
 };

@@ -70,8 +70,17 @@ constexpr unsigned kNoId = 0xffffffffu;
     const unsigned _b = __ballot_sync(kFull, (pred));                               \
     if (lane == 0 && _b) atomicAdd(A.counters + C_STAT + (slot), (unsigned long long)__popc(_b)); \
   } while (0)
+// the same inside divergent code (ballot over the active lanes)
+#define STAT_ADD_DIV(slot, pred)                                                    \
+  do {                                                                              \
+    const unsigned _m = __activemask();                                             \
+    const unsigned _b = __ballot_sync(_m, (pred));                                  \
+    if (lane == __ffs(_m) - 1 && _b)                                                \
+      atomicAdd(A.counters + C_STAT + (slot), (unsigned long long)__popc(_b));      \
+  } while (0)
 #else
 #define STAT_ADD(slot, pred) (void)0
+#define STAT_ADD_DIV(slot, pred) (void)0
 #endif
 
 // (d, rank) order.  Non-short-circuit: the three comparisons issue in
@@ -876,8 +885,22 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
 #endif
               }
 #pragma unroll
-              for (int k = 0; k < STP_PIX_UNROLL; ++k)
+              for (int k = 0; k < STP_PIX_UNROLL; ++k) {
+#ifdef STP_WORK_STATS
+                {  // head pushes onto a full queue; those sorting after every queued entry
+                  const bool doit = ps[k] && P.T >= term, fullq = H.n >= QH;
+                  const bool aft = !lt(ts[k], ids[k], H.t[QH - 1], H.id[QH - 1]);
+                  STAT_ADD_DIV(16, doit && fullq);
+                  STAT_ADD_DIV(17, doit && fullq && aft);
+                  const unsigned m_ = __activemask();
+                  const unsigned bd_ = __ballot_sync(m_, doit && fullq);
+                  const unsigned bn_ = __ballot_sync(m_, doit && fullq && !aft);
+                  STAT_ADD_DIV(18, lane == __ffs(m_) - 1 && bd_ != 0);
+                  STAT_ADD_DIV(19, lane == __ffs(m_) - 1 && bd_ != 0 && bn_ == 0);
+                }
+#endif
                 if (ps[k] && P.T >= term) head_push<QH, EXACT, XM>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
+              }
             }
 #ifdef STP_WORK_STATS
             STAT_ADD(8, lane == 0);

@@ -13,14 +13,16 @@ outs = r.alloc_outputs(cam.width, cam.height)
 for _ in range(2):
     st = r.render_into(cam, outs, stats=True, timings=True)
 L = r.ws.layout(r.scene.n, cam.width, cam.height)
-c = r.ws.buf[L.counters: L.counters + 64 * 8].view(torch.int64).cpu().numpy()
+c = r.ws.buf[L.counters: L.counters + 80 * 8].view(torch.int64).cpu().numpy()
 prof = c[32:38].astype(np.float64)
 names = ["load(+cull+d4)", "sort+merge", "push_mid", "pixel", "item_epilogue", "item_prologue"]
 tot = prof.sum()
-stat = c[48:64].astype(np.int64)
+stat = c[48:80].astype(np.int64)
 snames = ["load_evals(entry,subtile)", "kept_4x4", "batches", "batches_nonempty",
           "pixel_slots(lane,entry)", "pixel_evals(T>=term)", "alpha_pass", "evals_in_all_fail_quads", "pixel_warp_steps", "consume_calls", "mid_merges", "mid_merges_steady",
-          "compact_halves_nk_gt1", "compact_halves_sorted", "tail_merges", "tail_merges_append"]
+          "compact_halves_nk_gt1", "compact_halves_sorted", "tail_merges", "tail_merges_append",
+          "head_push_full(lanes)", "head_push_full_after_all(lanes)", "head_push_full(warp_steps)",
+          "head_push_full_all_after(warp_steps)"]
 print(json.dumps({"K6_ms": st.ms_blend, "entries": int(st.bin_entries),
                   "stats": {n: int(v) for n, v in zip(snames, stat)},
                   "phase_frac": {n: round(float(v / tot), 4) for n, v in zip(names, prof)},
