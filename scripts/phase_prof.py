@@ -22,7 +22,8 @@ snames = ["load_evals(entry,subtile)", "kept_4x4", "batches", "batches_nonempty"
           "pixel_slots(lane,entry)", "pixel_evals(T>=term)", "alpha_pass", "evals_in_all_fail_quads", "pixel_warp_steps", "consume_calls", "mid_merges", "mid_merges_steady",
           "compact_halves_nk_gt1", "compact_halves_sorted", "tail_merges", "tail_merges_append",
           "head_push_full(lanes)", "head_push_full_after_all(lanes)", "head_push_full(warp_steps)",
-          "head_push_full_all_after(warp_steps)"]
+          "head_push_full_all_after(warp_steps)", "mid_steady_append(quad_merges)",
+          "mid_steady_all_quads_append(warp_merges)"]
 print(json.dumps({"K6_ms": st.ms_blend, "entries": int(st.bin_entries),
                   "stats": {n: int(v) for n, v in zip(snames, stat)},
                   "phase_frac": {n: round(float(v / tot), 4) for n, v in zip(names, prof)},
