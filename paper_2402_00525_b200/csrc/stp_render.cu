@@ -774,8 +774,9 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
 #ifdef STP_WORK_STATS
           {  // merges that are appends (the group sorts after the mid queue)
             const bool app = lt(md[3], mi[3], g_d[0], g_i[0]);
+            const bool all_app = __all_sync(kFull, app);
             STAT_ADD(20, slot0 == 0 && app);
-            STAT_ADD(21, lane == 0 && __all_sync(kFull, app));
+            STAT_ADD(21, lane == 0 && all_app);
           }
 #endif
           int rk = ix;
