@@ -52,6 +52,13 @@ __device__ __forceinline__ void ld256(const void* p, double& a, double& b, doubl
       : "l"(p));
 }
 
+// 256-bit store (sm_100: STG.E.256), 32-B aligned
+__device__ __forceinline__ void st256(void* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
 struct DevCam {
   double R[9];
   double pos[3];

@@ -27,6 +27,9 @@ constexpr unsigned long long kRowsListed = ~0ull;
 #ifndef STP_SPLIT_SH
 #define STP_SPLIT_SH 0
 #endif
+#ifndef STP_K1_V2
+#define STP_K1_V2 1  // register-lean projection + streaming record stores
+#endif
 
 __constant__ double c_SH_C0 = 0.28209479177387814;
 __constant__ double c_SH_C1 = 0.4886025119029199;
@@ -103,10 +106,14 @@ __device__ __forceinline__ void sh_color(const float* __restrict__ sh, int K, fl
       }
     }
   } else {
-    for (int k = 0; k < K; ++k) {
-      acc[0] = fmaf(b[k], __ldg(sh + 3 * k + 0), acc[0]);
-      acc[1] = fmaf(b[k], __ldg(sh + 3 * k + 1), acc[1]);
-      acc[2] = fmaf(b[k], __ldg(sh + 3 * k + 2), acc[2]);
+    // compile-time indices (a runtime-indexed b[] would live in local memory)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      if (k < K) {
+        acc[0] = fmaf(b[k], __ldg(sh + 3 * k + 0), acc[0]);
+        acc[1] = fmaf(b[k], __ldg(sh + 3 * k + 1), acc[1]);
+        acc[2] = fmaf(b[k], __ldg(sh + 3 * k + 2), acc[2]);
+      }
     }
   }
   // np.clip(basis @ sh + 0.5, 0, None): lower clamp only
@@ -359,6 +366,129 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           if (sc.sh_coeffs > 5) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + 128));
         }
 #endif
+#if STP_K1_V2
+        // Register-lean form of the same algebra (round 2): with V = W R
+        // (3 x 3), cov2 = J W R S^2 R^T W^T J^T = (J V) S^2 (J V)^T and the
+        // camera-space inverse covariance M' = W inv3 W^T = V S^-2 V^T
+        // (clamped 1/s), so neither cov3 nor inv3 is materialised and every
+        // symmetric matrix keeps 3 or 6 values.  The record is written in
+        // four 256-bit stores as soon as each part is known, instead of one
+        // 160-B struct store that kept all 20 fields live to the end (K1 had
+        // spilled 176 B per thread).  Same real numbers as the reference's
+        // (gaussian_math.py:361-413), different rounding order (~1e-16).
+        double V[9];
+        {
+          // _quats_to_matrices (gaussian_math.py:102-115)
+          const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
+          const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;
+          const double qn = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+          const double w = fdiv(qw0, qn), x = fdiv(qx0, qn), y = fdiv(qy0, qn),
+                       zq = fdiv(qz0, qn);
+          const double rot[9] = {1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq),
+                                 2 * (x * zq + w * y),      2 * (x * y + w * zq),
+                                 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x),
+                                 2 * (x * zq - w * y),      2 * (y * zq + w * x),
+                                 1 - 2 * (x * x + y * y)};
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+              V[aa * 3 + bb] = W[aa * 3 + 0] * rot[0 * 3 + bb] + W[aa * 3 + 1] * rot[1 * 3 + bb] +
+                               W[aa * 3 + 2] * rot[2 * 3 + bb];
+        }
+        const double s0 = __ldg(sc.scales + 3 * i + 0);
+        const double s1 = __ldg(sc.scales + 3 * i + 1);
+        const double s2 = __ldg(sc.scales + 3 * i + 2);
+        // J (gaussian_math.py:378-383): rows (J00, 0, J02), (0, J11, J12)
+        const double zz = z * z;
+        const double J00 = fdiv(cam.fx, z), J02 = -fdiv(cam.fx * pv0, zz);
+        const double J11 = fdiv(cam.fy, z), J12 = -fdiv(cam.fy * pv1, zz);
+        double a = cfg.dilation, b = 0.0, c = cfg.dilation;  // :385-387
+        {
+          const double ss[3] = {s0 * s0, s1 * s1, s2 * s2};
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb) {
+            const double B0 = J00 * V[0 * 3 + bb] + J02 * V[2 * 3 + bb];
+            const double B1 = J11 * V[1 * 3 + bb] + J12 * V[2 * 3 + bb];
+            a += ss[bb] * B0 * B0;
+            b += ss[bb] * B0 * B1;
+            c += ss[bb] * B1 * B1;
+          }
+        }
+        const double det = a * c - b * b;
+        if (!(det > 0.0)) {
+          reason = 3;  // :388-390
+        } else {
+          reason = 0;
+          SplatRec* rp = recs + i;
+          const double ca = fdiv(c, det), cb = -fdiv(b, det), cc = fdiv(a, det);  // conic (:397)
+          st256(&rp->mx, px, py, ca, cb);
+          const double inv_a = fdiv(1.0, ca), inv_c = fdiv(1.0, cc);
+          // opacity-aware radius (:399-404)
+          const float opf = __ldg(sc.opacity + i);
+          const double op = opf;
+          const double mid = 0.5 * (a + c);
+          const double lam_max = mid + sqrt(fmax(mid * mid - a * c + b * b, 0.0));
+          const double lg = log(op / cfg.eps);
+          const double cutoff = (op > cfg.eps) ? sqrt(2.0 * lg) : 0.0;
+          const double radius = cutoff * sqrt(lam_max);
+          const double thr = (op > 0.0) ? lg : -INFINITY;
+          int x0, x1, y0, y1;
+          coarse_rect(px, py, radius, gw, gh, x0, x1, y0, y1);
+          {
+            const unsigned lo = ((unsigned)(uint16_t)(int16_t)x0) | ((unsigned)(uint16_t)(int16_t)x1 << 16);
+            const unsigned hi = ((unsigned)(uint16_t)(int16_t)y0) | ((unsigned)(uint16_t)(int16_t)y1 << 16);
+            st256(&rp->inv_a, inv_a, inv_c, thr, __hiloint2double((int)hi, (int)lo));
+          }
+          // M' = V diag(min(1/s, clamp)^2) V^T (:406-412) and q' = M' p_view (:413)
+          {
+            double is[3];
+            is[0] = fmin(fdiv(1.0, s0), cfg.clamp);
+            is[1] = fmin(fdiv(1.0, s1), cfg.clamp);
+            is[2] = fmin(fdiv(1.0, s2), cfg.clamp);
+            double m00 = 0.0, m11 = 0.0, m22 = 0.0, m01 = 0.0, m02 = 0.0, m12 = 0.0;
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) {
+              const double w2 = is[bb] * is[bb];
+              const double v0 = V[0 * 3 + bb], v1 = V[1 * 3 + bb], v2 = V[2 * 3 + bb];
+              m00 += w2 * v0 * v0;
+              m11 += w2 * v1 * v1;
+              m22 += w2 * v2 * v2;
+              m01 += w2 * v0 * v1;
+              m02 += w2 * v0 * v2;
+              m12 += w2 * v1 * v2;
+            }
+            const double q0 = m00 * pv0 + m01 * pv1 + m02 * z;
+            const double q1 = m01 * pv0 + m11 * pv1 + m12 * z;
+            const double q2 = m02 * pv0 + m12 * pv1 + m22 * z;
+            st256(&rp->cc, cc, q2, m00, m11);
+            st256(&rp->m[2], m22, 2.0 * m01, 2.0 * m02, 2.0 * m12);
+            // SH colour along (mean - origin) / |mean - origin| (:415-419)
+            const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
+            float col[3];
+            sh_color(sc.sh + (int64_t)i * sc.sh_coeffs * 3, sc.sh_coeffs, (float)(rel0 / dist),
+                     (float)(rel1 / dist), (float)(rel2 / dist), col);
+            st256(&rp->q0, q0, q1,
+                  __hiloint2double(__float_as_int(col[0]), __float_as_int(opf)),
+                  __hiloint2double(__float_as_int(col[2]), __float_as_int(col[1])));
+            // GlobalZ: view z and |mean - origin| (gaussian_math.py:421-430)
+            if (aux) aux[i] = make_double2(z, dist);
+          }
+          g.mx = px;
+          g.my = py;
+          g.a = ca;
+          g.b = cb;
+          g.c = cc;
+          g.ia = inv_a;
+          g.ic = inv_c;
+          g.thr = thr;
+          g.op = opf;
+          g.rx0 = x0;
+          g.rx1 = x1;
+          g.ry0 = y0;
+          g.ry1 = y1;
+        }
+#else
         // _quats_to_matrices (gaussian_math.py:102-115)
         const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
         const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;
@@ -508,6 +638,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           g.ry0 = y0;
           g.ry1 = y1;
         }
+#endif
       }
     }
   }
