@@ -901,26 +901,36 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
   const int wbase = threadIdx.x & ~31;
   const unsigned lt_mask = (1u << lane) - 1;
   warp_expand(area, lane, [&](bool v, int owner, int local) {
-    // the owner's record straight from L1/L2 (lanes of one owner broadcast)
-    const SplatRec& r = recs[(int64_t)blockIdx.x * kPreThreads + wbase + owner];
+    // the owner's record straight from L1/L2 (lanes of one owner broadcast),
+    // in 256-bit loads: the culling line now, the t_opt fields for survivors
+    const int64_t gid = (int64_t)blockIdx.x * kPreThreads + wbase + owner;
+    const SplatRec* rp = recs + gid;
     bool keep = false;
     int tx = 0, ty = 0;
     double ptx = 0.0, pty = 0.0;
+    double mx = 0.0, my = 0.0;
     if (v) {
-      const int w = r.rx1 - r.rx0 + 1;
-      if (w * (r.ry1 - r.ry0 + 1) <= 64) {
+      double ca, cb, ia, ic, thr, rectd;
+      ld256(&rp->mx, mx, my, ca, cb);
+      ld256(&rp->inv_a, ia, ic, thr, rectd);
+      const double cc = __ldg(&rp->cc);
+      const unsigned rlo = (unsigned)__double2loint(rectd), rhi = (unsigned)__double2hiint(rectd);
+      const int rx0 = (int16_t)(rlo & 0xffffu), rx1 = (int16_t)(rlo >> 16);
+      const int ry0 = (int16_t)(rhi & 0xffffu), ry1 = (int16_t)(rhi >> 16);
+      const int w = rx1 - rx0 + 1;
+      if (w * (ry1 - ry0 + 1) <= 64) {
         const int b = select_bit64(s_m[wbase + owner], local);
-        tx = r.rx0 + b % w;
-        ty = r.ry0 + b / w;
+        tx = rx0 + b % w;
+        ty = ry0 + b / w;
         if (!GZ)  // the peak only feeds the t_opt key
-          max_point(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, (double)(tx * kTile),
-                    (double)(ty * kTile), 16.0, 0.0625, ptx, pty);
+          max_point(mx, my, ca, cb, cc, ia, ic, (double)(tx * kTile), (double)(ty * kTile), 16.0,
+                    0.0625, ptx, pty);
         keep = true;
       } else {
-        tx = r.rx0 + local % w;
-        ty = r.ry0 + local / w;
-        keep = tile_survives(r.mx, r.my, r.ca, r.cb, r.cc, r.inv_a, r.inv_c, r.thr, r.op,
-                             cfg.eps, tx, ty, ptx, pty);
+        tx = rx0 + local % w;
+        ty = ry0 + local / w;
+        keep = tile_survives(mx, my, ca, cb, cc, ia, ic, thr, __ldg(&rp->op), cfg.eps, tx, ty,
+                             ptx, pty);
         if (!cfg.exact) keep = true;
       }
     }
@@ -931,13 +941,24 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
     __syncwarp();
     if (keep) {
       // rasterizer.py:343-350: view z (GlobalZ) or t_opt at the 16x16 peak
-      const double depth = GZ ? aux[(int64_t)blockIdx.x * kPreThreads + wbase + owner].x
-                               : key_rec_at(cam, r, ptx, pty);
+      double depth;
+      if (GZ) {
+        depth = aux[gid].x;
+      } else {
+        double cc, q2, q0, q1, x0, x1;
+        double mm[6];
+        ld256(&rp->cc, cc, q2, mm[0], mm[1]);
+        ld256(&rp->m[2], mm[2], mm[3], mm[4], mm[5]);
+        ld256(&rp->q0, q0, q1, x0, x1);
+        double u, wv, vn;
+        cam_ray(cam, ptx, pty, u, wv, vn);
+        depth = key_rec(mm, q0, q1, q2, u, wv, vn);
+      }
       const uint32_t pos = base + __popc(kb & lt_mask);
       if ((int64_t)pos < ecap) {
         const uint64_t key = ((uint64_t)(uint32_t)(ty * gw + tx) << depth_bits) |
                              (depth_key(depth) >> (32 - depth_bits));
-        keys[pos] = (key << id_bits) | (uint64_t)(blockIdx.x * kPreThreads + wbase + owner);
+        keys[pos] = (key << id_bits) | (uint64_t)gid;
       }
     }
     if (v && lane == __ffs(peers) - 1 && kb) s_pos[wbase + owner] = base + __popc(kb);
