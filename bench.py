@@ -307,7 +307,7 @@ def run_ours(args):
     stat = {}
     for v in sorted(set(my_views)):
         st = r.render_into(cams[v], outs, stats=True)
-        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles))
+        stat[v] = (int(st.kept), int(st.bin_entries), int(st.tiles), int(st.tie_runs))
     need = max(s_[1] for s_ in stat.values())
     r.ws.ensure(gs.n, W, H, int(need * 1.1) + 4096)
 
@@ -489,6 +489,7 @@ def run_ours(args):
         "config": config_dict(args, gs.n, W, H, n_views, mode_name(mode)),
         "workload_stats": {"sh_degree": int(round(gs.sh_coeffs ** 0.5)) - 1,
                            "mean_kept": n_v, "mean_entries": e,
+                           "mean_tie_runs": float(np.mean([stat[v][3] for v in timed_views])),
                            "parallelism": f"views sharded over {world} GPU(s), no hot-path "
                                           f"collective; {n_str} views in flight per GPU (streams)"},
         "stage_ms": {nm: float(x) for nm, x in zip(STAGES, stage_mean)},

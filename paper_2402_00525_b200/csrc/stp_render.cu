@@ -966,27 +966,24 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         if (j < k_total) {
           const uint32_t sid = A.vals[start + j];
           const SplatRec* r = A.recs + sid;
-          // the record in 256-bit loads (the M' tail only for survivors)
-          double mx, my, a, b, ia, ic, thr, rect, cc, q2, m0, m1, q0, q1, opc, c12;
+          double mx, my, a, b, ia, ic, thr, rect;
           ld256(&r->mx, mx, my, a, b);
           ld256(&r->inv_a, ia, ic, thr, rect);
-          ld256(&r->cc, cc, q2, m0, m1);
-          ld256(&r->q0, q0, q1, opc, c12);
-          const float op = __int_as_float(__double2loint(opc));
+          const double2 mxy = make_double2(mx, my);
+          const double2 ab = make_double2(a, b);
+          const double2 ct = make_double2(__ldg(&r->cc), thr);
+          const double2 inv = make_double2(ia, ic);
+          const float op = __ldg(&r->op);
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             if (s ? !prod1 : !prod0) continue;
             const double r4x = (double)(sx0 + 4 * s);
             double ptx, pty;
-            max_point(mx, my, a, b, cc, ia, ic, r4x, r4y, 4.0, 0.25, ptx, pty);
-            if (alpha_keep(gpower(a, b, cc, ptx - mx, pty - my), thr, op, A.cfg.eps)) {
-              double mm[6];
-              mm[0] = m0;
-              mm[1] = m1;
-              ld256(&r->m[2], mm[2], mm[3], mm[4], mm[5]);
-              double u, wv, vn;
-              cam_ray(A.cam, ptx, pty, u, wv, vn);
-              const double dv = key_rec(mm, q0, q1, q2, u, wv, vn);
+            max_point(mxy.x, mxy.y, ab.x, ab.y, ct.x, inv.x, inv.y, r4x, r4y, 4.0, 0.25, ptx,
+                      pty);
+            if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
+                           A.cfg.eps)) {
+              const double dv = key_rec_at(A.cam, *r, ptx, pty);
               if (s) {
                 dB = dv;
                 iB = sid;
