@@ -242,61 +242,81 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
   }
   const uint64_t id_mask = (1ull << id_bits) - 1ull;
   int heads = 0, runs = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t w = keys[i];
-    const uint64_t k = w >> id_bits;                      // tile | truncated depth
-    const uint32_t tile = (uint32_t)(k >> depth_bits);
-    const uint64_t kp = (i > 0) ? keys[i - 1] >> id_bits : ~k;
-    const uint64_t kn = (i + 1 < E) ? keys[i + 1] >> id_bits : ~k;
-    const uint32_t id = (uint32_t)(w & id_mask);
-    if (i == 0 || (uint32_t)(kp >> depth_bits) != tile) {
-      ranges[tile].x = (uint32_t)i;
-      ++heads;
-    }
-    if (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile) ranges[tile].y = (uint32_t)(i + 1);
-    const bool first = i == 0 || kp != k;
-    if (kn != k) {
-      if (first) vals[i] = id;  // not in a run
-      continue;
-    }
-    if (!first) continue;       // run member: written by the run's first entry
-    ++runs;
-    int64_t L = 2;
-    while (i + L < E && (keys[i + L] >> id_bits) == k) ++L;
-    if (L <= kTieLocal) {
-      double d[kTieLocal];
-      uint32_t ids[kTieLocal];
-      for (int m = 0; m < L; ++m) {
-        const uint32_t im = (uint32_t)(keys[i + m] & id_mask);
-        const double dv = entry_depth64(recs, cam, im, (int)tile, gw, aux);
-        // insertion by (depth, rank); members arrive in rank order
-        int p = m - 1;
-        while (p >= 0 && d[p] > dv) {
-          d[p + 1] = d[p];
-          ids[p + 1] = ids[p];
-          --p;
-        }
-        d[p + 1] = dv;
-        ids[p + 1] = im;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform loop: each warp takes 32 consecutive entries per step, so
+  // the runs found in a step are re-ordered by the whole warp (one lane per
+  // member) instead of serially by their first member's thread
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < E;
+       i0 += stride) {
+    const int64_t i = i0 + lane;
+    bool short_head = false;
+    int L = 1;
+    uint32_t tile = 0;
+    if (i < E) {
+      const uint64_t w = keys[i];
+      const uint64_t k = w >> id_bits;                      // tile | truncated depth
+      tile = (uint32_t)(k >> depth_bits);
+      const uint64_t kp = (i > 0) ? keys[i - 1] >> id_bits : ~k;
+      const uint64_t kn = (i + 1 < E) ? keys[i + 1] >> id_bits : ~k;
+      const uint32_t id = (uint32_t)(w & id_mask);
+      if (i == 0 || (uint32_t)(kp >> depth_bits) != tile) {
+        ranges[tile].x = (uint32_t)i;
+        ++heads;
       }
-      for (int m = 0; m < L; ++m) vals[i + m] = ids[m];
-    } else {
-      // long runs (coincident splats): insertion sort through memory
-      for (int64_t m = 0; m < L; ++m) {
-        const uint32_t iv = (uint32_t)(keys[i + m] & id_mask);
-        const double dv = entry_depth64(recs, cam, iv, (int)tile, gw, aux);
-        int64_t p = m - 1;
-        while (p >= 0) {
-          const double dp = d64[i + p];
-          if (!(dp > dv)) break;
-          vals[i + p + 1] = vals[i + p];
-          d64[i + p + 1] = dp;
-          --p;
+      if (i + 1 == E || (uint32_t)(kn >> depth_bits) != tile) ranges[tile].y = (uint32_t)(i + 1);
+      const bool first = i == 0 || kp != k;
+      if (kn != k) {
+        if (first) vals[i] = id;  // not in a run
+      } else if (first) {
+        ++runs;
+        L = 2;
+        while (i + L < E && (keys[i + L] >> id_bits) == k) ++L;
+        if (L <= kTieLocal) {
+          short_head = true;
+        } else {
+          // long runs (coincident splats): insertion sort through memory
+          for (int64_t m = 0; m < L; ++m) {
+            const uint32_t iv = (uint32_t)(keys[i + m] & id_mask);
+            const double dv = entry_depth64(recs, cam, iv, (int)tile, gw, aux);
+            int64_t p = m - 1;
+            while (p >= 0) {
+              const double dp = d64[i + p];
+              if (!(dp > dv)) break;
+              vals[i + p + 1] = vals[i + p];
+              d64[i + p + 1] = dp;
+              --p;
+            }
+            vals[i + p + 1] = iv;
+            d64[i + p + 1] = dv;
+          }
         }
-        vals[i + p + 1] = iv;
-        d64[i + p + 1] = dv;
       }
+    }
+    // the step's short runs, one at a time, all lanes: lane m < L computes
+    // member m's float64 depth, its rank by (depth, Gaussian id) -- the
+    // stable LSD sort delivered members in rank order, ids are ranks -- and
+    // writes its id to the run's slot of that rank
+    unsigned hb = __ballot_sync(kFull, short_head);
+    while (hb) {
+      const int src = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int64_t hi = __shfl_sync(kFull, i, src);
+      const int hl = __shfl_sync(kFull, L, src);
+      const int ht = (int)__shfl_sync(kFull, tile, src);
+      double d = INFINITY;
+      uint32_t im = 0xffffffffu;
+      if (lane < hl) {
+        im = (uint32_t)(keys[hi + lane] & id_mask);
+        d = entry_depth64(recs, cam, im, ht, gw, aux);
+      }
+      int rank = 0;
+      for (int m = 0; m < hl; ++m) {
+        const double od = __shfl_sync(kFull, d, m);
+        const uint32_t oi = __shfl_sync(kFull, im, m);
+        rank += (od < d) | ((od == d) & (oi < im));
+      }
+      if (lane < hl) vals[hi + rank] = im;
     }
   }
   const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
