@@ -30,6 +30,9 @@ constexpr unsigned long long kRowsListed = ~0ull;
 #ifndef STP_K1_V2
 #define STP_K1_V2 1  // register-lean projection + streaming record stores
 #endif
+#ifndef STP_K1_HOIST
+#define STP_K1_HOIST 1  // all input loads issued before the cull tests
+#endif
 
 __constant__ double c_SH_C0 = 0.28209479177387814;
 __constant__ double c_SH_C1 = 0.4886025119029199;
@@ -338,6 +341,20 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
 
   if (valid) {
     const double* W = cam.R;
+#if STP_K1_V2 && STP_K1_HOIST
+    // issue every per-Gaussian input load up front (before the near-plane and
+    // guard tests), so their latencies overlap instead of following the
+    // projection math; culled Gaussians cost 32 B of extra reads
+    float4 qf_h;
+    float s0_h, s1_h, s2_h, op_h;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(qf_h.x), "=f"(qf_h.y), "=f"(qf_h.z), "=f"(qf_h.w)
+                 : "l"(reinterpret_cast<const float4*>(sc.quats) + i));
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(s0_h) : "l"(sc.scales + 3 * i + 0));
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(s1_h) : "l"(sc.scales + 3 * i + 1));
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(s2_h) : "l"(sc.scales + 3 * i + 2));
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(op_h) : "l"(sc.opacity + i));
+#endif
     const double rel0 = (double)__ldg(sc.means + 3 * i + 0) - cam.pos[0];
     const double rel1 = (double)__ldg(sc.means + 3 * i + 1) - cam.pos[1];
     const double rel2 = (double)__ldg(sc.means + 3 * i + 2) - cam.pos[2];
@@ -379,7 +396,11 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
         double V[9];
         {
           // _quats_to_matrices (gaussian_math.py:102-115)
+#if STP_K1_HOIST
+          const float4 qf = qf_h;
+#else
           const float4 qf = __ldg(reinterpret_cast<const float4*>(sc.quats) + i);
+#endif
           const double qw0 = qf.x, qx0 = qf.y, qy0 = qf.z, qz0 = qf.w;
           const double qn = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
           const double w = fdiv(qw0, qn), x = fdiv(qx0, qn), y = fdiv(qy0, qn),
@@ -396,9 +417,13 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
               V[aa * 3 + bb] = W[aa * 3 + 0] * rot[0 * 3 + bb] + W[aa * 3 + 1] * rot[1 * 3 + bb] +
                                W[aa * 3 + 2] * rot[2 * 3 + bb];
         }
+#if STP_K1_HOIST
+        const double s0 = s0_h, s1 = s1_h, s2 = s2_h;
+#else
         const double s0 = __ldg(sc.scales + 3 * i + 0);
         const double s1 = __ldg(sc.scales + 3 * i + 1);
         const double s2 = __ldg(sc.scales + 3 * i + 2);
+#endif
         // J (gaussian_math.py:378-383): rows (J00, 0, J02), (0, J11, J12)
         const double zz = z * z;
         const double J00 = fdiv(cam.fx, z), J02 = -fdiv(cam.fx * pv0, zz);
@@ -425,7 +450,11 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           st256(&rp->mx, px, py, ca, cb);
           const double inv_a = fdiv(1.0, ca), inv_c = fdiv(1.0, cc);
           // opacity-aware radius (:399-404)
+#if STP_K1_HOIST
+          const float opf = op_h;
+#else
           const float opf = __ldg(sc.opacity + i);
+#endif
           const double op = opf;
           const double mid = 0.5 * (a + c);
           const double lam_max = mid + sqrt(fmax(mid * mid - a * c + b * b, 0.0));
