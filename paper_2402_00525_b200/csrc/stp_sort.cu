@@ -19,6 +19,12 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = STP_SORT_ITEMS;
 constexpr int kSortTile = kSortPartition;  // kSortThreads * kSortItems items per partition
 constexpr int kRadix = 256;
+#ifndef STP_SORT_SPIN_NS
+#define STP_SORT_SPIN_NS 0  // back-off of the look-back spin (0: none)
+#endif
+#ifndef STP_SORT_BALLOT
+#define STP_SORT_BALLOT 0  // warp ranking by ballots instead of match.any
+#endif
 
 // look-back word: [epoch:32 | flag:2 | count:30]
 constexpr unsigned long long kFlagAgg = 1ull << 30;
@@ -100,7 +106,18 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   const unsigned lt_mask = (1u << lane) - 1;
 #pragma unroll
   for (int k = 0; k < kSortItems; ++k) {
+#if STP_SORT_BALLOT
+    // peers with the same 8-bit digit from 8 ballots (VOTE is an ALU op;
+    // MATCH.ANY waits on the short scoreboard)
+    unsigned peers = kFull;
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      const unsigned bb = __ballot_sync(kFull, (dig[k] >> bit) & 1u);
+      peers &= ((dig[k] >> bit) & 1u) ? bb : ~bb;
+    }
+#else
     const unsigned peers = __match_any_sync(kFull, dig[k]);
+#endif
     const int leader = 31 - __clz(peers);
     const uint32_t before = sm.warp_hist[w][dig[k]];
     __syncwarp();
@@ -133,7 +150,12 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       while (true) {
         const unsigned long long v =
             *reinterpret_cast<volatile unsigned long long*>(lookback + (size_t)p * kRadix + d);
-        if ((v >> 32) != epoch || ((v >> 30) & 3ull) == 0) continue;  // not yet published
+        if ((v >> 32) != epoch || ((v >> 30) & 3ull) == 0) {  // not yet published
+#if STP_SORT_SPIN_NS > 0
+          __nanosleep(STP_SORT_SPIN_NS);
+#endif
+          continue;
+        }
         excl += v & kCountMask;
         if (((v >> 30) & 3ull) == 2) break;
         --p;
