@@ -59,6 +59,15 @@ __device__ __forceinline__ void st256(void* p, double a, double b, double c, dou
                : "memory");
 }
 
+__device__ __forceinline__ void st128d(void* p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void st128f(void* p, float a, float b, float c, float d) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
 struct DevCam {
   double R[9];
   double pos[3];

@@ -33,6 +33,9 @@ constexpr unsigned long long kRowsListed = ~0ull;
 #ifndef STP_K1_HOIST
 #define STP_K1_HOIST 1  // all input loads issued before the cull tests
 #endif
+#ifndef STP_K1_SH_EARLY
+#define STP_K1_SH_EARLY 0  // SH colour before the covariance algebra (needs HOIST)
+#endif
 
 __constant__ double c_SH_C0 = 0.28209479177387814;
 __constant__ double c_SH_C1 = 0.4886025119029199;
@@ -188,6 +191,21 @@ __device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
   }
 }
 
+// Lanes sharing warp_expand's owner: owners are non-decreasing across the
+// valid lanes (pairs are handed out in owner order) and invalid lanes get a
+// unique key, so the peers of a lane are the run of equal keys around it --
+// found with one shuffle and one ballot instead of MATCH.ANY (which waits on
+// the short scoreboard).
+__device__ __forceinline__ unsigned run_peers(int key, int lane) {
+  const int prev = __shfl_up_sync(kFull, key, 1);
+  const unsigned heads = __ballot_sync(kFull, lane == 0 || prev != key);
+  const unsigned upto = 0xffffffffu >> (31 - lane);         // bits 0..lane
+  const int start = 31 - __clz(heads & upto);
+  const unsigned above = heads & ~upto;                     // heads after this lane
+  const unsigned end_mask = above ? ((1u << (__ffs(above) - 1)) - 1u) : 0xffffffffu;
+  return end_mask & ~((1u << start) - 1u);
+}
+
 // coarse tile rect (rasterizer.py:307-321), clamped in double first; empty
 // rects come back as x0 > x1.
 __device__ __forceinline__ void coarse_rect(double px, double py, double radius, int gw, int gh,
@@ -274,7 +292,7 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
       keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
                                           cfg.eps, tx, ty, px, py);
     }
-    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned peers = run_peers(v ? owner : 32 + lane, lane);
     const unsigned kb = __ballot_sync(kFull, keep);
     if (v && lane == __ffs(peers) - 1 && (kb & peers)) {
       s_cnt[wbase + owner] += __popc(kb & peers);
@@ -381,6 +399,19 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
           const char* shp = reinterpret_cast<const char*>(sc.sh + i * sc.sh_coeffs * 3);
           asm volatile("prefetch.global.L2 [%0];" ::"l"(shp));
           if (sc.sh_coeffs > 5) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + 128));
+        }
+#endif
+#if STP_K1_V2 && STP_K1_SH_EARLY
+        // SH colour first (gaussian_math.py:415-419), so its 48 registers of
+        // coefficients are dead before the covariance algebra; opacity and
+        // colour go out in one 128-bit store (a degenerate Gaussian's record
+        // is never read)
+        {
+          const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
+          float col[3];
+          sh_color(sc.sh + (int64_t)i * sc.sh_coeffs * 3, sc.sh_coeffs, (float)(rel0 / dist),
+                   (float)(rel1 / dist), (float)(rel2 / dist), col);
+          st128f(&recs[i].op, op_h, col[0], col[1], col[2]);
         }
 #endif
 #if STP_K1_V2
@@ -492,6 +523,11 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
             const double q2 = m02 * pv0 + m12 * pv1 + m22 * z;
             st256(&rp->cc, cc, q2, m00, m11);
             st256(&rp->m[2], m22, 2.0 * m01, 2.0 * m02, 2.0 * m12);
+#if STP_K1_SH_EARLY
+            st128d(&rp->q0, q0, q1);
+            // GlobalZ: view z and |mean - origin| (gaussian_math.py:421-430)
+            if (aux) aux[i] = make_double2(z, sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2));
+#else
             // SH colour along (mean - origin) / |mean - origin| (:415-419)
             const double dist = sqrt(rel0 * rel0 + rel1 * rel1 + rel2 * rel2);
             float col[3];
@@ -502,6 +538,7 @@ __global__ void __launch_bounds__(kPreThreads, STP_K1_MINB) k_preprocess(
                   __hiloint2double(__float_as_int(col[2]), __float_as_int(col[1])));
             // GlobalZ: view z and |mean - origin| (gaussian_math.py:421-430)
             if (aux) aux[i] = make_double2(z, dist);
+#endif
           }
           g.mx = px;
           g.my = py;
@@ -964,7 +1001,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
       }
     }
     // deterministic slot: rank among this round's survivors of the same splat
-    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
+    const unsigned peers = run_peers(v ? owner : 32 + lane, lane);
     const unsigned kb = __ballot_sync(kFull, keep) & peers;
     const uint32_t base = v ? s_pos[wbase + owner] : 0;
     __syncwarp();

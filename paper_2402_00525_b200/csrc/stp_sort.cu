@@ -23,7 +23,7 @@ constexpr int kRadix = 256;
 #define STP_SORT_SPIN_NS 0  // back-off of the look-back spin (0: none)
 #endif
 #ifndef STP_SORT_BALLOT
-#define STP_SORT_BALLOT 0  // warp ranking by ballots instead of match.any
+#define STP_SORT_BALLOT 1  // warp ranking by ballots instead of match.any (K4 0.410 -> 0.382 ms)
 #endif
 
 // look-back word: [epoch:32 | flag:2 | count:30]
