@@ -191,21 +191,6 @@ __device__ __forceinline__ void warp_expand(int area, int lane, F&& fn) {
   }
 }
 
-// Lanes sharing warp_expand's owner: owners are non-decreasing across the
-// valid lanes (pairs are handed out in owner order) and invalid lanes get a
-// unique key, so the peers of a lane are the run of equal keys around it --
-// found with one shuffle and one ballot instead of MATCH.ANY (which waits on
-// the short scoreboard).
-__device__ __forceinline__ unsigned run_peers(int key, int lane) {
-  const int prev = __shfl_up_sync(kFull, key, 1);
-  const unsigned heads = __ballot_sync(kFull, lane == 0 || prev != key);
-  const unsigned upto = 0xffffffffu >> (31 - lane);         // bits 0..lane
-  const int start = 31 - __clz(heads & upto);
-  const unsigned above = heads & ~upto;                     // heads after this lane
-  const unsigned end_mask = above ? ((1u << (__ffs(above) - 1)) - 1u) : 0xffffffffu;
-  return end_mask & ~((1u << start) - 1u);
-}
-
 // coarse tile rect (rasterizer.py:307-321), clamped in double first; empty
 // rects come back as x0 > x1.
 __device__ __forceinline__ void coarse_rect(double px, double py, double radius, int gw, int gh,
@@ -292,7 +277,7 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
       keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
                                           cfg.eps, tx, ty, px, py);
     }
-    const unsigned peers = run_peers(v ? owner : 32 + lane, lane);
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
     const unsigned kb = __ballot_sync(kFull, keep);
     if (v && lane == __ffs(peers) - 1 && (kb & peers)) {
       s_cnt[wbase + owner] += __popc(kb & peers);
@@ -1001,7 +986,7 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
       }
     }
     // deterministic slot: rank among this round's survivors of the same splat
-    const unsigned peers = run_peers(v ? owner : 32 + lane, lane);
+    const unsigned peers = __match_any_sync(kFull, v ? owner : 32 + lane);
     const unsigned kb = __ballot_sync(kFull, keep) & peers;
     const uint32_t base = v ? s_pos[wbase + owner] : 0;
     __syncwarp();

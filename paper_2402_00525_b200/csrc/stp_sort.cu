@@ -19,6 +19,9 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = STP_SORT_ITEMS;
 constexpr int kSortTile = kSortPartition;  // kSortThreads * kSortItems items per partition
 constexpr int kRadix = 256;
+#ifndef STP_HIST_BALLOT
+#define STP_HIST_BALLOT 0  // digit histogram with warp-aggregated (ballot) updates
+#endif
 #ifndef STP_SORT_SPIN_NS
 #define STP_SORT_SPIN_NS 0  // back-off of the look-back spin (0: none)
 #endif
@@ -44,12 +47,34 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
   for (int i = threadIdx.x; i < 8 * kRadix; i += kSortThreads) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   const int64_t E = n_entries(counters, ecap);
+#if STP_HIST_BALLOT
+  // warp-aggregated: the lanes holding the same digit (8 ballots) add once
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * kSortThreads;
+  for (int64_t i0 = (int64_t)blockIdx.x * kSortThreads + (threadIdx.x & ~31); i0 < E;
+       i0 += stride) {
+    const int64_t i = i0 + lane;
+    const bool in = i < E;
+    const uint64_t k = in ? keys[i] : 0ull;
+    for (int p = 0; p < passes; ++p) {
+      const uint32_t d = (uint32_t)(k >> (shift0 + 8 * p)) & 0xffu;
+      unsigned peers = __ballot_sync(kFull, in);
+#pragma unroll
+      for (int bit = 0; bit < 8; ++bit) {
+        const unsigned bb = __ballot_sync(kFull, (d >> bit) & 1u);
+        peers &= ((d >> bit) & 1u) ? bb : ~bb;
+      }
+      if (in && lane == __ffs(peers) - 1) atomicAdd(&s_hist[p][d], (unsigned)__popc(peers));
+    }
+  }
+#else
   for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * kSortThreads) {
     const uint64_t k = keys[i];
     for (int p = 0; p < passes; ++p)
       atomicAdd(&s_hist[p][(k >> (shift0 + 8 * p)) & 0xff], 1u);
   }
+#endif
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += kSortThreads) {
     const uint32_t v = (&s_hist[0][0])[i];
