@@ -19,6 +19,9 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = STP_SORT_ITEMS;
 constexpr int kSortTile = kSortPartition;  // kSortThreads * kSortItems items per partition
 constexpr int kRadix = 256;
+#ifndef STP_SORT_WARPSCAN
+#define STP_SORT_WARPSCAN 1  // digit scans by warp shuffles, global prefix once per block
+#endif
 #ifndef STP_HIST_BALLOT
 #define STP_HIST_BALLOT 0  // digit histogram with warp-aggregated (ballot) updates
 #endif
@@ -87,9 +90,30 @@ struct SortSmem {
   uint32_t local_off[kRadix];              // block-local exclusive digit offsets
   uint32_t global_off[kRadix];             // this partition's first output slot per digit
   uint32_t scan_tmp[kRadix];
+  uint32_t gex[kRadix];                    // exclusive prefix of the pass's global histogram
+  uint32_t wtot[kSortWarps];               // per-warp totals of a 256-digit block scan
   uint32_t part;
   uint64_t keys[kSortTile];
 };
+
+// exclusive prefix over the 256 digits (thread = digit): warp shuffles + the
+// 8 warp totals (two barriers instead of a 16-barrier Hillis-Steele scan)
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* wtot, int lane,
+                                                       int w) {
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wtot[w] = inc;
+  __syncthreads();
+  uint32_t off = 0;
+#pragma unroll
+  for (int ww = 0; ww < kSortWarps; ++ww) off += (ww < w) ? wtot[ww] : 0u;
+  __syncthreads();  // wtot is reused by the next scan
+  return off + inc - v;
+}
 
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
@@ -101,6 +125,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t E = n_entries(counters, ecap);
   const uint32_t epoch = (uint32_t)counters[C_EPOCH];
+#if STP_SORT_WARPSCAN
+  // the pass's global digit offsets: the same for every partition, so once
+  // per persistent block
+  sm.gex[tid] = block_excl_scan256(hist[tid], sm.wtot, lane, w);
+#endif
   // persistent: partitions are claimed in increasing order (so the look-back
   // predecessor is always held by a running block) until the entries run out
   for (;;) {
@@ -187,6 +216,13 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
       }
       atomicExch(my, tag | kFlagPre | ((excl + block_cnt) & kCountMask));
     }
+#if STP_SORT_WARPSCAN
+    sm.global_off[d] = (uint32_t)excl + sm.gex[d];
+  }
+  // block-local exclusive digit offsets
+  sm.local_off[tid] = block_excl_scan256(block_cnt, sm.wtot, lane, w);
+  __syncthreads();
+#else
     sm.global_off[d] = (uint32_t)excl;
     sm.scan_tmp[d] = hist[d];
   }
@@ -211,6 +247,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     sm.local_off[d] = s_b[d] - b;
   }
   __syncthreads();
+#endif
   // scatter into shared memory in block-local sorted order
 #pragma unroll
   for (int k = 0; k < kSortItems; ++k) {
