@@ -105,7 +105,12 @@ enum Counter {
   C_SM = 80,        // render: per-SM sub-tile counters [256]
   C_SMT = 336,      // render: per-SM tile ring [256][kSmRing] (tag<<32 | tile+2)
   C_PSTAT = C_SMT + 256 * 64,  // K1: per-SM projection stats [256][4] (behind, guard, degenerate, kept)
+#ifdef STP_TAIL_PROF
+  C_TAILP = C_PSTAT + 256 * 4,  // render: per-warp (start, end) globaltimer [4096][2]
+  C_COUNT = C_TAILP + 4096 * 2
+#else
   C_COUNT = C_PSTAT + 256 * 4
+#endif
 };
 
 // ---------------------------------------------------------------------------

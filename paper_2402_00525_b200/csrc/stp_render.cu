@@ -91,9 +91,42 @@ __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t i
   return l | (e & li);
 }
 
+// Sort keys of the hierarchical kernel.  STP_IKEY=1: the float64 key as an
+// order-preserving int64 (sign-magnitude -> two's complement: negative
+// doubles flip their magnitude bits; -0 is canonicalised to +0 first, so
+// int64 equality is float64 equality).  The (key, rank) order is unchanged
+// bit for bit; compares run on the integer pipe instead of DSETP chains.
+#ifndef STP_IKEY
+#define STP_IKEY 0  // measured slower: K6 3.71 vs 3.59 ms (profiles/r2w)
+#endif
+#if STP_IKEY
+typedef long long Key;
+__device__ __forceinline__ Key dkey(double d) {
+  const long long b = __double_as_longlong(d + 0.0);
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double kdbl(Key k) {  // the transform is an involution
+  return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL));
+}
+__device__ __forceinline__ bool lt(Key a, uint32_t ia, Key b, uint32_t ib) {
+  const bool l = a < b, e = a == b, li = ia < ib;
+  return l | (e & li);
+}
+constexpr Key kInfKey = 0x7ff0000000000000LL;  // dkey(+inf)
+#else
+typedef double Key;
+__device__ __forceinline__ Key dkey(double d) { return d; }
+__device__ __forceinline__ double kdbl(Key k) { return k; }
+#define kInfKey ((double)INFINITY)
+#endif
+__device__ __forceinline__ Key shfl_k(Key v, int src, int w = 32) {
+  return __shfl_sync(kFull, v, src, w);
+}
+__device__ __forceinline__ Key shfl_xor_k(Key v, int m) { return __shfl_xor_sync(kFull, v, m); }
+
 template <int QH>
 struct Head {
-  double t[QH];
+  Key t[QH];
   double a[QH];
   uint32_t id[QH];
   int n;
@@ -352,7 +385,7 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
 // EXACT: the queue size equals QH; else runtime qh <= QH.
 template <int QH, bool EXACT, int XM>
 __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArgs& A, int qh_rt,
-                                          double t, double al, uint32_t id) {
+                                          Key t, double al, uint32_t id) {
   const int qh = EXACT ? QH : qh_rt;
   const bool full = H.n >= qh;
   if (EXACT && full) {
@@ -363,7 +396,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     bool c[QH];
 #pragma unroll
     for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
-    blend_live<XM>(P, A, c[0] ? t : H.t[0], c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
+    blend_live<XM>(P, A, kdbl(c[0] ? t : H.t[0]), c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
       const bool nx = i + 1 < QH;
@@ -377,7 +410,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
   }
   if (full) {
     const bool e_min = lt(t, id, H.t[0], H.id[0]);
-    blend<XM>(P, A, e_min ? t : H.t[0], e_min ? al : H.a[0], e_min ? id : H.id[0]);
+    blend<XM>(P, A, kdbl(e_min ? t : H.t[0]), e_min ? al : H.a[0], e_min ? id : H.id[0]);
     if (e_min) return;
     // drop H[0], insert e at position c among H[1..qh-1]
     int c = 0;
@@ -396,12 +429,14 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     return;
   }
   H.n++;
-  double xt = t, xa = al;
+  Key xt = t;
+  double xa = al;
   uint32_t xi = id;
 #pragma unroll
   for (int i = 0; i < QH; ++i) {
     const bool sw = lt(xt, xi, H.t[i], H.id[i]);
-    const double ht = H.t[i], ha = H.a[i];
+    const Key ht = H.t[i];
+    const double ha = H.a[i];
     const uint32_t hi = H.id[i];
     H.t[i] = sw ? xt : ht;
     H.a[i] = sw ? xa : ha;
@@ -434,15 +469,15 @@ __device__ __forceinline__ void warp_sort(double& d, uint32_t& id, int lane) {
 // Bitonic sort of two (d, id) arrays, one pair per lane each, ascending.
 // Rolled loops: the kernel is instruction-fetch bound, code size matters more
 // than the loop overhead here.
-__device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1, uint32_t& i1,
+__device__ __forceinline__ void warp_sort2(Key& d0, uint32_t& i0, Key& d1, uint32_t& i1,
                                            int lane) {
 #pragma unroll 1
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
-      const double od0 = shfl_xor_d(d0, j);
+      const Key od0 = shfl_xor_k(d0, j);
       const uint32_t oi0 = __shfl_xor_sync(kFull, i0, j);
-      const double od1 = shfl_xor_d(d1, j);
+      const Key od1 = shfl_xor_k(d1, j);
       const uint32_t oi1 = __shfl_xor_sync(kFull, i1, j);
       const bool want_min = (((lane & j) == 0) == ((lane & k) == 0));
       // elements are distinct (ids unique) except empty slots, whose swap is
@@ -459,12 +494,12 @@ __device__ __forceinline__ void warp_sort2(double& d0, uint32_t& i0, double& d1,
 
 // Bitonic sort of (d, id) within each 16-lane half of the warp (L = lane &
 // 15; both halves sorted ascending at once).
-__device__ __forceinline__ void half_sort16(double& d, uint32_t& id, int L) {
+__device__ __forceinline__ void half_sort16(Key& d, uint32_t& id, int L) {
 #pragma unroll 1
   for (int k = 2; k <= 16; k <<= 1) {
 #pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
-      const double od = shfl_xor_d(d, j);
+      const Key od = shfl_xor_k(d, j);
       const uint32_t oi = __shfl_xor_sync(kFull, id, j);
       const bool want_min = (((L & j) == 0) == ((L & k) == 0));
       const bool take = want_min == lt(od, oi, d, id);
@@ -489,8 +524,31 @@ __device__ __forceinline__ int select_bit32(unsigned m, int k) {
 }
 
 // number of (d,id) in sorted a[0..n) strictly below (x, xi)
-__device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai, int n, double x,
+#ifndef STP_CB8
+#define STP_CB8 0  // measured slower: K6 4.08 vs 3.60 ms (profiles/r2x)
+#endif
+__device__ __forceinline__ int count_below(const Key* ad, const uint32_t* ai, int n, Key x,
                                            uint32_t xi) {
+#if STP_CB8
+  // 8-ary search: each round issues 7 independent probes (lo + i q - 1) and
+  // narrows [lo, hi) to at most q - 1 elements, so n <= 63 takes two
+  // rounds of shared-memory latency instead of five dependent ones
+  int lo = 0, hi = n;
+  while (hi > lo) {
+    const int q = (hi - lo + 8) >> 3;  // 8q > hi - lo: the range after is < q
+    int k = 0;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+      const int p = lo + i * q - 1;
+      const int pc = p < hi ? p : lo;
+      k += (p < hi) & lt(ad[pc], ai[pc], x, xi);
+    }
+    const int nlo = lo + k * q;
+    hi = min(hi, nlo + q - 1);
+    lo = nlo;
+  }
+  return lo;
+#else
   int lo = 0, hi = n;
   while (lo < hi) {
     const int m = (lo + hi) >> 1;
@@ -498,6 +556,7 @@ __device__ __forceinline__ int count_below(const double* ad, const uint32_t* ai,
     else hi = m;
   }
   return lo;
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -546,12 +605,12 @@ __host__ __device__ inline size_t warp_smem_bytes(int qt, int qm) {
 }
 
 struct SubQ {
-  double* d;
+  Key* d;
   uint32_t* i;
   int qt, qm;
-  __device__ __forceinline__ double* td(int c) const { return d + c * qt; }
+  __device__ __forceinline__ Key* td(int c) const { return d + c * qt; }
   __device__ __forceinline__ uint32_t* ti(int c) const { return i + c * qt; }
-  __device__ __forceinline__ double* bd() const { return d + q_grp0(qt, qm); }
+  __device__ __forceinline__ Key* bd() const { return d + q_grp0(qt, qm); }
   __device__ __forceinline__ uint32_t* bi() const { return i + q_grp0(qt, qm); }
   __device__ __forceinline__ int o_mid(int q) const { return q_mid0(qt) + q * (qm + 1); }
   __device__ __forceinline__ int o_scr(int q) const { return q_scr0(qt, qm) + q * (qm + 5); }
@@ -585,8 +644,8 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
   const int nd = sub_nd(qt, qm), ni = sub_ni(qt, qm);
   auto subq = [&](int s) {
     SubQ q;
-    q.d = reinterpret_cast<double*>(wbase) + s * nd;
-    q.i = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(wbase) + 2 * nd) + s * ni;
+    q.d = reinterpret_cast<Key*>(wbase) + s * nd;
+    q.i = reinterpret_cast<uint32_t*>(reinterpret_cast<Key*>(wbase) + 2 * nd) + s * ni;
     q.qt = qt;
     q.qm = qm;
     return q;
@@ -607,6 +666,11 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
   unsigned long long* sm_cnt = A.counters + C_SM + smid;
   unsigned long long* sm_ring = A.counters + C_SMT + smid * kSmRing;
 
+#ifdef STP_TAIL_PROF
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int gwarp = blockIdx.x * kWarpsPerBlock + warp;
+#endif
   for (;;) {
     // ---- work item: (tile, pair) with the 8 pairs of a tile on one SM
     int tile = -1, pair = 0;
@@ -646,6 +710,14 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
     }
     tile = __shfl_sync(kFull, tile, 0);
     pair = __shfl_sync(kFull, pair, 0);
+#ifdef STP_TAIL_PROF
+    if (tile < 0 && lane == 0 && gwarp < 4096) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      A.counters[C_TAILP + 2 * gwarp] = t_start;
+      A.counters[C_TAILP + 2 * gwarp + 1] = t_end;
+    }
+#endif
     if (tile < 0) break;
     const int tx = tile % A.gw, ty = tile / A.gw;
     // pair p covers sub-tiles (row p>>1, columns 2*(p&1), 2*(p&1)+1)
@@ -668,7 +740,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
     H.n = 0;
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
-      H.t[i] = INFINITY;
+      H.t[i] = kInfKey;
       H.a[i] = 0.0;
       H.id[i] = kNoId;
     }
@@ -694,9 +766,9 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
       const int c = min(16, nt);
       const uint32_t* tip = Q.ti(cur) + th;
       const double r2x = (double)(sx0 + 4 * s) + (mq & 1) * 2, r2y = r4y + (mq >> 1) * 2;
-      double gd[4];
+      Key gd[4];
       uint32_t gi[4];
-      gd[0] = gd[1] = INFINITY;
+      gd[0] = gd[1] = kInfKey;
       gi[0] = gi[1] = kNoId;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -720,7 +792,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           }
           double cu, cw, cv;
           cam_ray(A.cam, ptx, pty, cu, cw, cv);
-          const double dv = key_rec(m, q0, q1, q2, cu, cw, cv);
+          const Key dv = dkey(key_rec(m, q0, q1, q2, cu, cw, cv));
           if (u) {
             gd[1] = dv;
             gi[1] = sid;
@@ -730,18 +802,18 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           }
         }
       }
-      gd[2] = shfl_xor_d(gd[0], 1);
+      gd[2] = shfl_xor_k(gd[0], 1);
       gi[2] = __shfl_xor_sync(kFull, gi[0], 1);
-      gd[3] = shfl_xor_d(gd[1], 1);
+      gd[3] = shfl_xor_k(gd[1], 1);
       gi[3] = __shfl_xor_sync(kFull, gi[1], 1);
 #define CSWAP(a, b)                                        \
   if (lt(gd[b], gi[b], gd[a], gi[a])) {                    \
-    const double td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_;   \
+    const Key td_ = gd[a]; gd[a] = gd[b]; gd[b] = td_;      \
     const uint32_t ti_ = gi[a]; gi[a] = gi[b]; gi[b] = ti_; \
   }
       CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
 #undef CSWAP
-      double* gdp = Q.d + Q.o_grp(mq);
+      Key* gdp = Q.d + Q.o_grp(mq);
       uint32_t* gip = Q.i + Q.o_grp(mq);
       // lane half mh stores sorted slots 2mh, 2mh+1 (selects: no local memory)
       gdp[4 * mg + 2 * mh] = mh ? gd[2] : gd[0];
@@ -749,15 +821,15 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
       gdp[4 * mg + 2 * mh + 1] = mh ? gd[3] : gd[1];
       gip[4 * mg + 2 * mh + 1] = mh ? gi[3] : gi[1];
       __syncwarp();
-      double* md = Q.d + Q.o_mid(mq);
+      Key* md = Q.d + Q.o_mid(mq);
       uint32_t* mi = Q.i + Q.o_mid(mq);
-      double* sd = Q.d + Q.o_scr(mq);
+      Key* sd = Q.d + Q.o_scr(mq);
       uint32_t* si = Q.i + Q.o_scr(mq);
       uint32_t* ring = Q.ring(mq, R);
       const int slot0 = lane & 7;
       for (int gg = 0; 4 * gg < c; ++gg) {
         const int ng = min(4, c - 4 * gg);
-        const double* g_d = gdp + 4 * gg;
+        const Key* g_d = gdp + 4 * gg;
         const uint32_t* g_i = gip + 4 * gg;
         STAT_ADD(10, (lane & 7) == 0);                                        // mid merges
         STAT_ADD(11, (lane & 7) == 0 && QMX == 8 && qm == 8 && nm == 4 && ng == 4);  // steady
@@ -767,9 +839,9 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           // element: its rank = index + #(other list < it), 4 comparisons.
           const bool from_mid = slot0 < 4;
           const int ix = slot0 & 3;
-          const double x = from_mid ? md[ix] : g_d[ix];
+          const Key x = from_mid ? md[ix] : g_d[ix];
           const uint32_t xi = from_mid ? mi[ix] : g_i[ix];
-          const double* od = from_mid ? g_d : md;
+          const Key* od = from_mid ? g_d : md;
           const uint32_t* oi = from_mid ? g_i : mi;
 #ifdef STP_WORK_STATS
           {  // merges that are appends (the group sorts after the mid queue)
@@ -797,7 +869,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         for (int k = 0; k < 1; ++k) {
 #pragma unroll 1
           for (int sl = slot0; sl < L; sl += 8) {
-            double x;
+            Key x;
             uint32_t xi;
             int rk;
             if (sl < nm) {
@@ -911,7 +983,8 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
                 // 92% of full-queue pushes -- measured slower: 3.86 vs 3.59
                 // ms, profiles/r2o; the select network is cheaper than the
                 // vote + second code path)
-                if (ps[k] && P.T >= term) head_push<QH, EXACT, XM>(P, H, A, qh_rt, ts[k], as[k], ids[k]);
+                if (ps[k] && P.T >= term)
+                  head_push<QH, EXACT, XM>(P, H, A, qh_rt, dkey(ts[k]), as[k], ids[k]);
               }
             }
 #ifdef STP_WORK_STATS
@@ -961,7 +1034,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         if (!prod0 && !prod1) continue;
         // ---- load + 4x4 cull + d4 for both sub-tiles (hierarchy.py:190-199)
         const int j = pos + lane;
-        double dA = INFINITY, dB = INFINITY;
+        Key dA = kInfKey, dB = kInfKey;
         uint32_t iA = kNoId, iB = kNoId;
         if (j < k_total) {
           const uint32_t sid = A.vals[start + j];
@@ -983,7 +1056,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
                       pty);
             if (alpha_keep(gpower(ab.x, ab.y, ct.x, ptx - mxy.x, pty - mxy.y), ct.y, op,
                            A.cfg.eps)) {
-              const double dv = key_rec_at(A.cam, *r, ptx, pty);
+              const Key dv = dkey(key_rec_at(A.cam, *r, ptx, pty));
               if (s) {
                 dB = dv;
                 iB = sid;
@@ -1010,7 +1083,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         // and run ONE 16-wide bitonic network over both halves at once (10
         // stages, one array) instead of two 32-wide networks (15 stages, two
         // arrays).  Lane h*16+L then holds element L of sub-tile h.
-        double dS0, dS1;
+        Key dS0, dS1;
         uint32_t iS0, iS1;
         int xS0, xS1;
         bool vS0, vS1;
@@ -1020,17 +1093,17 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           const int h = lane >> 4, L = lane & 15;
           const int nk = h ? nkB : nkA;
           const int src = select_bit32(h ? bB : bA, L < nk ? L : 0);
-          const double sdA = shfl_d(dA, src), sdB = shfl_d(dB, src);
+          const Key sdA = shfl_k(dA, src), sdB = shfl_k(dB, src);
           const uint32_t siA = __shfl_sync(kFull, iA, src), siB = __shfl_sync(kFull, iB, src);
-          double d = h ? sdB : sdA;
+          Key d = h ? sdB : sdA;
           uint32_t id = h ? siB : siA;
           if (L >= nk) {
-            d = INFINITY;
+            d = kInfKey;
             id = kNoId;
           }
 #ifdef STP_WORK_STATS
           {  // sortedness of each half's candidates in bin order
-            const double pd = __shfl_up_sync(kFull, d, 1, 16);
+            const Key pd = __shfl_up_sync(kFull, d, 1, 16);
             const uint32_t pi = __shfl_up_sync(kFull, id, 1, 16);
             const bool ok = L == 0 || L >= nk || lt(pd, pi, d, id);
             const unsigned bo = __ballot_sync(kFull, ok);
@@ -1045,7 +1118,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           int rank = 0;
 #pragma unroll kRankUnroll
           for (int jj = 0; jj < 16; ++jj) {
-            const double od = __shfl_sync(kFull, d, jj, 16);
+            const Key od = shfl_k(d, jj, 16);
             const uint32_t oi = __shfl_sync(kFull, id, jj, 16);
             rank += lt(od, oi, d, id);
           }
@@ -1081,7 +1154,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
           // h, else sub-tile 0; pass 2 (non-compact only): sub-tile 1
           const int s1 = cpt ? (lane >> 4) : 0;
           const bool v1 = s1 ? vS1 : vS0;
-          const double d1 = s1 ? dS1 : dS0;
+          const Key d1 = s1 ? dS1 : dS0;
           const uint32_t i1 = s1 ? iS1 : iS0;
           const int x1 = s1 ? xS1 : xS0;
           const SubQ Q1 = subq(s1);
@@ -1141,7 +1214,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
             // tail elements to (re)place: none for an append onto a tail at slot 0
             const int n0 = (nkA && !(app0 && th0 == 0)) ? nt0 : 0;
             const int n1 = (nkB && !(app1 && th1 == 0)) ? nt1 : 0;
-            double tv[2];
+            Key tv[2];
             uint32_t tiv[2];
             int trk[2], tpos[2], tst[2];
 #pragma unroll
@@ -1210,7 +1283,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
             const int t = u - (st ? n0 : 0);
             const SubQ Q = subq(st);
             const int cur = st ? cur1 : cur0, th = st ? th1 : th0;
-            const double tv = Q.td(cur)[th + t];
+            const Key tv = Q.td(cur)[th + t];
             const uint32_t tiv = Q.ti(cur)[th + t];
             const int rk = count_below(Q.bd(), Q.bi(), st ? nkB : nkA, tv, tiv);
             Q.td(cur ^ 1)[t + rk] = tv;
@@ -1255,7 +1328,7 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
     // terminated sub-tiles
 #pragma unroll
     for (int i = 0; i < QH; ++i)
-      if (i < H.n) blend<XM>(P, A, H.t[i], H.a[i], H.id[i]);
+      if (i < H.n) blend<XM>(P, A, kdbl(H.t[i]), H.a[i], H.id[i]);
     PROF_ADD(4);
 
     xm_done<XM>(P, A);
