@@ -439,35 +439,56 @@ def run_ours(args):
     # e2e: the public render path (Renderer.render_into, one per view slot)
     # with host output buffers (pinned): per step the camera goes host->device
     # (by-value launch params) and colour + transmittance + the status word
-    # come back device->host, on the same streams / views-in-flight as the
-    # timed region; every step's status is checked.
+    # come back device->host.  The device->host copies run on their own
+    # stream (the copy engine) behind an event of the view that produced
+    # them, so they overlap the next views' kernels; every view slot has two
+    # output buffers, and a slot waits for the copy of the buffer it is about
+    # to overwrite (two views earlier).  Every step's status is checked.
     e2e_steps = args.e2e_steps or min(steps, 32)
     rs = [r] + [Renderer(gs, mode, cfg, dev) for _ in range(n_str - 1)]
     for k in range(1, n_str):
         rs[k].ws = wss[k]
-    host = [(torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True),
-             torch.empty((H, W), dtype=torch.float32, pin_memory=True)) for _ in range(n_str)]
+    bufs = [[keep[k], r.alloc_outputs(W, H)] for k in range(n_str)]
+    for k in range(n_str):
+        for b in bufs[k]:
+            b["status"] = torch.zeros(2, dtype=torch.int64, device=dev)
+    host = [[(torch.empty((H, W, 3), dtype=torch.float32, pin_memory=True),
+              torch.empty((H, W), dtype=torch.float32, pin_memory=True)) for _ in range(2)]
+            for _ in range(n_str)]
     host_status = torch.zeros((e2e_steps, 2), dtype=torch.int64, pin_memory=True)
+    copy_stream = torch.cuda.Stream(dev)
+    copied = [[None, None] for _ in range(n_str)]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(streams[0])
-    for st in streams[1:]:
+    for st in streams[1:] + [copy_stream]:
         st.wait_event(e0)
     for s in range(e2e_steps):
         k = s % n_str
+        pb = (s // n_str) & 1
+        o = bufs[k][pb]
+        if copied[k][pb] is not None:
+            streams[k].wait_event(copied[k][pb])
         with torch.cuda.stream(streams[k]):
-            rs[k].render_into(cams[my_views[warm + s % steps]], keep[k],
-                              stream=streams[k].cuda_stream)
-            host[k][0].copy_(keep[k]["color"], non_blocking=True)
-            host[k][1].copy_(keep[k]["transmittance"], non_blocking=True)
-            host_status[s].copy_(rs[k].status, non_blocking=True)
+            rs[k].render_into(cams[my_views[warm + s % steps]], o, stream=streams[k].cuda_stream)
+        done = torch.cuda.Event()
+        done.record(streams[k])
+        copy_stream.wait_event(done)
+        with torch.cuda.stream(copy_stream):
+            host[k][pb][0].copy_(o["color"], non_blocking=True)
+            host[k][pb][1].copy_(o["transmittance"], non_blocking=True)
+            host_status[s].copy_(o["status"], non_blocking=True)
+        c = torch.cuda.Event()
+        c.record(copy_stream)
+        copied[k][pb] = c
     for st in streams[1:]:
         j = torch.cuda.Event()
         j.record(st)
-        streams[0].wait_event(j)
+        copy_stream.wait_event(j)
+    streams[0].wait_stream(copy_stream)
     e1.record(streams[0])
     torch.cuda.synchronize()
     if (host_status[:, 0] != 0).any():
@@ -514,7 +535,8 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": ctypes.sizeof(_lib.StpCamera),
                 "d2h_bytes_per_step": H * W * 16 + 16, "steps": e2e_steps,
-                "path": "Renderer.render_into (C ABI stp_render) -> pinned host colour + T"},
+                "path": "Renderer.render_into (C ABI stp_render) -> pinned host colour + T "
+                        "(copies on a copy stream, double-buffered outputs per view slot)"},
         "gpu_launches": launches_per_view * steps,
         "clocks": clk,
         "wall_s_timed_region": t_wall,
