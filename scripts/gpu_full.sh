@@ -1,5 +1,5 @@
 #!/bin/bash
-# smoke, GPU tests (incl. the reference replay), bench, per-kernel ncu.  Usage: scripts/r2_full.sh TAG
+# smoke, GPU tests (incl. the reference replay), bench, per-kernel ncu.  Usage: scripts/gpu_full.sh TAG
 TAG=${1:-r2c}
 O=gpurun_out/$TAG
 mkdir -p $O
