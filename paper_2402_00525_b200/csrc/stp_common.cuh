@@ -254,6 +254,36 @@ __device__ __forceinline__ double exp_neg_nb(double p, const double* tab) {
   return ts * e;
 }
 
+// exp_neg_nb with shorter dependency chains (same table and polynomial):
+// the lo part of the ln2/64 reduction becomes a factor exp(kd lo) = 1 + kd lo
+// (|kd lo| < 1e-13) applied to the table entry in parallel, and exp(-r) - 1
+// is evaluated in powers of r^2 (Estrin-like), folded into the final
+// tsc * (1 + q) as one fma: 8 dependent float64 steps instead of 11.
+// Host check against expl: max 2.4 ulp (exp_neg_nb: 1.9 ulp).
+__device__ __forceinline__ double exp_neg_fast(double p, const double* tab) {
+  const double sh = fma(p, c_exp_k[0], 0x1.8p52);
+  const int k = __double2loint(sh);
+  const double kd = sh - 0x1.8p52;
+  const double r = fma(-kd, c_exp_k[1], p);
+  const double corr = fma(kd, c_exp_k[2], 1.0);
+  const double tj = tab[k & 63];
+  const double ts = __hiloint2double(__double2hiint(tj) - ((k >> 6) << 20), __double2loint(tj));
+  const double tsc = ts * corr;
+  const double s2 = r * r;
+  const double a1 = fma(-r, c_exp_k[6], c_exp_k[7]);  // 1/2 - r/6
+  const double a2 = fma(-r, c_exp_k[4], c_exp_k[5]);  // 1/24 - r/120
+  const double a2b = fma(s2, c_exp_k[3], a2);         // + r^2/720
+  const double inner = fma(s2, a2b, a1);
+  const double q = fma(s2, inner, -r);                 // exp(-r) - 1
+  return fma(tsc, q, tsc);
+}
+
+// gauss2d's exponent from the halved conic (ha = a/2, hc = c/2; halving is
+// exact): one multiply shorter than 0.5 * (...)
+__device__ __forceinline__ double gpower_h(double ha, double b, double hc, double dx, double dy) {
+  return fma(b * dx, dy, fma(hc * dy, dy, (ha * dx) * dx));
+}
+
 // exponent of gauss2d (tile_culling.py:96)
 __device__ __forceinline__ double gpower(double a, double b, double c, double dx, double dy) {
   return 0.5 * (a * dx * dx + c * dy * dy) + b * dx * dy;

@@ -96,6 +96,12 @@ __device__ __forceinline__ bool lt(double da, uint32_t ia, double db, uint32_t i
 // doubles flip their magnitude bits; -0 is canonicalised to +0 first, so
 // int64 equality is float64 equality).  The (key, rank) order is unchanged
 // bit for bit; compares run on the integer pipe instead of DSETP chains.
+#ifndef STP_EXP_FAST
+#define STP_EXP_FAST 0  // exp_neg_fast in the pixel stage: measured neutral-to-slower (3.59-3.63 vs 3.58 ms, profiles/r2aa)
+#endif
+#ifndef STP_GPOW_H
+#define STP_GPOW_H 1  // pixel-stage power from the halved conic (gpower_h): K6 3.578 vs 3.592 ms (profiles/r2aa)
+#endif
 #ifndef STP_IKEY
 #define STP_IKEY 0  // measured slower: K6 3.71 vs 3.59 ms (profiles/r2w)
 #endif
@@ -368,11 +374,19 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
   ld256(&r->q0, q0, q1, opc, c12);
   const float op = __int_as_float(__double2loint(opc));
   const double dx = P.px - mx, dy = P.py - my;
+#if STP_GPOW_H
+  const double pw = gpower_h(0.5 * a, b, 0.5 * c, dx, dy);
+#else
   const double pw = gpower(a, b, c, dx, dy);
+#endif
   const double mm[6] = {m0, m1, m2, m3, m4, m5};
   t = key_rec(mm, q0, q1, q2, P.u, P.w, P.vn);
   const double pc = min_le(pw, 700.0);
+#if STP_EXP_FAST
+  al = (double)op * exp_neg_fast(pc, tab);
+#else
   al = (double)op * exp_neg_nb(pc, tab);
+#endif
   const bool pass = al >= A.cfg.eps;  // hierarchy.py:99-101
   al = min_le(al, A.cfg.cap);
   return pass;
