@@ -392,6 +392,29 @@ __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A
   return pass;
 }
 
+// emit_eval_bf behind a conservative float32 early-out (alpha < eps beyond
+// doubt, the float64 test decides everything else) for the scans of the
+// Window / FullPerPixel kernel, which evaluate every bin entry at every pixel
+// of a 16 x 2 strip: most entries miss the whole strip, and the warp then
+// skips the t_opt division and the exp.
+#ifndef STP_WIN_PRETEST
+#define STP_WIN_PRETEST 1
+#endif
+__device__ __forceinline__ bool emit_eval_pre(const Pixel& P, const RenderArgs& A, uint32_t id,
+                                              const double* tab, double& t, double& al) {
+#if STP_WIN_PRETEST
+  const SplatRec* r = A.recs + id;
+  double mx, my, a, b;
+  ld256(&r->mx, mx, my, a, b);
+  const double c = __ldg(&r->cc);
+  const float op = __ldg(&r->op);
+  const double pw = gpower_h(0.5 * a, b, 0.5 * c, P.px - mx, P.py - my);
+  const float thr = __logf(op) - A.log_eps;
+  if ((float)pw > thr + fmaf(1e-5f, fabsf(thr), 1e-5f)) return false;
+#endif
+  return emit_eval_bf(P, A, id, tab, t, al);
+}
+
 // insort into the pixel queue; on overflow blend the minimum
 // (hierarchy.py:110-113).  Branch-free: empty slots hold (+inf, ~0), the
 // overflow case blends min(e, H[0]) and, if H[0] left, shifts the queue and
@@ -1674,7 +1697,7 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
         if (!__any_sync(kFull, P.T >= term)) break;
         const uint32_t id = A.vals[j];
         double t, al;
-        const bool pass = emit_eval_bf(P, A, id, s_tab, t, al);
+        const bool pass = emit_eval_pre(P, A, id, s_tab, t, al);
         if (!(pass && P.T >= term)) continue;
         if (n < cap) {
           sift_up(t, id, n++);
@@ -1706,7 +1729,7 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
         for (uint32_t j = rg.x; j < rg.y; ++j) {
           const uint32_t id = A.vals[j];
           double t, al;
-          if (!emit_eval_bf(P, A, id, s_tab, t, al)) continue;
+          if (!emit_eval_pre(P, A, id, s_tab, t, al)) continue;
           if (!first && !lt(lo_t, lo_id, t, id)) continue;  // blended by an earlier pass
           if (n < cap) sift_up(t, id, n++);
           else if (lt(t, id, hd[0], hid[0])) sift_down(t, id, n);  // replaces the maximum
