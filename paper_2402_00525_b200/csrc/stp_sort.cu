@@ -28,6 +28,12 @@ constexpr int kRadix = 256;
 #ifndef STP_SORT_SPIN_NS
 #define STP_SORT_SPIN_NS 0  // back-off of the look-back spin (0: none)
 #endif
+#ifndef STP_SORT_LATE_LB
+#define STP_SORT_LATE_LB 1  // publish the aggregate, scatter locally, then look back
+#endif
+#ifndef STP_SORT_LB_VEC
+#define STP_SORT_LB_VEC 4  // predecessors read per look-back step
+#endif
 #ifndef STP_SORT_BALLOT
 #define STP_SORT_BALLOT 1  // warp ranking by ballots instead of match.any (K4 0.410 -> 0.382 ms)
 #endif
@@ -71,11 +77,21 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
     }
   }
 #else
-  for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < E;
-       i += (int64_t)gridDim.x * kSortThreads) {
-    const uint64_t k = keys[i];
-    for (int p = 0; p < passes; ++p)
-      atomicAdd(&s_hist[p][(k >> (shift0 + 8 * p)) & 0xff], 1u);
+  // four independent key loads in flight per thread
+  constexpr int U = 4;
+  for (int64_t i0 = (int64_t)blockIdx.x * kSortThreads * U + threadIdx.x; i0 < E;
+       i0 += (int64_t)gridDim.x * kSortThreads * U) {
+    uint64_t k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kSortThreads;
+      k[u] = i < E ? keys[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + (int64_t)u * kSortThreads < E)
+        for (int p = 0; p < passes; ++p)
+          atomicAdd(&s_hist[p][(k[u] >> (shift0 + 8 * p)) & 0xff], 1u);
   }
 #endif
   __syncthreads();
@@ -113,6 +129,39 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* wto
   for (int ww = 0; ww < kSortWarps; ++ww) off += (ww < w) ? wtot[ww] : 0u;
   __syncthreads();  // wtot is reused by the next scan
   return off + inc - v;
+}
+
+// Decoupled look-back for digit d of partition part (> 0): sums the
+// predecessors' aggregates back to the first inclusive prefix.  LB_VEC
+// predecessors are read per step with independent loads (one round trip
+// instead of LB_VEC); an unpublished one is re-read until it is published.
+__device__ __forceinline__ unsigned long long look_back(const unsigned long long* lookback,
+                                                        int64_t part, int d, uint32_t epoch) {
+  unsigned long long excl = 0;
+  int64_t p = part - 1;
+  for (;;) {
+    unsigned long long v[STP_SORT_LB_VEC];
+#pragma unroll
+    for (int k = 0; k < STP_SORT_LB_VEC; ++k) {
+      const int64_t q = p - k >= 0 ? p - k : 0;
+      v[k] = *reinterpret_cast<volatile const unsigned long long*>(lookback + (size_t)q * kRadix + d);
+    }
+    bool done = false;
+    int used = 0;
+#pragma unroll
+    for (int k = 0; k < STP_SORT_LB_VEC; ++k) {
+      if (done || used < k) continue;  // stopped at an earlier word
+      if ((v[k] >> 32) != epoch || ((v[k] >> 30) & 3ull) == 0) continue;  // not yet published
+      excl += v[k] & kCountMask;
+      ++used;
+      if (((v[k] >> 30) & 3ull) == 2) done = true;  // inclusive prefix (partition 0 always is)
+    }
+    if (done) return excl;
+    p -= used;
+#if STP_SORT_SPIN_NS > 0
+    if (!used) __nanosleep(STP_SORT_SPIN_NS);
+#endif
+  }
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
@@ -182,6 +231,42 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   __syncthreads();
   // per digit: exclusive scan across warps, block total
   uint32_t block_cnt;
+#if STP_SORT_LATE_LB && STP_SORT_WARPSCAN
+  // publish the aggregate, build the block-local order in shared memory, and
+  // only then look back: the predecessors publish while this block scatters
+  {
+    const int d = tid;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = sm.warp_hist[ww][d];
+      sm.warp_hist[ww][d] = sum;
+      sum += c;
+    }
+    block_cnt = sum;
+    const unsigned long long tag = (unsigned long long)epoch << 32;
+    atomicExch(lookback + (size_t)part * kRadix + d,
+               tag | (part == 0 ? kFlagPre : kFlagAgg) | (unsigned long long)block_cnt);
+  }
+  sm.local_off[tid] = block_excl_scan256(block_cnt, sm.wtot, lane, w);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t pos = sm.local_off[dig[k]] + sm.warp_hist[w][dig[k]] + rank[k];
+    if (pos < (uint32_t)kSortTile) sm.keys[pos] = key[k];
+  }
+  {
+    const int d = tid;
+    unsigned long long excl = 0;
+    if (part > 0) {
+      excl = look_back(lookback, part, d, epoch);
+      atomicExch(lookback + (size_t)part * kRadix + d,
+                 ((unsigned long long)epoch << 32) | kFlagPre | ((excl + block_cnt) & kCountMask));
+    }
+    sm.global_off[d] = (uint32_t)excl + sm.gex[d];
+  }
+  __syncthreads();
+#else
   {
     const int d = tid;  // kSortThreads == kRadix
     uint32_t sum = 0;
@@ -255,6 +340,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     if (pos < (uint32_t)kSortTile) sm.keys[pos] = key[k];
   }
   __syncthreads();
+#endif
   for (int i = tid; i < n_valid; i += kSortThreads) {
     const uint64_t k = sm.keys[i];
     const uint32_t d = (uint32_t)(k >> shift) & 0xff;
