@@ -1614,6 +1614,34 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
 #define STP_FULL_HEAP 48  // K (round 1: K = 16 selection in registers, 112.9 ms)
 #endif
 
+// Strip cull of the Window / FullPerPixel scans: may entry `id` reach
+// alpha >= eps at any pixel centre of the 16 x 2 strip with top-left pixel
+// (x0, y0)?  Exact minimum of the power over each row's segment of centres
+// (a 1-D quadratic, vertex clamped to the segment) against thr = log(op/eps)
+// plus a margin, so a culled entry fails the float64 alpha test at every
+// pixel of the strip (NaN fields are kept: the exact test decides them).
+#ifndef STP_WIN_STRIP
+#define STP_WIN_STRIP 1
+#endif
+__device__ __forceinline__ bool strip_may_pass(const SplatRec* r, double x0, double y0) {
+  double mx, my, a, b, ia, ic, thr, rect;
+  ld256(&r->mx, mx, my, a, b);
+  ld256(&r->inv_a, ia, ic, thr, rect);
+  const double c = __ldg(&r->cc);
+  if (!(a > 0.0)) return true;  // not convex in x (e.g. a SplatBatch conic): no bound
+  const double X0 = x0 + 0.5 - mx, X1 = x0 + 15.5 - mx;
+  double qmin = INFINITY, mag = 0.0;
+#pragma unroll
+  for (int row = 0; row < 2; ++row) {
+    const double dy = y0 + 0.5 + row - my;
+    const double dx = fmin(fmax(-b * dy * ia, X0), X1);  // vertex of 0.5 a dx^2 + b dy dx
+    const double t1 = 0.5 * a * dx * dx, t2 = b * dx * dy, t3 = 0.5 * c * dy * dy;
+    qmin = fmin(qmin, t1 + t2 + t3);
+    mag = fmax(mag, fabs(t1) + fabs(t2) + fabs(t3));
+  }
+  return !(qmin > thr + 1e-6 * (1.0 + fabs(thr)) + 1e-9 * mag);
+}
+
 template <int XM, bool FULL>
 __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1646,6 +1674,8 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
       P.rc = 0;
       xm_init<XM>(P, A);
     }
+    const double sx = (double)(tx * kTile), sy = (double)(ty * kTile + 2 * strip);
+    const bool strip_ok = A.cfg.eps > 0.0;  // eps <= 0: every entry passes alpha
     // place (xd, xi) in the root's hole and sift it down over n elements
     auto sift_down = [&](double xd, uint32_t xi, int n) {
       int p = 0;
@@ -1693,22 +1723,35 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
     const uint2 rg = A.ranges[tile];
     if (!FULL) {
       int n = 0;
-      for (uint32_t j = rg.x; j < rg.y; ++j) {
-        if (!__any_sync(kFull, P.T >= term)) break;
-        const uint32_t id = A.vals[j];
-        double t, al;
-        const bool pass = emit_eval_pre(P, A, id, s_tab, t, al);
-        if (!(pass && P.T >= term)) continue;
-        if (n < cap) {
-          sift_up(t, id, n++);
-        } else if (lt(t, id, hd[0], hid[0])) {
-          blend<XM>(P, A, t, al, id);  // the incoming entry is the smallest: emitted
-        } else {
-          // emit the minimum; the incoming entry takes its place
-          const double t0 = hd[0];
-          const uint32_t i0 = hid[0];
-          sift_down(t, id, n);
-          blend_at(t0, i0);
+      bool stop = false;
+      for (uint32_t j0 = rg.x; j0 < rg.y && !stop; j0 += 32) {
+        // lane-per-entry strip cull, then the survivors in bin order
+        const uint32_t jl = j0 + lane;
+        const uint32_t idl = jl < rg.y ? A.vals[jl] : 0u;
+        unsigned surv = __ballot_sync(kFull, jl < rg.y && (!STP_WIN_STRIP || !strip_ok ||
+                                                          strip_may_pass(A.recs + idl, sx, sy)));
+        while (surv) {
+          const int src = __ffs(surv) - 1;
+          surv &= surv - 1;
+          if (!__any_sync(kFull, P.T >= term)) {
+            stop = true;
+            break;
+          }
+          const uint32_t id = __shfl_sync(kFull, idl, src);
+          double t, al;
+          const bool pass = emit_eval_pre(P, A, id, s_tab, t, al);
+          if (!(pass && P.T >= term)) continue;
+          if (n < cap) {
+            sift_up(t, id, n++);
+          } else if (lt(t, id, hd[0], hid[0])) {
+            blend<XM>(P, A, t, al, id);  // the incoming entry is the smallest: emitted
+          } else {
+            // emit the minimum; the incoming entry takes its place
+            const double t0 = hd[0];
+            const uint32_t i0 = hid[0];
+            sift_down(t, id, n);
+            blend_at(t0, i0);
+          }
         }
       }
       // drain in ascending (t, rank) (rasterizer.py:565-573); no-ops once terminated
@@ -1724,16 +1767,28 @@ __global__ void __launch_bounds__(kWinPix) k_render_window(RenderArgs A, int cap
       uint32_t lo_id = 0;
       bool first = true, more = true;
       while (__any_sync(kFull, more && P.T >= term)) {
-        if (!(more && P.T >= term)) continue;
+        // every lane runs the scan (lane-per-entry cull, warp shuffles);
+        // only the pixels still selecting (act) evaluate and keep entries
+        const bool act = more && P.T >= term;
         int n = 0;
-        for (uint32_t j = rg.x; j < rg.y; ++j) {
-          const uint32_t id = A.vals[j];
-          double t, al;
-          if (!emit_eval_pre(P, A, id, s_tab, t, al)) continue;
-          if (!first && !lt(lo_t, lo_id, t, id)) continue;  // blended by an earlier pass
-          if (n < cap) sift_up(t, id, n++);
-          else if (lt(t, id, hd[0], hid[0])) sift_down(t, id, n);  // replaces the maximum
+        for (uint32_t j0 = rg.x; j0 < rg.y; j0 += 32) {
+          const uint32_t jl = j0 + lane;
+          const uint32_t idl = jl < rg.y ? A.vals[jl] : 0u;
+          unsigned surv = __ballot_sync(kFull, jl < rg.y && (!STP_WIN_STRIP || !strip_ok ||
+                                                            strip_may_pass(A.recs + idl, sx, sy)));
+          while (surv) {
+            const int src = __ffs(surv) - 1;
+            surv &= surv - 1;
+            const uint32_t id = __shfl_sync(kFull, idl, src);
+            if (!act) continue;
+            double t, al;
+            if (!emit_eval_pre(P, A, id, s_tab, t, al)) continue;
+            if (!first && !lt(lo_t, lo_id, t, id)) continue;  // blended by an earlier pass
+            if (n < cap) sift_up(t, id, n++);
+            else if (lt(t, id, hd[0], hid[0])) sift_down(t, id, n);  // replaces the maximum
+          }
         }
+        if (!act) continue;
         // heap-sort ascending in place, then blend in order
         for (int m = n - 1; m > 0; --m) {
           const double xd = hd[(size_t)m * kWinPix];
