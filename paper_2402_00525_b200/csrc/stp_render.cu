@@ -48,6 +48,12 @@ constexpr int kWarpsPerBlock = STP_WARPS_PER_BLOCK;
 constexpr int kRenderThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kNoId = 0xffffffffu;
 
+// Warp-level strip culls in the Window / FullPerPixel and GlobalZ scans
+// (strip_may_pass)
+#ifndef STP_WIN_STRIP
+#define STP_WIN_STRIP 1
+#endif
+
 // Optional phase profiler (-DSTP_PHASE_PROF): warp-cycles per phase are
 // accumulated into counters C_PROF.. (load, merge, push_mid, pixel, items).
 #ifdef STP_PHASE_PROF
@@ -1450,6 +1456,10 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
       s_c[kGzThreads], s_dist[kGzThreads];
   __shared__ float4 s_oc[kGzThreads];  // opacity, colour
   __shared__ uint32_t s_id[kGzThreads];
+#if STP_WIN_STRIP
+  __shared__ double s_ia[kGzThreads], s_thr[kGzThreads];
+  __shared__ unsigned s_msk[kGzThreads / 32][kGzThreads / 32];  // [warp][32-entry group]
+#endif
   const int tid = threadIdx.x;
   if (tid < 64) s_tab[tid] = kExp2Tab[tid];
   // the per-blend helpers take RenderArgs
@@ -1499,10 +1509,53 @@ __global__ void __launch_bounds__(kGzThreads) k_render_globalz(GzArgs A) {
         s_oc[tid] = __ldg(reinterpret_cast<const float4*>(&r->op));
         s_dist[tid] = A.aux[id].y;
         s_id[tid] = id;
+#if STP_WIN_STRIP
+        s_ia[tid] = __ldg(&r->inv_a);
+        s_thr[tid] = __ldg(&r->thr);
+#endif
       }
       __syncthreads();
       const int n = (int)min((uint32_t)kGzThreads, rg.y - base);
+#if STP_WIN_STRIP
+      // warp-level strip cull (the warp's pixels are a 16 x 2 strip): lane l
+      // tests staged entries l, l + 32, ...; the warp walks the survivors in
+      // bin order (strip_may_pass's bound, on the staged fields)
+      unsigned* const msk = s_msk[tid >> 5];
+      {
+        const int lane = tid & 31;
+        const double sx = (double)(tx * kTile), sy = (double)(ty * kTile + 2 * (tid >> 5));
+#pragma unroll
+        for (int q = 0; q < kGzThreads / 32; ++q) {
+          const int k = 32 * q + lane;
+          bool keep = k < n;
+          if (keep && A.cfg.eps > 0.0) {
+            const double a = s_a[k], b = s_b[k], c = s_c[k], ia = s_ia[k], thr = s_thr[k];
+            if (a > 0.0) {
+              const double X0 = sx + 0.5 - s_mx[k], X1 = sx + 15.5 - s_mx[k];
+              double qmin = INFINITY, mag = 0.0;
+#pragma unroll
+              for (int row = 0; row < 2; ++row) {
+                const double dy = sy + 0.5 + row - s_my[k];
+                const double dx = fmin(fmax(-b * dy * ia, X0), X1);
+                const double t1 = 0.5 * a * dx * dx, t2 = b * dx * dy, t3 = 0.5 * c * dy * dy;
+                qmin = fmin(qmin, t1 + t2 + t3);
+                mag = fmax(mag, fabs(t1) + fabs(t2) + fabs(t3));
+              }
+              keep = !(qmin > thr + 1e-6 * (1.0 + fabs(thr)) + 1e-9 * mag);
+            }
+          }
+          const unsigned bq = __ballot_sync(kFull, keep);
+          if (lane == 0) msk[q] = bq;
+        }
+        __syncwarp();
+      }
+      for (int q = 0; q < kGzThreads / 32; ++q)
+      for (unsigned mq = msk[q]; mq; mq &= mq - 1) {
+        const int k = 32 * q + __ffs(mq) - 1;
+        if (!(P.T >= A.cfg.term)) continue;
+#else
       for (int k = 0; k < n && P.T >= A.cfg.term; ++k) {
+#endif
         const double dx = P.px - s_mx[k], dy = P.py - s_my[k];
         const double pw = gpower(s_a[k], s_b[k], s_c[k], dx, dy);
         const float4 oc = s_oc[k];
@@ -1620,9 +1673,6 @@ __host__ __device__ inline size_t window_smem_bytes(int cap) {
 // (a 1-D quadratic, vertex clamped to the segment) against thr = log(op/eps)
 // plus a margin, so a culled entry fails the float64 alpha test at every
 // pixel of the strip (NaN fields are kept: the exact test decides them).
-#ifndef STP_WIN_STRIP
-#define STP_WIN_STRIP 1
-#endif
 __device__ __forceinline__ bool strip_may_pass(const SplatRec* r, double x0, double y0) {
   double mx, my, a, b, ia, ic, thr, rect;
   ld256(&r->mx, mx, my, a, b);
