@@ -335,40 +335,9 @@ __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double
 }
 
 // alpha / eps test / cap / pixel-ray t_opt of one emitted entry
-// (hierarchy.py:94-105).  Returns false when the entry is dropped.
-__device__ __forceinline__ bool emit_eval(const Pixel& P, const RenderArgs& A, uint32_t id,
-                                          const double* tab, double& t, double& al) {
-  const SplatRec* r = A.recs + id;
-  const double2 mxy = __ldg(reinterpret_cast<const double2*>(&r->mx));
-  const double2 ab = __ldg(reinterpret_cast<const double2*>(&r->ca));
-  const double2 ct = __ldg(reinterpret_cast<const double2*>(&r->cc));  // cc q2
-  const double dx = P.px - mxy.x, dy = P.py - mxy.y;
-  const double pw = gpower(ab.x, ab.y, ct.x, dx, dy);
-  const float op = __ldg(&r->op);
-  // early out when alpha < eps beyond doubt (MUFU log; the decision is the
-  // float64 test below)
-  const float thr = __logf(op) - A.log_eps;
-  if ((float)pw > thr + fmaf(1e-5f, fabsf(thr), 1e-5f)) return false;
-  const double2 m01 = __ldg(reinterpret_cast<const double2*>(&r->m[0]));
-  const double2 m23 = __ldg(reinterpret_cast<const double2*>(&r->m[2]));
-  const double2 m45 = __ldg(reinterpret_cast<const double2*>(&r->m[4]));
-  const double2 q01 = __ldg(reinterpret_cast<const double2*>(&r->q0));
-  const double q2 = ct.y;
-  // t_opt on the pixel ray (camera-space form of rasterizer.py:405-406).
-  // Evaluated before the alpha test: the exp chain and this chain are
-  // independent, so the two float64 dependency chains overlap (alpha < eps
-  // after the early-out above is rare).
-  const double mm[6] = {m01.x, m01.y, m23.x, m23.y, m45.x, m45.y};
-  t = key_rec(mm, q01.x, q01.y, q2, P.u, P.w, P.vn);
-  al = (double)op * exp_neg(pw, tab);
-  if (al < A.cfg.eps) return false;
-  if (al > A.cfg.cap) al = A.cfg.cap;
-  return true;
-}
-
-// Branch-free variant: everything computed, the decision returned, so two
-// evaluations placed side by side form one basic block whose float64 chains
-// the scheduler interleaves.
+// (hierarchy.py:94-105), branch-free: everything computed, the decision
+// returned, so two evaluations placed side by side form one basic block
+// whose float64 chains the scheduler interleaves.
 __device__ __forceinline__ bool emit_eval_bf(const Pixel& P, const RenderArgs& A, uint32_t id,
                                              const double* tab, double& t, double& al) {
   const SplatRec* r = A.recs + id;
@@ -487,25 +456,6 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     xt = sw ? ht : xt;
     xa = sw ? ha : xa;
     xi = sw ? hi : xi;
-  }
-}
-
-// Bitonic sort of one (d, id) per lane, ascending across the warp.
-__device__ __forceinline__ void warp_sort(double& d, uint32_t& id, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const double od = shfl_xor_d(d, j);
-      const uint32_t oi = __shfl_xor_sync(kFull, id, j);
-      const bool want_min = (((lane & j) == 0) == ((lane & k) == 0));
-      const bool o_less = lt(od, oi, d, id);
-      const bool o_greater = lt(d, id, od, oi);
-      if (want_min ? o_less : o_greater) {
-        d = od;
-        id = oi;
-      }
-    }
   }
 }
 
