@@ -157,6 +157,29 @@ struct SplatGeo {
   float op;
   int rx0, rx1, ry0, ry1;
 };
+// x = q * w + r for 0 <= x < 2^22, 0 < w < 2^12: the float reciprocal
+// estimate is within one of the quotient, one correction makes it exact
+// (an integer division by a runtime w is a ~20-instruction sequence)
+#ifndef STP_FDIVMOD
+#define STP_FDIVMOD 1
+#endif
+__device__ __forceinline__ void divmod_small(int x, int w, int& q, int& r) {
+#if STP_FDIVMOD
+  q = __float2int_rz(((float)x + 0.5f) * __frcp_rn((float)w));
+  r = x - q * w;
+  if (r < 0) {
+    --q;
+    r += w;
+  } else if (r >= w) {
+    ++q;
+    r -= w;
+  }
+#else
+  q = x / w;
+  r = x - q * w;
+#endif
+}
+
 struct StagedGeo {
   double mx, my, a, b, c, ia, ic, thr;
   float op;
@@ -272,7 +295,9 @@ __device__ __forceinline__ void count_tiles(int reason, const SplatGeo& g, int64
     bool keep = false;
     if (v) {
       const StagedGeo& o = s_geo[wbase + owner];
-      const int tx = o.rx0 + local % o.wx, ty = o.ry0 + local / o.wx;
+      int qy, rx;
+      divmod_small(local, o.wx, qy, rx);
+      const int tx = o.rx0 + rx, ty = o.ry0 + qy;
       double px, py;
       keep = !cfg.exact || tile_survives(o.mx, o.my, o.a, o.b, o.c, o.ia, o.ic, o.thr, o.op,
                                           cfg.eps, tx, ty, px, py);
@@ -971,15 +996,19 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
       const int w = rx1 - rx0 + 1;
       if (w * (ry1 - ry0 + 1) <= 64) {
         const int b = select_bit64(s_m[wbase + owner], local);
-        tx = rx0 + b % w;
-        ty = ry0 + b / w;
+        int qy, rx;
+        divmod_small(b, w, qy, rx);
+        tx = rx0 + rx;
+        ty = ry0 + qy;
         if (!GZ)  // the peak only feeds the t_opt key
           max_point(mx, my, ca, cb, cc, ia, ic, (double)(tx * kTile), (double)(ty * kTile), 16.0,
                     0.0625, ptx, pty);
         keep = true;
       } else {
-        tx = rx0 + local % w;
-        ty = ry0 + local / w;
+        int qy, rx;
+        divmod_small(local, w, qy, rx);
+        tx = rx0 + rx;
+        ty = ry0 + qy;
         keep = tile_survives(mx, my, ca, cb, cc, ia, ic, thr, __ldg(&rp->op), cfg.eps, tx, ty,
                              ptx, pty);
         if (!cfg.exact) keep = true;
