@@ -199,7 +199,8 @@ def run_reference(args):
     threads = host_threads()
     mode = parse_mode(args.mode)
     warm = min(args.warmup, 2)
-    cpu_view_rate(scene, cams, list(range(warm)), 1e9, threads, mode)   # bounded warmup
+    if warm:
+        cpu_view_rate(scene, cams, list(range(warm)), 1e9, threads, mode)   # bounded warmup
     # the views our arm times: rank 0's views after its warmup
     views = [(args.warmup + s) * args.gpus % len(cams) for s in range(args.steps)]
     rate, done, times, _ = cpu_view_rate(scene, cams, views, args.cpu_seconds, threads, mode)
