@@ -52,7 +52,7 @@ void plan(int64_t n, int32_t W, int32_t H, int64_t ecap, StpLayout& L) {
   L.partitions = (int32_t)((ecap + kSortTile - 1) / kSortTile);
   L.splat_record_bytes = (int32_t)sizeof(SplatRec);
   L.final_buffer = L.sort_passes & 1;
-  const int64_t nb = (n + kSortTile - 1) / kSortTile;
+  const int64_t nb = (n + kScanBlockItems - 1) / kScanBlockItems;  // K2 partials
   size_t o = 0;
   L.counters = o;     o = align_up(o + C_COUNT * 8);
   L.hist = o;         o = align_up(o + 8 * 256 * 4);

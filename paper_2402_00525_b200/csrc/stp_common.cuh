@@ -22,6 +22,7 @@ constexpr int kTile = 16;
 #define STP_SORT_ITEMS 16  // with the late look-back: C3 K4 0.342 vs 0.347 ms at 12 (profiles/r2ap)
 #endif
 constexpr int kSortPartition = 256 * STP_SORT_ITEMS;  // K4 entries per partition (256 threads)
+constexpr int kScanBlockItems = 256 * 16;             // K2 counts per scan block (partials)
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSmRing = 64;  // K6 per-SM tile ring slots (C_SMT)

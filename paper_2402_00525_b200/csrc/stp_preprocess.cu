@@ -835,6 +835,7 @@ __global__ void __launch_bounds__(kPreThreads) k_ingest(
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+static_assert(kScanTile == kScanBlockItems, "the workspace sizes the K2 partials by kScanBlockItems");
 
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -150,6 +150,24 @@ def test_workspace_layout(lib):
                                                     "scan_scratch"))
     offs = [o for o, _ in regions]
     assert len(set(offs)) == len(offs) and all(o % 256 == 0 for o in offs)
+    # every region holds what its kernels write: K2's block partials (one per
+    # 4096 counts, + 1), the per-Gaussian arrays, the ping-pong key buffers
+    size = {k: (regions[i + 1][0] if i + 1 < len(regions) else L.total) - o
+            for i, (o, k) in enumerate(regions)}
+    for nn in (1000, 4095, 4097, 3_000_000):
+        Ln = _lib.StpLayout()
+        bn = lib.stp_workspace_bytes(nn, W, H, 1000)
+        assert lib.stp_workspace_layout(nn, W, H, bn, ctypes.byref(Ln)) == _lib.STP_OK
+        rn = sorted((getattr(Ln, k), k) for k in ("recs", "camera", "masks", "state", "counts",
+                                                   "offsets", "keys0", "keys1", "vals", "ranges",
+                                                   "counters", "hist", "lookback",
+                                                   "scan_scratch"))
+        sz = {k: (rn[i + 1][0] if i + 1 < len(rn) else Ln.total) - o
+              for i, (o, k) in enumerate(rn)}
+        assert sz["scan_scratch"] >= ((nn + 4095) // 4096 + 1) * 4
+        assert sz["counts"] >= 4 * nn and sz["offsets"] >= 4 * nn
+        assert sz["keys0"] >= 8 * Ln.entry_capacity and sz["vals"] >= 4 * Ln.entry_capacity
+    assert size["recs"] >= 160 * n
     assert lib.stp_workspace_layout(n, W, H, 16, ctypes.byref(L)) == \
         _lib.STP_ERR_WORKSPACE_TOO_SMALL
     # 4K frame: 32,400 tiles -> 47-bit keys
