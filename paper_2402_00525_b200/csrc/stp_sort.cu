@@ -34,6 +34,9 @@ constexpr int kRadix = 256;
 #ifndef STP_SORT_LB_VEC
 #define STP_SORT_LB_VEC 4  // predecessors read per look-back step
 #endif
+#ifndef STP_TIE_PACK
+#define STP_TIE_PACK 1  // K5: a step's short tie runs packed into one round
+#endif
 #ifndef STP_SORT_BALLOT
 #define STP_SORT_BALLOT 1  // warp ranking by ballots instead of match.any (K4 0.410 -> 0.382 ms)
 #endif
@@ -468,6 +471,46 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
     // stable LSD sort delivered members in rank order, ids are ranks -- and
     // writes its id to the run's slot of that rank
     unsigned hb = __ballot_sync(kFull, short_head);
+#if STP_TIE_PACK
+    // the step's short runs packed whole into rounds of <= 32 lanes: every
+    // lane of a round computes one member's float64 depth (the record
+    // fetches of all packed runs overlap) and ranks it inside its run
+    while (hb) {
+      int64_t my_hi = 0;
+      int my_m = -1, my_L = 0, my_off = 0, my_t = 0, fill = 0;
+      while (hb) {
+        const int src = __ffs(hb) - 1;
+        const int hl = __shfl_sync(kFull, L, src);
+        if (fill + hl > 32) break;  // the next run starts the next round
+        hb &= hb - 1;
+        const int64_t hi = __shfl_sync(kFull, i, src);
+        const int ht = (int)__shfl_sync(kFull, tile, src);
+        if (lane >= fill && lane < fill + hl) {
+          my_hi = hi;
+          my_m = lane - fill;
+          my_L = hl;
+          my_off = fill;
+          my_t = ht;
+        }
+        fill += hl;
+      }
+      double d = INFINITY;
+      uint32_t im = 0xffffffffu;
+      if (my_m >= 0) {
+        im = (uint32_t)(keys[my_hi + my_m] & id_mask);
+        d = entry_depth64(recs, cam, im, my_t, gw, aux);
+      }
+      int rank = 0;
+      for (int m = 0; m < 32; ++m) {
+        const bool in_run = m < my_L;
+        const double od = __shfl_sync(kFull, d, (my_off + (in_run ? m : 0)) & 31);
+        const uint32_t oi = __shfl_sync(kFull, im, (my_off + (in_run ? m : 0)) & 31);
+        rank += in_run & ((od < d) | ((od == d) & (oi < im)));
+        if (!__any_sync(kFull, m + 1 < my_L)) break;
+      }
+      if (my_m >= 0) vals[my_hi + rank] = im;
+    }
+#else
     while (hb) {
       const int src = __ffs(hb) - 1;
       hb &= hb - 1;
@@ -488,6 +531,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
       }
       if (lane < hl) vals[hi + rank] = im;
     }
+#endif
   }
   const int nh = __syncthreads_count(heads > 0) ? block_sum(heads) : 0;
   if (threadIdx.x == 0 && nh) atomicAdd(counters + C_TILES, (unsigned long long)nh);
