@@ -948,6 +948,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t* __r
 // ---------------------------------------------------------------------------
 // K3 duplicate.
 
+#ifndef STP_K3_PREFETCH
+#define STP_K3_PREFETCH 0  // K3 0.1336 -> 0.1309 ms but the step 4.279 -> 4.288 ms (profiles/r2ax): off
+#endif
 // GZ: GlobalZ keys (view z from aux) -- a template parameter so the
 // hierarchical instantiation carries no GlobalZ code
 template <bool GZ>
@@ -964,6 +967,11 @@ __global__ void __launch_bounds__(kPreThreads) k_duplicate(
   const uint32_t cnt = (i < n) ? counts[i] : 0;
   int area = 0;
   if (cnt > 0) {
+#if STP_K3_PREFETCH
+    // the warp_expand rounds below read this record's two lines once per
+    // owner round: start pulling them into L2 now
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(recs + i));
+#endif
     const short4 rc = *reinterpret_cast<const short4*>(&recs[i].rx0);
     area = (rc.y - rc.x + 1) * (rc.w - rc.z + 1);
     // rects of <= 64 tiles: K1 left the survivors' positions in a mask, so
