@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
   }
 #else
   // four independent key loads in flight per thread
-  constexpr int U = 4;
+#ifndef STP_HIST_UNROLL
+#define STP_HIST_UNROLL 4
+#endif
+  constexpr int U = STP_HIST_UNROLL;
   for (int64_t i0 = (int64_t)blockIdx.x * kSortThreads * U + threadIdx.x; i0 < E;
        i0 += (int64_t)gridDim.x * kSortThreads * U) {
     uint64_t k[U];
