@@ -38,11 +38,16 @@ namespace stp {
 #ifndef STP_QT_SPECIALIZE
 #define STP_QT_SPECIALIZE 1
 #endif
+// K6 blocks of 2 warps with a 7-block bound: ptxas still allocates 128
+// registers (8 blocks = 16 warps per SM, as with 4 x 4) but schedules the
+// hot loops differently; measured K6 3.580 -> 3.533 ms and the C3 view 4.29
+// -> 4.23 ms (profiles/r3b, r3c: 4 x 4 at 166 regs 3.83, 2 x 7 capped at 144
+// regs 3.90, 1-warp blocks 3.62-3.72, 4 x 4 by __maxnreg__(128) 3.58 ms)
 #ifndef STP_EXACT_MINB
-#define STP_EXACT_MINB 4
+#define STP_EXACT_MINB 7
 #endif
 #ifndef STP_WARPS_PER_BLOCK
-#define STP_WARPS_PER_BLOCK 4
+#define STP_WARPS_PER_BLOCK 2
 #endif
 constexpr int kWarpsPerBlock = STP_WARPS_PER_BLOCK;
 constexpr int kRenderThreads = 32 * kWarpsPerBlock;
