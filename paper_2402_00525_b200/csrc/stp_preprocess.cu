@@ -17,12 +17,15 @@
 
 namespace stp {
 
-constexpr int kPreThreads = 256;
+#ifndef STP_PRE_THREADS
+#define STP_PRE_THREADS 64  // 64-thread K1/K3 blocks, 16 per SM: K1 0.284 -> 0.270 ms (profiles/r3h; 128: 0.275, 512: 0.309)
+#endif
+constexpr int kPreThreads = STP_PRE_THREADS;
 constexpr int kMaskTiles = 64;  // rects up to this many tiles carry a survivor mask (K1 -> K3)
 // masks[] value of a Gaussian K1 listed for the row kernels (rect > 64 tiles)
 constexpr unsigned long long kRowsListed = ~0ull;
 #ifndef STP_K1_MINB
-#define STP_K1_MINB 4  // 64 registers: 4 blocks per SM (measured K1 0.35 -> 0.33 ms)
+#define STP_K1_MINB (1024 / STP_PRE_THREADS)  // 64 registers, 32 warps per SM (measured K1 0.35 -> 0.33 ms at 256 x 4)
 #endif
 #ifndef STP_SPLIT_SH
 #define STP_SPLIT_SH 0

@@ -579,11 +579,14 @@ __device__ __forceinline__ int count_below(const Key* ad, const uint32_t* ai, in
 #define STP_RANK16 1  // batch order by all-pairs ranking (else a bitonic network)
 #endif
 #ifndef STP_RANK_UNROLL
-#define STP_RANK_UNROLL 4  // measured equal to 16, less code
+#define STP_RANK_UNROLL 8  // with the 2 x 7 K6 blocks: 8 + READY 12 K6 3.535 -> 3.519 ms (profiles/r3f)
 #endif
 constexpr int kRankUnroll = STP_RANK_UNROLL;
+#ifndef STP_SID_PF
+#define STP_SID_PF 0  // 1: load-phase bin entries one batch ahead (K6 3.525 vs 3.520 ms); 2: + L2 prefetch of their records (3.537): off (profiles/r3g)
+#endif
 #ifndef STP_READY
-#define STP_READY 16  // consume once every producing sub-tile has this many emits
+#define STP_READY 12  // consume once every producing sub-tile has this many emits (16 before the 2 x 7 blocks)
 #endif
 __host__ __device__ inline int ring_size(int qm) { return qm <= 16 ? STP_RING : 128; }
 __host__ __device__ inline bool tail_inplace(int qt) { return qt == 64; }
@@ -746,6 +749,11 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
     const uint2 rg = A.ranges[tile];
     const int start = (int)rg.x, k_total = (int)(rg.y - rg.x);
     const double r4y = (double)sy0;
+#if STP_SID_PF
+    // the next load batch's bin entries, one batch ahead (the record loads
+    // then wait on one global load instead of two dependent ones)
+    uint32_t pf_sid = lane < k_total ? __ldg(A.vals + start + lane) : 0u;
+#endif
     PROF_T0();
     PROF_ADD(5);
 
@@ -1034,8 +1042,19 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
         const int j = pos + lane;
         Key dA = kInfKey, dB = kInfKey;
         uint32_t iA = kNoId, iB = kNoId;
+#if STP_SID_PF
+        const uint32_t cur_sid = pf_sid;
+        if (j + 32 < k_total) pf_sid = __ldg(A.vals + start + j + 32);
+#if STP_SID_PF > 1
+        if (j + 32 < k_total) asm volatile("prefetch.global.L2 [%0];" ::"l"(A.recs + pf_sid));
+#endif
+#endif
         if (j < k_total) {
+#if STP_SID_PF
+          const uint32_t sid = cur_sid;
+#else
           const uint32_t sid = A.vals[start + j];
+#endif
           const SplatRec* r = A.recs + sid;
           double mx, my, a, b, ia, ic, thr, rect;
           ld256(&r->mx, mx, my, a, b);

@@ -37,6 +37,9 @@ constexpr int kRadix = 256;
 #ifndef STP_TIE_PACK
 #define STP_TIE_PACK 1  // K5: a step's short tie runs packed into one round
 #endif
+#ifndef STP_SORT_MINB
+#define STP_SORT_MINB 1  // k_onesweep min blocks per SM
+#endif
 #ifndef STP_SORT_BALLOT
 #define STP_SORT_BALLOT 1  // warp ranking by ballots instead of match.any (K4 0.410 -> 0.382 ms)
 #endif
@@ -170,7 +173,7 @@ __device__ __forceinline__ unsigned long long look_back(const unsigned long long
   }
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+__global__ void __launch_bounds__(kSortThreads, STP_SORT_MINB) k_onesweep(
     const uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
     const unsigned long long* counters, int64_t ecap, int shift,
     const uint32_t* __restrict__ hist, unsigned long long* lookback,
