@@ -43,6 +43,9 @@ namespace stp {
 // hot loops differently; measured K6 3.580 -> 3.533 ms and the C3 view 4.29
 // -> 4.23 ms (profiles/r3b, r3c: 4 x 4 at 166 regs 3.83, 2 x 7 capped at 144
 // regs 3.90, 1-warp blocks 3.62-3.72, 4 x 4 by __maxnreg__(128) 3.58 ms)
+#ifndef STP_HCOL_PF
+#define STP_HCOL_PF 0  // head queue: colour of H[0] loaded ahead of its blend
+#endif
 #ifndef STP_EXACT_MINB
 #define STP_EXACT_MINB 7
 #endif
@@ -147,6 +150,9 @@ struct Head {
   double a[QH];
   uint32_t id[QH];
   int n;
+#if STP_HCOL_PF
+  float c0, c1, c2;  // colour of H[0] once the queue is full (loaded ahead of its blend)
+#endif
 };
 
 // Extra per-blend work of a K6 instantiation (template int XM):
@@ -324,9 +330,16 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
 
 // blend of a live pixel (P.T >= term checked by the caller)
 template <int XM>
+__device__ __forceinline__ void blend_live_c(Pixel& P, const RenderArgs& A, double t, double al,
+                                             uint32_t id, float4 oc);
+template <int XM>
 __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double t, double al,
                                            uint32_t id) {
-  const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
+  blend_live_c<XM>(P, A, t, al, id, __ldg(reinterpret_cast<const float4*>(&A.recs[id].op)));
+}
+template <int XM>
+__device__ __forceinline__ void blend_live_c(Pixel& P, const RenderArgs& A, double t, double al,
+                                             uint32_t id, float4 oc) {
   const double w = al * P.T;
   const float wf = (float)w;
   P.C0 += oc.y * wf;
@@ -413,7 +426,15 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     bool c[QH];
 #pragma unroll
     for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
+#if STP_HCOL_PF
+    if (c[0]) {
+      blend_live<XM>(P, A, kdbl(t), al, id);
+      return;  // the queue is unchanged (R[i] = H[i] when c[0])
+    }
+    blend_live_c<XM>(P, A, kdbl(H.t[0]), H.a[0], H.id[0], make_float4(0.f, H.c0, H.c1, H.c2));
+#else
     blend_live<XM>(P, A, kdbl(c[0] ? t : H.t[0]), c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
+#endif
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
       const bool nx = i + 1 < QH;
@@ -423,6 +444,14 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
       H.a[i] = c[i] ? H.a[i] : (cn ? al : (nx ? H.a[j] : al));
       H.id[i] = c[i] ? H.id[i] : (cn ? id : (nx ? H.id[j] : id));
     }
+#if STP_HCOL_PF
+    {  // the new H[0]'s colour, needed at the next push onto the full queue
+      const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[H.id[0]].op));
+      H.c0 = oc.y;
+      H.c1 = oc.z;
+      H.c2 = oc.w;
+    }
+#endif
     return;
   }
   if (full) {
@@ -462,6 +491,14 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     xa = sw ? ha : xa;
     xi = sw ? hi : xi;
   }
+#if STP_HCOL_PF
+  if (EXACT && H.n == QH) {  // just filled: H[0]'s colour for the first overflow blend
+    const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[H.id[0]].op));
+    H.c0 = oc.y;
+    H.c1 = oc.z;
+    H.c2 = oc.w;
+  }
+#endif
 }
 
 // Bitonic sort of two (d, id) arrays, one pair per lane each, ascending.
@@ -582,6 +619,9 @@ __device__ __forceinline__ int count_below(const Key* ad, const uint32_t* ai, in
 #define STP_RANK_UNROLL 8  // with the 2 x 7 K6 blocks: 8 + READY 12 K6 3.535 -> 3.519 ms (profiles/r3f)
 #endif
 constexpr int kRankUnroll = STP_RANK_UNROLL;
+#ifndef STP_RING_PF
+#define STP_RING_PF 1  // pixel stage: ring ids one step ahead: K6 3.516 -> 3.453 ms (profiles/r3k)
+#endif
 #ifndef STP_SID_PF
 #define STP_SID_PF 0  // 1: load-phase bin entries one batch ahead (K6 3.525 vs 3.520 ms); 2: + L2 prefetch of their records (3.537): off (profiles/r3g)
 #endif
@@ -948,10 +988,25 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
 #ifndef STP_PIX_UNROLL
 #define STP_PIX_UNROLL 2
 #endif
+#if STP_RING_PF
+          // the next step's ring ids one step ahead (the record loads then
+          // start without waiting on the shared-memory load)
+          const int lim1 = max(min(pend, rounds) - 1, 0);
+          uint32_t nid[STP_PIX_UNROLL];
+#pragma unroll
+          for (int k = 0; k < STP_PIX_UNROLL; ++k) nid[k] = ring[(base + min(k, lim1)) & (R - 1)];
+#endif
           for (int e = 0; e < rounds; e += STP_PIX_UNROLL) {
             const int lim = min(pend, rounds);
             const bool live = P.T >= term;
             uint32_t ids[STP_PIX_UNROLL];
+#if STP_RING_PF
+#pragma unroll
+            for (int k = 0; k < STP_PIX_UNROLL; ++k) {
+              ids[k] = nid[k];
+              nid[k] = ring[(base + min(e + STP_PIX_UNROLL + k, lim1)) & (R - 1)];
+            }
+#endif
             double ts[STP_PIX_UNROLL], as[STP_PIX_UNROLL];
             bool ps[STP_PIX_UNROLL];
 #ifdef STP_WORK_STATS
@@ -963,7 +1018,9 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
 #pragma unroll
               for (int k = 0; k < STP_PIX_UNROLL; ++k) {
                 const bool vk = e + k < lim;
+#if !STP_RING_PF
                 ids[k] = ring[(base + e + (vk ? k : 0)) & (R - 1)];
+#endif
                 ps[k] = emit_eval_bf(P, A, ids[k], s_tab, ts[k], as[k]) & vk;
 #ifdef STP_WORK_STATS
                 evk[k] = vk;

@@ -38,7 +38,7 @@ constexpr int kRadix = 256;
 #define STP_TIE_PACK 1  // K5: a step's short tie runs packed into one round
 #endif
 #ifndef STP_SORT_MINB
-#define STP_SORT_MINB 1  // k_onesweep min blocks per SM
+#define STP_SORT_MINB 2  // k_onesweep min blocks per SM (1: 147 registers, K4 0.44 ms; 3: 80 registers with spills, K4 0.32 ms but the step 4.32 vs 4.22 ms, profiles/r3j)
 #endif
 #ifndef STP_SORT_BALLOT
 #define STP_SORT_BALLOT 1  // warp ranking by ballots instead of match.any (K4 0.410 -> 0.382 ms)
