@@ -44,7 +44,7 @@ namespace stp {
 // -> 4.23 ms (profiles/r3b, r3c: 4 x 4 at 166 regs 3.83, 2 x 7 capped at 144
 // regs 3.90, 1-warp blocks 3.62-3.72, 4 x 4 by __maxnreg__(128) 3.58 ms)
 #ifndef STP_HCOL_PF
-#define STP_HCOL_PF 0  // head queue: colour of H[0] loaded ahead of its blend
+#define STP_HCOL_PF 0  // head queue: colour of H[0] loaded ahead of its blend (K6 3.70 vs 3.45 ms: spills, profiles/r3m): off
 #endif
 #ifndef STP_EXACT_MINB
 #define STP_EXACT_MINB 7
@@ -620,7 +620,7 @@ __device__ __forceinline__ int count_below(const Key* ad, const uint32_t* ai, in
 #endif
 constexpr int kRankUnroll = STP_RANK_UNROLL;
 #ifndef STP_RING_PF
-#define STP_RING_PF 1  // pixel stage: ring ids one step ahead: K6 3.516 -> 3.453 ms (profiles/r3k)
+#define STP_RING_PF 1  // pixel stage: ring ids one step ahead: K6 3.516 -> 3.453 ms (profiles/r3k); 2: + L1 prefetch of those records, 3.50 ms (r3n)
 #endif
 #ifndef STP_SID_PF
 #define STP_SID_PF 0  // 1: load-phase bin entries one batch ahead (K6 3.525 vs 3.520 ms); 2: + L2 prefetch of their records (3.537): off (profiles/r3g)
@@ -1006,6 +1006,16 @@ __global__ void STP_K6_BOUNDS k_render(RenderArgs A) {
               ids[k] = nid[k];
               nid[k] = ring[(base + min(e + STP_PIX_UNROLL + k, lim1)) & (R - 1)];
             }
+#if STP_RING_PF > 1
+            if (e + STP_PIX_UNROLL < lim && live) {
+#pragma unroll
+              for (int k = 0; k < STP_PIX_UNROLL; ++k) {
+                const char* rp = reinterpret_cast<const char*>(A.recs + nid[k]);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + 96));
+              }
+            }
+#endif
 #endif
             double ts[STP_PIX_UNROLL], as[STP_PIX_UNROLL];
             bool ps[STP_PIX_UNROLL];
