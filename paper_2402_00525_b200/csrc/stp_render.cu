@@ -43,9 +43,6 @@ namespace stp {
 // hot loops differently; measured K6 3.580 -> 3.533 ms and the C3 view 4.29
 // -> 4.23 ms (profiles/r3b, r3c: 4 x 4 at 166 regs 3.83, 2 x 7 capped at 144
 // regs 3.90, 1-warp blocks 3.62-3.72, 4 x 4 by __maxnreg__(128) 3.58 ms)
-#ifndef STP_HCOL_PF
-#define STP_HCOL_PF 0  // head queue: colour of H[0] loaded ahead of its blend (K6 3.70 vs 3.45 ms: spills, profiles/r3m): off
-#endif
 #ifndef STP_EXACT_MINB
 #define STP_EXACT_MINB 7
 #endif
@@ -150,9 +147,6 @@ struct Head {
   double a[QH];
   uint32_t id[QH];
   int n;
-#if STP_HCOL_PF
-  float c0, c1, c2;  // colour of H[0] once the queue is full (loaded ahead of its blend)
-#endif
 };
 
 // Extra per-blend work of a K6 instantiation (template int XM):
@@ -330,16 +324,9 @@ __device__ __forceinline__ void blend(Pixel& P, const RenderArgs& A, double t, d
 
 // blend of a live pixel (P.T >= term checked by the caller)
 template <int XM>
-__device__ __forceinline__ void blend_live_c(Pixel& P, const RenderArgs& A, double t, double al,
-                                             uint32_t id, float4 oc);
-template <int XM>
 __device__ __forceinline__ void blend_live(Pixel& P, const RenderArgs& A, double t, double al,
                                            uint32_t id) {
-  blend_live_c<XM>(P, A, t, al, id, __ldg(reinterpret_cast<const float4*>(&A.recs[id].op)));
-}
-template <int XM>
-__device__ __forceinline__ void blend_live_c(Pixel& P, const RenderArgs& A, double t, double al,
-                                             uint32_t id, float4 oc) {
+  const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[id].op));
   const double w = al * P.T;
   const float wf = (float)w;
   P.C0 += oc.y * wf;
@@ -426,15 +413,7 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     bool c[QH];
 #pragma unroll
     for (int i = 0; i < QH; ++i) c[i] = lt(t, id, H.t[i], H.id[i]);
-#if STP_HCOL_PF
-    if (c[0]) {
-      blend_live<XM>(P, A, kdbl(t), al, id);
-      return;  // the queue is unchanged (R[i] = H[i] when c[0])
-    }
-    blend_live_c<XM>(P, A, kdbl(H.t[0]), H.a[0], H.id[0], make_float4(0.f, H.c0, H.c1, H.c2));
-#else
     blend_live<XM>(P, A, kdbl(c[0] ? t : H.t[0]), c[0] ? al : H.a[0], c[0] ? id : H.id[0]);
-#endif
 #pragma unroll
     for (int i = 0; i < QH; ++i) {
       const bool nx = i + 1 < QH;
@@ -444,14 +423,6 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
       H.a[i] = c[i] ? H.a[i] : (cn ? al : (nx ? H.a[j] : al));
       H.id[i] = c[i] ? H.id[i] : (cn ? id : (nx ? H.id[j] : id));
     }
-#if STP_HCOL_PF
-    {  // the new H[0]'s colour, needed at the next push onto the full queue
-      const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[H.id[0]].op));
-      H.c0 = oc.y;
-      H.c1 = oc.z;
-      H.c2 = oc.w;
-    }
-#endif
     return;
   }
   if (full) {
@@ -491,14 +462,6 @@ __device__ __forceinline__ void head_push(Pixel& P, Head<QH>& H, const RenderArg
     xa = sw ? ha : xa;
     xi = sw ? hi : xi;
   }
-#if STP_HCOL_PF
-  if (EXACT && H.n == QH) {  // just filled: H[0]'s colour for the first overflow blend
-    const float4 oc = __ldg(reinterpret_cast<const float4*>(&A.recs[H.id[0]].op));
-    H.c0 = oc.y;
-    H.c1 = oc.z;
-    H.c2 = oc.w;
-  }
-#endif
 }
 
 // Bitonic sort of two (d, id) arrays, one pair per lane each, ascending.
